@@ -1,0 +1,246 @@
+/*
+ * batmap.h -- C ABI of the B200-native BatMap all-pairs support counting library.
+ *
+ * The hot path of Amossen & Pagh, "A New Data Layout For Set Intersection on GPUs"
+ * (arXiv 1102.1003; cited as P:<line> of /root/reference/PAPER.md):
+ *
+ *   vertical tidlists S_i
+ *     --batmap_build-->          one BatMap per item: 2-of-3 cuckoo placement,
+ *                                superblock layout, 8-bit entries with the
+ *                                indicator bit as MSB, ⊥ = 0x7F
+ *     --batmap_pair_supports-->  every selected pair intersected word by word with the
+ *                                wrap-around SWAR compare-and-count (P:218-234, P:273-274,
+ *                                P:423-431), failed insertions corrected, and
+ *                                the pairs with support >= threshold emitted
+ *
+ * Conventions
+ *   - Plain C types only.  Pointers are marked [device] (CUDA global memory) or [host].
+ *   - Item ids are the caller's ids 0..n_items-1 (the row index of the input CSR);
+ *     transaction ids are 0-based, 0 <= tid < n_transactions (reading #2).
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream).  Calls that return a count (build, pair_supports) synchronise `stream`
+ *     once to read it; all other device work stays asynchronous.
+ *   - No C++ exception crosses the ABI.  On a non-OK status, batmap_last_error()
+ *     returns a thread-local message.  A handle may be used by one thread at a time.
+ *   - Out-of-memory is reported as BATMAP_E_NOMEM, CUDA runtime failures as
+ *     BATMAP_E_CUDA.  After BATMAP_E_CUDA the handle must only be destroyed.
+ */
+#ifndef BATMAP_H_
+#define BATMAP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BATMAP_OK = 0,
+    BATMAP_E_INVALID = -1,   /* bad argument or input (see each function)            */
+    BATMAP_E_NOMEM = -2,     /* device or host allocation failed                     */
+    BATMAP_E_CUDA = -3,      /* CUDA runtime error; details in batmap_last_error()   */
+    BATMAP_E_CAPACITY = -4,  /* output buffer too small; *n_out holds the size needed */
+    BATMAP_E_OVERFLOW = -5   /* n_transactions >= 2^31, n_items >= 2^31, size overflow */
+} batmap_status;
+
+typedef struct CUstream_st* batmap_stream_t;   /* == cudaStream_t */
+typedef struct batmap_collection* batmap_handle; /* library-owned; free with batmap_destroy */
+
+/* Build flags */
+#define BATMAP_CHECK_INPUT 0x1u  /* validate on device: every tidlist strictly increasing, 0 <= tid < m */
+
+/* pair_supports flags (batmap_pair_supports_ex) */
+#define BATMAP_PAIRS_RAW 0x1u      /* test hook: emit the raw BatMap counts (no failure corrections) */
+#define BATMAP_PAIRS_SIMPLE 0x2u   /* test hook: use the one-thread-per-pair kernel (cross-check)    */
+
+/*
+ * Build options.  Zero-initialised = defaults.
+ *   seed      seeds the three permutations π_1..π_3 (reading #3).
+ *   r_min     floor on every table range r_i; power of two >= 4.  0 => 128.  With r_min
+ *             >= 128 every BatMap is a multiple of 32 words, which the tiled intersection
+ *             kernel requires; smaller values fall back to the simple kernel.
+ *   max_loop  MaxLoop rounds of INSERT.  0 => 16 + ceil(3 log2 r_i).
+ *   flags     BATMAP_CHECK_INPUT.
+ *   pi_table  [device] test hook: 3 x U uint32 table replacing the mixer (row t-1 = π_t),
+ *             each row a permutation of [0, U), U = 127 * 2^s.  NULL => seeded mixer.
+ *             Read during batmap_build only.
+ */
+typedef struct {
+    uint64_t seed;
+    uint32_t r_min;
+    uint32_t max_loop;
+    uint32_t flags;
+    uint32_t reserved;
+    const uint32_t* pi_table;
+} batmap_build_opts;
+
+/* One output record: i < j in caller ids; support = |S_i ∩ S_j|. */
+typedef struct {
+    uint32_t i, j, support;
+} batmap_triple;
+
+typedef struct {
+    int32_t s_shift;      /* s: entries store π_t(x) >> s                 */
+    int32_t n_classes;    /* distinct table ranges r among the items             */
+    int64_t U;            /* permutation domain 127 * 2^s                        */
+    int64_t r0;           /* min_i r_i (|B_0| = 3 r0)                     */
+    int64_t n_items;
+    int64_t n_transactions;
+    int64_t arena_bytes;  /* sum_i 3 r_i (the BatMaps, without padding)          */
+    int64_t n_failures;   /* |F|: (item, tid) insertions that failed */
+    int64_t n_failed_tids;/* distinct transactions b with F_b non-empty          */
+} batmap_info_t;
+
+/*
+ * batmap_build -- construct the BatMap of every item.
+ *   offsets   [device] int64[n_items+1], offsets[0] = 0, non-decreasing: item i's tidlist
+ *             is tids[offsets[i] .. offsets[i+1]).
+ *   tids      [device] int32[offsets[n_items]]: each tidlist strictly increasing,
+ *             0 <= tid < n_transactions (validated only with BATMAP_CHECK_INPUT).
+ *   n_items, n_transactions   n and m; 1 <= m < 2^31, 0 <= n < 2^31.
+ *   opts      [host] may be NULL (defaults).
+ *   out       [host] receives the handle.
+ * The handle owns the BatMaps (HBM), the failure list F, per-item failure counts and
+ * the item lists A_b of failed transactions.  The input CSR is read during the
+ * call only and may be freed once `stream` has completed this call's work.
+ * Errors: E_INVALID (null pointer, bad offsets, r_min not a power of two >= 4, invalid
+ * tidlists in checked mode), E_OVERFLOW, E_NOMEM, E_CUDA.
+ */
+batmap_status batmap_build(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                           int64_t n_transactions, const batmap_build_opts* opts,
+                           batmap_stream_t stream, batmap_handle* out);
+
+/*
+ * batmap_pair_supports -- all pairs {i, j} of the selected items with
+ * |S_i ∩ S_j| >= threshold, as triples (i < j, caller ids) sorted by (i, j).
+ *   items     [device] int32[n_sel] distinct caller ids, or NULL => all items.
+ *   threshold emit iff support >= threshold (inclusive); 0 => every pair,
+ *             including zero supports.
+ *   out       [device] caller-owned, capacity records.
+ *   n_out     [host] number of records; also set on E_CAPACITY (the size needed).
+ * On E_CAPACITY the computed result is kept in the handle: an immediately following
+ * call with the same arguments (same items pointer and contents) and enough capacity
+ * returns it without recomputation.
+ * Errors: E_INVALID (null handle/out/n_out, duplicate or out-of-range items),
+ * E_CAPACITY, E_NOMEM, E_CUDA.
+ */
+batmap_status batmap_pair_supports(batmap_handle h, const int32_t* items, int64_t n_sel,
+                                   uint32_t threshold, batmap_triple* out, int64_t capacity,
+                                   int64_t* n_out, batmap_stream_t stream);
+
+/*
+ * batmap_pair_supports_part -- the share of rank `part` (0 <= part < n_parts) of the
+ * pairs of batmap_pair_supports: the work tiles of the pair triangle are
+ * ordered by cost and dealt round-robin to the parts, so the union over parts is
+ * exactly the full result and the parts are disjoint.  Output sorted by (i, j).
+ */
+batmap_status batmap_pair_supports_part(batmap_handle h, const int32_t* items, int64_t n_sel,
+                                        uint32_t threshold, int32_t part, int32_t n_parts,
+                                        batmap_triple* out, int64_t capacity, int64_t* n_out,
+                                        batmap_stream_t stream);
+
+/* General form: flags = BATMAP_PAIRS_RAW | BATMAP_PAIRS_SIMPLE (test hooks), else 0. */
+batmap_status batmap_pair_supports_ex(batmap_handle h, const int32_t* items, int64_t n_sel,
+                                      uint32_t threshold, int32_t part, int32_t n_parts,
+                                      uint32_t flags, batmap_triple* out, int64_t capacity,
+                                      int64_t* n_out, batmap_stream_t stream);
+
+/* batmap_info -- parameters of a built collection.  info [host].  E_INVALID on NULL. */
+batmap_status batmap_info(batmap_handle h, batmap_info_t* info);
+
+/* batmap_destroy -- release everything the handle owns (stream-ordered).  NULL is a no-op. */
+void batmap_destroy(batmap_handle h);
+
+/* batmap_last_error -- thread-local message for the last non-OK status ("" if none). */
+const char* batmap_last_error(void);
+
+/* batmap_version -- library version string. */
+const char* batmap_version(void);
+
+/*
+ * batmap_mine_host -- end-to-end call on HOST buffers: copies the CSR to the device,
+ * builds, computes the pairs, copies the triples back and frees the device state.
+ *   offsets, tids, items [host] as in batmap_build / batmap_pair_supports (items may be NULL).
+ *   out [host] capacity records; n_out [host] (set also on E_CAPACITY).
+ */
+batmap_status batmap_mine_host(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                               int64_t n_transactions, const batmap_build_opts* opts,
+                               const int32_t* items, int64_t n_sel, uint32_t threshold,
+                               batmap_triple* out, int64_t capacity, int64_t* n_out,
+                               batmap_stream_t stream);
+
+/*
+ * batmap_stats -- measurements of the last batmap_build and batmap_pair_supports* calls on
+ * this handle.  Device times come from CUDA events recorded on the launching stream around
+ * each phase.  word_compares is the algorithmic work of the intersection:
+ * the sum over the selected pairs of this part of max(W_i, W_j), W = 3r/4 words;
+ * tile_compares is what the kernel executed (tile padding and diagonal tiles included).
+ * launches_* count the kernels this library launched (its own and its CUB sorts/scans).
+ */
+typedef struct {
+    double build_ms;        /* batmap_build, device time of all its work                 */
+    double k1_insert_ms;    /* ★K1 cuckoo insertion kernel                                */
+    double k1_encode_ms;    /* ★K1 encode kernel(s)                                       */
+    double pairs_ms;        /* batmap_pair_supports*, device time of all its work         */
+    double k2_ms;           /* ★K2 intersection kernel (one launch)                       */
+    double k3_ms;           /* ★K3 correction + sort                                      */
+    int64_t word_compares;
+    int64_t tile_compares;
+    int64_t n_candidates;   /* K2 epilogue candidates (c + f_i + f_j >= threshold)        */
+    int64_t n_results;
+    int32_t k2_kind;        /* 1 = tiled TMA kernel, 2 = one-thread-per-pair kernel        */
+    int32_t k2_grid;        /* CTAs launched for K2                                        */
+    int64_t launches_build;
+    int64_t launches_pairs;
+} batmap_stats_t;
+
+batmap_status batmap_stats(batmap_handle h, batmap_stats_t* out);
+
+/*
+ * batmap_sort_triples -- sort triples in place by (i, j) on the device (used to merge the
+ * parts gathered from several ranks).  triples [device] n records.
+ */
+batmap_status batmap_sort_triples(batmap_triple* triples, int64_t n, batmap_stream_t stream);
+
+/* ---------------------------------------------------------------- inspection / test hooks */
+
+/*
+ * batmap_export_entries -- the 3 r_i entry bytes of item `item` in entry order
+ * e = 0 .. 3 r_i - 1 (superblock layout P:378-379, 4 entries per little-endian word).
+ *   out [host] capacity bytes; r_out [host] receives r_i.  E_CAPACITY if capacity < 3 r_i.
+ */
+batmap_status batmap_export_entries(batmap_handle h, int32_t item, uint8_t* out,
+                                    int64_t capacity, int64_t* r_out);
+
+/*
+ * batmap_export_failures -- F as (item, tid) pairs sorted by (item, tid).
+ *   items, tids [host] capacity entries each; n_out [host].  E_CAPACITY if too small.
+ */
+batmap_status batmap_export_failures(batmap_handle h, int32_t* items, int32_t* tids,
+                                     int64_t capacity, int64_t* n_out);
+
+/*
+ * batmap_swar_device -- runs the device compare routines on word pairs:
+ *   out[k]     = matches of (x[k], y[k]) by the intersection kernel's 4-instruction form,
+ *   out[n + k] = matches by the paper's literal formula.
+ *   x, y [device] uint32[n]; out [device] uint32[2n].
+ */
+batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n, uint32_t* out,
+                                 batmap_stream_t stream);
+
+/*
+ * batmap_plan_tiles -- host-only view of the intersection planner.  For width classes
+ * a = 0..n_classes-1 with class_n[a] items of class_w[a] words (class_w ascending),
+ * lists the tiles (a, b, ti, tj) of the pair triangle (a <= b; tj >= ti when a == b)
+ * assigned to `part` of `n_parts`, in execution order, and their total estimated work
+ * (word compares incl. padding).  tiles [host] 4*capacity int32; n_tiles, work [host].
+ * tile_m: tile edge in items (0 => the kernel's 128).
+ */
+batmap_status batmap_plan_tiles(int32_t n_classes, const int64_t* class_n, const int64_t* class_w,
+                                int32_t tile_m, int32_t part, int32_t n_parts, int32_t* tiles,
+                                int64_t capacity, int64_t* n_tiles, int64_t* work);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BATMAP_H_ */

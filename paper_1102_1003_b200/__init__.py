@@ -1,0 +1,15 @@
+"""B200-native BatMap all-pairs support counting (Amossen & Pagh, arXiv 1102.1003).
+
+The product is the C-ABI library ``libbatmap.so`` (include/batmap.h); this package is
+its thin binding (``batmap``), the multi-GPU gather (``dist``) and the build script.
+"""
+from .batmap import (  # noqa: F401
+    BatMapError,
+    Collection,
+    load_library,
+    mine_host,
+    plan_tiles,
+    sort_triples,
+    swar_device,
+    version,
+)

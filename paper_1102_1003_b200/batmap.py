@@ -1,0 +1,289 @@
+"""Thin Python binding of include/batmap.h (argument marshalling only).
+
+Every step of the hot path runs in libbatmap.so's CUDA kernels; torch provides device
+memory and the current stream.  There is no CPU fallback: if the extension is missing
+or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbatmap.so")
+
+BATMAP_OK = 0
+BATMAP_E_INVALID = -1
+BATMAP_E_NOMEM = -2
+BATMAP_E_CUDA = -3
+BATMAP_E_CAPACITY = -4
+BATMAP_E_OVERFLOW = -5
+_NAMES = {0: "OK", -1: "E_INVALID", -2: "E_NOMEM", -3: "E_CUDA", -4: "E_CAPACITY", -5: "E_OVERFLOW"}
+
+BATMAP_CHECK_INPUT = 0x1
+BATMAP_PAIRS_RAW = 0x1
+BATMAP_PAIRS_SIMPLE = 0x2
+
+
+class BatMapError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"batmap {_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class BuildOpts(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("r_min", ctypes.c_uint32), ("max_loop", ctypes.c_uint32),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("pi_table", ctypes.c_void_p)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("build_ms", ctypes.c_double), ("k1_insert_ms", ctypes.c_double), ("k1_encode_ms", ctypes.c_double),
+                ("pairs_ms", ctypes.c_double), ("k2_ms", ctypes.c_double), ("k3_ms", ctypes.c_double),
+                ("word_compares", ctypes.c_int64), ("tile_compares", ctypes.c_int64),
+                ("n_candidates", ctypes.c_int64), ("n_results", ctypes.c_int64), ("k2_kind", ctypes.c_int32),
+                ("k2_grid", ctypes.c_int32), ("launches_build", ctypes.c_int64), ("launches_pairs", ctypes.c_int64)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("s_shift", ctypes.c_int32), ("n_classes", ctypes.c_int32), ("U", ctypes.c_int64),
+                ("r0", ctypes.c_int64), ("n_items", ctypes.c_int64), ("n_transactions", ctypes.c_int64),
+                ("arena_bytes", ctypes.c_int64), ("n_failures", ctypes.c_int64), ("n_failed_tids", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libbatmap.so (built by paper_1102_1003_b200.build_ext); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"CUDA extension not built: {LIB_PATH} is missing "
+                           "(run `python -m paper_1102_1003_b200.build_ext`); there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, U32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+    PI64 = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "batmap_build": ([P, P, I64, I64, ctypes.POINTER(BuildOpts), P, ctypes.POINTER(P)], ctypes.c_int),
+        "batmap_pair_supports": ([P, P, I64, U32, P, I64, PI64, P], ctypes.c_int),
+        "batmap_pair_supports_part": ([P, P, I64, U32, I32, I32, P, I64, PI64, P], ctypes.c_int),
+        "batmap_pair_supports_ex": ([P, P, I64, U32, I32, I32, U32, P, I64, PI64, P], ctypes.c_int),
+        "batmap_info": ([P, ctypes.POINTER(Info)], ctypes.c_int),
+        "batmap_destroy": ([P], None),
+        "batmap_last_error": ([], ctypes.c_char_p),
+        "batmap_version": ([], ctypes.c_char_p),
+        "batmap_mine_host": ([P, P, I64, I64, ctypes.POINTER(BuildOpts), P, I64, U32, P, I64, PI64, P], ctypes.c_int),
+        "batmap_export_entries": ([P, I32, P, I64, PI64], ctypes.c_int),
+        "batmap_export_failures": ([P, P, P, I64, PI64], ctypes.c_int),
+        "batmap_swar_device": ([P, P, I64, P, P], ctypes.c_int),
+        "batmap_plan_tiles": ([I32, P, P, I32, I32, I32, P, I64, PI64, PI64], ctypes.c_int),
+        "batmap_stats": ([P, ctypes.POINTER(Stats)], ctypes.c_int),
+        "batmap_sort_triples": ([P, I64, P], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, ok=(BATMAP_OK,)):
+    if rc not in ok:
+        raise BatMapError(rc, load_library().batmap_last_error().decode())
+    return rc
+
+
+def version() -> str:
+    return load_library().batmap_version().decode()
+
+
+def _stream_ptr(stream):
+    import torch
+
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _opts(seed, r_min, max_loop, check, pi_table):
+    o = BuildOpts()
+    o.seed = int(seed) & (2 ** 64 - 1)
+    o.r_min = int(r_min)
+    o.max_loop = int(max_loop)
+    o.flags = BATMAP_CHECK_INPUT if check else 0
+    o.pi_table = pi_table.data_ptr() if pi_table is not None else None
+    return o
+
+
+class Collection:
+    """The BatMaps of one instance on the current CUDA device (batmap_build)."""
+
+    def __init__(self, offsets, tids, n_transactions: int, *, seed: int = 0, r_min: int = 128,
+                 max_loop: int = 0, check: bool = False, pi_table=None, stream=None):
+        import torch
+
+        lib = load_library()
+        if not (offsets.is_cuda and tids.is_cuda):
+            raise ValueError("offsets and tids must be CUDA tensors")
+        self._offsets = offsets.contiguous().to(torch.int64)
+        self._tids = tids.contiguous().to(torch.int32)
+        self._pi = pi_table.contiguous().to(torch.int32) if pi_table is not None else None
+        self.n_items = self._offsets.numel() - 1
+        self.m = int(n_transactions)
+        self._stream = stream
+        opts = _opts(seed, r_min, max_loop, check, self._pi)
+        h = ctypes.c_void_p()
+        _check(lib.batmap_build(_dptr(self._offsets), _dptr(self._tids), self.n_items, self.m,
+                                ctypes.byref(opts), _stream_ptr(stream), ctypes.byref(h)))
+        self._h = h
+        self._last_k = 1 << 16
+        # the input CSR is not retained by the library
+        self._offsets = self._tids = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().batmap_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def info(self) -> dict:
+        inf = Info()
+        _check(load_library().batmap_info(self._h, ctypes.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in Info._fields_}
+
+    def stats(self) -> dict:
+        """Event-timed phases and work counts of the last build / pair_supports (batmap_stats)."""
+        st = Stats()
+        _check(load_library().batmap_stats(self._h, ctypes.byref(st)))
+        return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+    def pair_supports(self, items=None, threshold: int = 1, *, part: int = 0, n_parts: int = 1,
+                      raw: bool = False, simple: bool = False, stream=None):
+        """int32 tensor [K, 3] of (i, j, support), i < j, support >= threshold, sorted by (i, j)."""
+        import torch
+
+        lib = load_library()
+        flags = (BATMAP_PAIRS_RAW if raw else 0) | (BATMAP_PAIRS_SIMPLE if simple else 0)
+        it = None
+        n_sel = 0
+        if items is not None:
+            it = items if (hasattr(items, "is_cuda") and items.is_cuda) else torch.as_tensor(np.asarray(items))
+            it = it.to(device="cuda", dtype=torch.int32).contiguous()
+            n_sel = it.numel()
+        st = _stream_ptr(stream if stream is not None else self._stream)
+        n_out = ctypes.c_int64(0)
+        cap = max(1, self._last_k)
+        out = torch.empty((cap, 3), dtype=torch.int32, device="cuda")
+        rc = lib.batmap_pair_supports_ex(self._h, _dptr(it), n_sel, int(threshold), part, n_parts, flags,
+                                         _dptr(out), cap, ctypes.byref(n_out), st)
+        if rc == BATMAP_E_CAPACITY:
+            cap = int(n_out.value)
+            out = torch.empty((max(cap, 1), 3), dtype=torch.int32, device="cuda")
+            rc = lib.batmap_pair_supports_ex(self._h, _dptr(it), n_sel, int(threshold), part, n_parts, flags,
+                                             _dptr(out), cap, ctypes.byref(n_out), st)
+        _check(rc)
+        k = int(n_out.value)
+        self._last_k = max(k, 1)
+        return out[:k]
+
+    def export_entries(self, item: int) -> np.ndarray:
+        """Entry bytes of item's BatMap in entry order (3 r bytes)."""
+        lib = load_library()
+        r = ctypes.c_int64(0)
+        cap = 0
+        rc = lib.batmap_export_entries(self._h, int(item), ctypes.c_void_p(1), cap, ctypes.byref(r))
+        _check(rc, ok=(BATMAP_OK, BATMAP_E_CAPACITY))
+        buf = np.empty(3 * r.value, dtype=np.uint8)
+        _check(lib.batmap_export_entries(self._h, int(item), buf.ctypes.data_as(ctypes.c_void_p), buf.size,
+                                         ctypes.byref(r)))
+        return buf
+
+    def failures(self) -> np.ndarray:
+        """F as an int32 array [F, 2] of (item, tid), sorted."""
+        lib = load_library()
+        n = ctypes.c_int64(0)
+        rc = lib.batmap_export_failures(self._h, None, None, 0, ctypes.byref(n))
+        _check(rc, ok=(BATMAP_OK, BATMAP_E_CAPACITY))
+        items = np.empty(max(n.value, 1), np.int32)
+        tids = np.empty(max(n.value, 1), np.int32)
+        _check(lib.batmap_export_failures(self._h, items.ctypes.data_as(ctypes.c_void_p),
+                                          tids.ctypes.data_as(ctypes.c_void_p), items.size, ctypes.byref(n)))
+        return np.stack([items[: n.value], tids[: n.value]], axis=1)
+
+
+def mine_host(offsets, tids, n_transactions: int, items=None, threshold: int = 1, *, seed: int = 0,
+              r_min: int = 128, max_loop: int = 0, capacity: int | None = None, stream=None) -> np.ndarray:
+    """End to end on host arrays (batmap_mine_host): returns uint32 [K, 3]."""
+    lib = load_library()
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    tids = np.ascontiguousarray(tids, dtype=np.int32)
+    it = None if items is None else np.ascontiguousarray(items, dtype=np.int32)
+    opts = _opts(seed, r_min, max_loop, False, None)
+    cap = int(capacity) if capacity is not None else 1 << 16
+    n_out = ctypes.c_int64(0)
+    st = _stream_ptr(stream)
+    for _ in range(2):
+        out = np.empty((max(cap, 1), 3), dtype=np.uint32)
+        rc = lib.batmap_mine_host(offsets.ctypes.data_as(ctypes.c_void_p), tids.ctypes.data_as(ctypes.c_void_p),
+                                  offsets.shape[0] - 1, int(n_transactions), ctypes.byref(opts),
+                                  None if it is None else it.ctypes.data_as(ctypes.c_void_p),
+                                  0 if it is None else it.shape[0], int(threshold),
+                                  out.ctypes.data_as(ctypes.c_void_p), cap, ctypes.byref(n_out), st)
+        if rc != BATMAP_E_CAPACITY:
+            break
+        cap = int(n_out.value)
+    _check(rc)
+    return out[: n_out.value]
+
+
+def sort_triples(t, stream=None):
+    """Sort an int32 [K, 3] CUDA tensor of triples in place by (i, j) (batmap_sort_triples)."""
+    t = t.contiguous()
+    _check(load_library().batmap_sort_triples(_dptr(t), t.shape[0], _stream_ptr(stream)))
+    return t
+
+
+def swar_device(x, y, stream=None):
+    """(kernel form, paper form) match counts of word pairs, computed on the device."""
+    import torch
+
+    x = x.to(device="cuda", dtype=torch.int32).contiguous()
+    y = y.to(device="cuda", dtype=torch.int32).contiguous()
+    n = x.numel()
+    out = torch.empty(2 * max(n, 1), dtype=torch.int32, device="cuda")
+    _check(load_library().batmap_swar_device(_dptr(x), _dptr(y), n, _dptr(out), _stream_ptr(stream)))
+    return out[:n], out[n:2 * n]
+
+
+def plan_tiles(class_n, class_w, part: int = 0, n_parts: int = 1, tile_m: int = 0):
+    """Host-only planner view: (tiles int32 [T, 4] as (a, b, ti, tj), total work)."""
+    lib = load_library()
+    cn = np.ascontiguousarray(class_n, dtype=np.int64)
+    cw = np.ascontiguousarray(class_w, dtype=np.int64)
+    nt, work = ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = lib.batmap_plan_tiles(cn.shape[0], cn.ctypes.data_as(ctypes.c_void_p), cw.ctypes.data_as(ctypes.c_void_p),
+                               tile_m, part, n_parts, None, 0, ctypes.byref(nt), ctypes.byref(work))
+    _check(rc, ok=(BATMAP_OK, BATMAP_E_CAPACITY))
+    tiles = np.empty((max(nt.value, 1), 4), dtype=np.int32)
+    _check(lib.batmap_plan_tiles(cn.shape[0], cn.ctypes.data_as(ctypes.c_void_p), cw.ctypes.data_as(ctypes.c_void_p),
+                                 tile_m, part, n_parts, tiles.ctypes.data_as(ctypes.c_void_p), nt.value,
+                                 ctypes.byref(nt), ctypes.byref(work)))
+    return tiles[: nt.value], int(work.value)

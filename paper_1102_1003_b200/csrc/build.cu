@@ -1,0 +1,472 @@
+// build.cu -- ★K1: BatMap construction.
+//
+// Per item (width-sorted position), one thread runs the paper's generalized cuckoo
+// INSERT twice per element in ascending tid order (reading #10) on a working
+// table of raw tids, handles failures per P:309-310 / reading #9 and records them in F.
+// A second kernel encodes each table entry as (b << 7) | (π_t(x) >> s), with
+// b from the partner table (Fig. 5, reading #6) and ⊥ = 0x7F (reading #1), and writes the
+// words into the class-blocked, word-major arena the intersection kernel reads.
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace bm {
+
+// ------------------------------------------------------------------ device: INSERT
+__device__ __forceinline__ uint32_t insert_one(uint32_t* A, uint32_t tau, const PiParams& P,
+                                               uint32_t r, uint32_t r0, int log2r0,
+                                               uint32_t max_loop) {
+    for (uint32_t l = 0; l < max_loop; ++l) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            uint32_t q = slot_of(t, pi_eval(P, t, tau), r, r0, log2r0);
+            uint32_t old = A[q];
+            A[q] = tau;  // τ <-> A_t[h_t(τ)]
+            tau = old;
+            if (tau == kEmpty) return kEmpty;
+        }
+    }
+    return tau;  // nestless element after MaxLoop rounds
+}
+
+__device__ __forceinline__ void delete_all(uint32_t* A, uint32_t x, const PiParams& P, uint32_t r,
+                                           uint32_t r0, int log2r0) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        uint32_t q = slot_of(t, pi_eval(P, t, x), r, r0, log2r0);
+        if (A[q] == x) A[q] = kEmpty;
+    }
+}
+
+__global__ void __launch_bounds__(128) k1_insert(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
+    const int32_t* __restrict__ pos2orig, const int64_t* __restrict__ work_off,
+    const uint8_t* __restrict__ log2r, int64_t n, PiParams P, uint32_t r0, int log2r0,
+    uint32_t max_loop_opt, uint32_t* __restrict__ work, int32_t* __restrict__ fcount,
+    uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr, int64_t fail_cap) {
+    int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= n) return;
+    const int orig = pos2orig[pos];
+    const int64_t b = offsets[orig], e = offsets[orig + 1];
+    const int lr = log2r[pos];
+    const uint32_t r = 1u << lr;
+    const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)lr;
+    uint32_t* A = work + work_off[pos];
+    int nf = 0;
+    for (int64_t k = b; k < e; ++k) {
+        const uint32_t x = (uint32_t)__ldg(tids + k);
+        uint32_t y = insert_one(A, x, P, r, r0, log2r0, max_loop);  // first copy
+        if (y == kEmpty) y = insert_one(A, x, P, r, r0, log2r0, max_loop);  // second copy
+        if (y == kEmpty) continue;
+        // delete any occurrences of x, re-insert the nestless element unless it is x;
+        // a failing re-insertion is handled the same way (reading #9).
+        uint32_t cur = x, nest = y;
+        while (true) {
+            delete_all(A, cur, P, r, r0, log2r0);
+            unsigned long long idx = atomicAdd(fail_ctr, 1ull);
+            if ((int64_t)idx < fail_cap) fails[idx] = ((uint64_t)pos << 32) | cur;
+            ++nf;
+            if (nest == cur) break;
+            uint32_t z = insert_one(A, nest, P, r, r0, log2r0, max_loop);
+            if (z == kEmpty) break;
+            cur = nest;
+            nest = z;
+        }
+    }
+    fcount[pos] = nf;
+}
+
+// Encode one class: thread per (word w, column c); writes arena_cls[w * n_pad + c].
+__global__ void __launch_bounds__(256) k1_encode(
+    const uint32_t* __restrict__ work, const int64_t* __restrict__ work_off, int64_t first, int n,
+    int n_pad, int W, uint32_t r, PiParams P, uint32_t r0, int log2r0,
+    uint32_t* __restrict__ arena_cls) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)W * n_pad) return;
+    const int w = (int)(idx / n_pad);
+    const int c = (int)(idx - (int64_t)w * n_pad);
+    if (c >= n) {
+        arena_cls[idx] = kNullWord;
+        return;
+    }
+    const uint32_t* A = work + work_off[first + c];
+    const uint4 q4 = *reinterpret_cast<const uint4*>(A + 4 * (int64_t)w);
+    const uint32_t xs[4] = {q4.x, q4.y, q4.z, q4.w};
+    uint32_t word = 0;
+    const uint32_t sb = 3u * r0;
+#pragma unroll
+    for (int lane = 0; lane < 4; ++lane) {
+        const uint32_t x = xs[lane];
+        uint32_t byte = kNullByte;
+        if (x != kEmpty) {
+            const uint32_t q = 4u * (uint32_t)w + lane;
+            const int t = (int)((q % sb) >> log2r0);  // table of entry q
+            const uint32_t code = pi_eval(P, t, x) >> P.s;  // 7 MSBs of π_t(x)
+            const int t1 = (t + 1) % 3;
+            const uint32_t q1 = slot_of(t1, pi_eval(P, t1, x), r, r0, log2r0);
+            // partner in the following table => this copy precedes it => b = 0;
+            // otherwise the partner is in the preceding table => b = 1  (Fig. 5)
+            const uint32_t bit = (A[q1] == x) ? 0u : 1u;
+            byte = (bit << 7) | code;
+        }
+        word |= byte << (8 * lane);  // little-endian lanes (reading #17)
+    }
+    arena_cls[idx] = word;
+}
+
+__global__ void k1_check(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
+                         int64_t n, int64_t m, int* __restrict__ bad) {
+    int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    int lane = threadIdx.x & 31;
+    if (item >= n) return;
+    int64_t b = offsets[item], e = offsets[item + 1];
+    for (int64_t k = b + lane; k < e; k += 32) {
+        int32_t t = tids[k];
+        if (t < 0 || t >= m || (k > b && tids[k - 1] >= t)) atomicOr(bad, 1);
+    }
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+__global__ void k_fail_split(const uint64_t* __restrict__ keys, int64_t F, int32_t* __restrict__ tid,
+                             int32_t* __restrict__ mark) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= F) return;
+    uint32_t t = (uint32_t)keys[i];
+    tid[i] = (int32_t)t;
+    mark[t] = 1;
+}
+
+__global__ void k_fidx(const int32_t* __restrict__ mark, const int32_t* __restrict__ rank, int64_t m,
+                       int32_t* __restrict__ fidx) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) fidx[i] = mark[i] ? rank[i] : -1;
+}
+
+// warp per item: count / emit (fidx << 32 | pos) for entries whose tid failed somewhere
+template <bool kEmit>
+__global__ void k_ab_scan(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
+                          const int32_t* __restrict__ orig2pos, int64_t n,
+                          const int32_t* __restrict__ fidx, unsigned long long* __restrict__ cnt,
+                          uint64_t* __restrict__ keys, unsigned long long* __restrict__ cursor) {
+    int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    int lane = threadIdx.x & 31;
+    if (item >= n) return;
+    int64_t b = offsets[item], e = offsets[item + 1];
+    uint32_t pos = (uint32_t)orig2pos[item];
+    for (int64_t k = b + lane; k < e; k += 32) {
+        int32_t f = fidx[tids[k]];
+        if (f < 0) continue;
+        if (kEmit) {
+            unsigned long long at = atomicAdd(cursor, 1ull);
+            keys[at] = ((uint64_t)(uint32_t)f << 32) | pos;
+        } else {
+            atomicAdd(cnt + f, 1ull);
+        }
+    }
+}
+
+__global__ void k_low32(const uint64_t* __restrict__ keys, int64_t n, int32_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)(uint32_t)keys[i];
+}
+
+static inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+static batmap_status cub_tmp(batmap_collection* h, size_t need, cudaStream_t st) {
+    if (h->cub_tmp && h->cub_tmp_bytes >= need) return BATMAP_OK;
+    dfree(h->cub_tmp, st);
+    h->cub_tmp = nullptr;
+    size_t b = need + need / 4 + 4096;
+    BM_TRY(dalloc(&h->cub_tmp, b, st));
+    h->cub_tmp_bytes = b;
+    return BATMAP_OK;
+}
+
+static int ilog2_u64(uint64_t v) {
+    int l = 0;
+    while ((1ull << l) < v) ++l;
+    return l;
+}
+
+// Failure list F sorted by (pos, tid), per-item offsets and A_b of failed tids.
+static batmap_status post_failures(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
+                                   uint64_t* fails, int64_t F, cudaStream_t st) {
+    const int64_t n = h->n, m = h->m;
+    BM_TRY(dalloc_t(&h->fail_off_d, n + 1, st));
+    {
+        size_t tb = 0;
+        BM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, h->f_d, h->fail_off_d, (int)std::max<int64_t>(n, 1), st));
+        BM_TRY(cub_tmp(h, tb, st));
+        if (n > 0) BM_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp, tb, h->f_d, h->fail_off_d, (int)n, st));
+        h->launches += 1;
+        k_set_i64<<<1, 1, 0, st>>>(h->fail_off_d + n, F);
+        h->launches += 1;
+    }
+    BM_TRY(dalloc_t(&h->fidx_of_tid_d, m, st));
+    if (F == 0) {
+        k_fill_i32<<<grid_for(m, 256), 256, 0, st>>>(h->fidx_of_tid_d, m, -1);
+        h->launches += 1;
+        BM_TRY(dalloc_t(&h->fail_tid_d, 1, st));
+        BM_TRY(dalloc_t(&h->ab_off_d, 1, st));
+        BM_TRY(dalloc_t(&h->ab_pos_d, 1, st));
+        BM_CUDA(cudaMemsetAsync(h->ab_off_d, 0, sizeof(int64_t), st));
+        h->n_ftid = 0;
+        return BATMAP_OK;
+    }
+    // sort F by (pos, tid)
+    uint64_t* sorted = nullptr;
+    BM_TRY(dalloc_t(&sorted, F, st));
+    int end_bit = 32 + std::max(1, ilog2_u64((uint64_t)n + 1));
+    {
+        size_t tb = 0;
+        BM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, fails, sorted, (int)F, 0, end_bit, st));
+        BM_TRY(cub_tmp(h, tb, st));
+        BM_CUDA(cub::DeviceRadixSort::SortKeys(h->cub_tmp, tb, fails, sorted, (int)F, 0, end_bit, st));
+        h->launches += 1;
+    }
+    BM_TRY(dalloc_t(&h->fail_tid_d, F, st));
+    int32_t *mark = nullptr, *rank = nullptr;
+    BM_TRY(dalloc_t(&mark, m + 1, st));
+    BM_TRY(dalloc_t(&rank, m + 1, st));
+    BM_CUDA(cudaMemsetAsync(mark, 0, (m + 1) * sizeof(int32_t), st));
+    k_fail_split<<<grid_for(F, 256), 256, 0, st>>>(sorted, F, h->fail_tid_d, mark);
+    h->launches += 1;
+    {
+        size_t tb = 0;
+        BM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, mark, rank, (int)(m + 1), st));
+        BM_TRY(cub_tmp(h, tb, st));
+        BM_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp, tb, mark, rank, (int)(m + 1), st));
+        h->launches += 1;
+    }
+    k_fidx<<<grid_for(m, 256), 256, 0, st>>>(mark, rank, m, h->fidx_of_tid_d);
+    h->launches += 1;
+    int32_t nft = 0;
+    BM_CUDA(cudaMemcpyAsync(&nft, rank + m, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    h->n_ftid = nft;
+    // A_b: counts per failed tid, then (fidx, pos) keys sorted
+    unsigned long long* cnt = nullptr;
+    BM_TRY(dalloc_t(&cnt, nft + 1, st));
+    BM_CUDA(cudaMemsetAsync(cnt, 0, (nft + 1) * sizeof(unsigned long long), st));
+    k_ab_scan<false><<<grid_for(n * 32, 256), 256, 0, st>>>(offsets, tids, h->orig2pos_d, n,
+                                                             h->fidx_of_tid_d, cnt, nullptr, nullptr);
+    h->launches += 1;
+    BM_TRY(dalloc_t(&h->ab_off_d, nft + 1, st));
+    {
+        int64_t* c64 = reinterpret_cast<int64_t*>(cnt);
+        size_t tb = 0;
+        BM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c64, h->ab_off_d, (int)(nft + 1), st));
+        BM_TRY(cub_tmp(h, tb, st));
+        BM_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp, tb, c64, h->ab_off_d, (int)(nft + 1), st));
+        h->launches += 1;
+    }
+    int64_t total = 0;
+    BM_CUDA(cudaMemcpyAsync(&total, h->ab_off_d + nft, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    uint64_t *keys = nullptr, *keys2 = nullptr;
+    unsigned long long* cursor = nullptr;
+    BM_TRY(dalloc_t(&keys, total, st));
+    BM_TRY(dalloc_t(&keys2, total, st));
+    BM_TRY(dalloc_t(&cursor, 1, st));
+    BM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+    k_ab_scan<true><<<grid_for(n * 32, 256), 256, 0, st>>>(offsets, tids, h->orig2pos_d, n,
+                                                            h->fidx_of_tid_d, nullptr, keys, cursor);
+    h->launches += 1;
+    {
+        int eb = 32 + std::max(1, ilog2_u64((uint64_t)nft + 1));
+        size_t tb = 0;
+        BM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, (int)total, 0, eb, st));
+        BM_TRY(cub_tmp(h, tb, st));
+        BM_CUDA(cub::DeviceRadixSort::SortKeys(h->cub_tmp, tb, keys, keys2, (int)total, 0, eb, st));
+        h->launches += 1;
+    }
+    BM_TRY(dalloc_t(&h->ab_pos_d, total, st));
+    k_low32<<<grid_for(total, 256), 256, 0, st>>>(keys2, total, h->ab_pos_d);
+    h->launches += 1;
+    dfree(keys, st);
+    dfree(keys2, st);
+    dfree(cursor, st);
+    dfree(cnt, st);
+    dfree(mark, st);
+    dfree(rank, st);
+    dfree(sorted, st);
+    return BATMAP_OK;
+}
+
+batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
+                               const batmap_build_opts* o, cudaStream_t st) {
+    const int64_t n = h->n, m = h->m;
+    const int64_t l0 = h->launches;
+    rec(h, EV_B0, st);
+    // ---- parameters (readings #2, #4)
+    int s = 0;
+    while ((127ll << s) < m) ++s;
+    h->s = s;
+    h->U = 127ll << s;
+    h->pi = make_pi(h->seed, s, o ? o->pi_table : nullptr);
+
+    std::vector<int64_t> off_h(n + 1);
+    BM_CUDA(cudaMemcpyAsync(off_h.data(), offsets, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    if (off_h[0] != 0) {
+        set_error("offsets[0] must be 0");
+        return BATMAP_E_INVALID;
+    }
+    std::vector<uint8_t> lr_item(n);
+    const int lmin = std::max(s, ilog2_u64(h->r_min));
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t sz = off_h[i + 1] - off_h[i];
+        if (sz < 0) {
+            set_error("offsets must be non-decreasing (item %lld)", (long long)i);
+            return BATMAP_E_INVALID;
+        }
+        if (sz > m) {
+            set_error("item %lld has %lld > n_transactions tids", (long long)i, (long long)sz);
+            return BATMAP_E_INVALID;
+        }
+        int l = ilog2_u64((uint64_t)(2 * sz));  // 2^ceil(log2 2|S|)
+        lr_item[i] = (uint8_t)std::max(l, lmin);
+    }
+    const int64_t nnz = off_h[n];
+    // ---- sort by width, stable by id (reading #16): counting sort over log2 r
+    h->pos2orig_h.resize(n);
+    h->orig2pos_h.resize(n);
+    {
+        int64_t cnt[64] = {0};
+        for (int64_t i = 0; i < n; ++i) cnt[lr_item[i]]++;
+        int64_t acc = 0;
+        for (int l = 0; l < 64; ++l) {
+            int64_t c = cnt[l];
+            cnt[l] = acc;
+            acc += c;
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            int64_t p = cnt[lr_item[i]]++;
+            h->pos2orig_h[p] = (int32_t)i;
+            h->orig2pos_h[i] = (int32_t)p;
+        }
+    }
+    std::vector<uint8_t> lr_pos(n);
+    std::vector<int64_t> work_off(n + 1);
+    work_off[0] = 0;
+    for (int64_t p = 0; p < n; ++p) {
+        lr_pos[p] = lr_item[h->pos2orig_h[p]];
+        work_off[p + 1] = work_off[p] + 3ll * (1ll << lr_pos[p]);
+    }
+    h->arena_bytes_raw = work_off[n];
+    h->classes.clear();
+    int64_t word_off = 0;
+    for (int64_t p = 0; p < n;) {
+        int64_t q = p;
+        while (q < n && lr_pos[q] == lr_pos[p]) ++q;
+        ClassInfo c{};
+        c.first = p;
+        c.n = (int32_t)(q - p);
+        c.n_pad = (int32_t)((c.n + kPadItems - 1) / kPadItems * kPadItems);
+        c.r = 1 << lr_pos[p];
+        c.W = 3 * c.r / 4;
+        c.word_off = word_off;
+        word_off += (int64_t)c.W * c.n_pad;
+        h->classes.push_back(c);
+        p = q;
+    }
+    h->arena_words = word_off;
+    h->r0 = n ? (1ll << lr_pos[0]) : (1ll << lmin);  // r0 = min r_i (reading #5)
+    h->log2r0 = ilog2_u64((uint64_t)h->r0);
+    if (h->arena_words > (1ll << 40)) {
+        set_error("arena too large");
+        return BATMAP_E_OVERFLOW;
+    }
+
+    // ---- device state
+    BM_TRY(dalloc_t(&h->pos2orig_d, n, st));
+    BM_TRY(dalloc_t(&h->orig2pos_d, n, st));
+    BM_TRY(dalloc_t(&h->f_d, n, st));
+    BM_TRY(dalloc_t(&h->arena_d, h->arena_words, st));
+    int64_t* work_off_d = nullptr;
+    uint8_t* lr_d = nullptr;
+    uint32_t* work = nullptr;
+    BM_TRY(dalloc_t(&work_off_d, n + 1, st));
+    BM_TRY(dalloc_t(&lr_d, n, st));
+    BM_TRY(dalloc_t(&work, h->arena_bytes_raw, st));
+    if (n) {
+        BM_CUDA(cudaMemcpyAsync(h->pos2orig_d, h->pos2orig_h.data(), n * 4, cudaMemcpyHostToDevice, st));
+        BM_CUDA(cudaMemcpyAsync(h->orig2pos_d, h->orig2pos_h.data(), n * 4, cudaMemcpyHostToDevice, st));
+        BM_CUDA(cudaMemcpyAsync(work_off_d, work_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+        BM_CUDA(cudaMemcpyAsync(lr_d, lr_pos.data(), n, cudaMemcpyHostToDevice, st));
+    }
+    if (o && (o->flags & BATMAP_CHECK_INPUT) && n) {
+        int* bad = nullptr;
+        BM_TRY(dalloc_t(&bad, 1, st));
+        BM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+        k1_check<<<grid_for(n * 32, 256), 256, 0, st>>>(offsets, tids, n, m, bad);
+        int bad_h = 0;
+        BM_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        dfree(bad, st);
+        if (bad_h) {
+            dfree(work_off_d, st);
+            dfree(lr_d, st);
+            dfree(work, st);
+            set_error("invalid tidlists: every tidlist must be strictly increasing in [0, n_transactions)");
+            return BATMAP_E_INVALID;
+        }
+    }
+    // failure buffer: generous first guess, exact retry if exceeded (the build is deterministic)
+    int64_t fail_cap = std::max<int64_t>(1 << 16, nnz / 16);
+    uint64_t* fails = nullptr;
+    unsigned long long* fail_ctr = nullptr;
+    BM_TRY(dalloc_t(&fail_ctr, 1, st));
+    int64_t F = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        BM_TRY(dalloc_t(&fails, fail_cap, st));
+        BM_CUDA(cudaMemsetAsync(work, 0xFF, h->arena_bytes_raw * sizeof(uint32_t), st));
+        BM_CUDA(cudaMemsetAsync(fail_ctr, 0, sizeof(unsigned long long), st));
+        rec(h, EV_I0, st);
+        if (n)
+            k1_insert<<<grid_for(n, 128), 128, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d, lr_d, n,
+                                                        h->pi, (uint32_t)h->r0, h->log2r0, h->max_loop_opt,
+                                                        work, h->f_d, fails, fail_ctr, fail_cap);
+        rec(h, EV_I1, st);
+        h->launches += 1;
+        BM_CUDA(cudaGetLastError());
+        unsigned long long Fh = 0;
+        BM_CUDA(cudaMemcpyAsync(&Fh, fail_ctr, sizeof(Fh), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        F = (int64_t)Fh;
+        if (F <= fail_cap) break;
+        dfree(fails, st);
+        fail_cap = F;
+    }
+    h->n_fail = F;
+    rec(h, EV_E0, st);
+    for (const ClassInfo& c : h->classes) {
+        int64_t cnt = (int64_t)c.W * c.n_pad;
+        k1_encode<<<grid_for(cnt, 256), 256, 0, st>>>(work, work_off_d, c.first, c.n, c.n_pad, c.W,
+                                                      (uint32_t)c.r, h->pi, (uint32_t)h->r0, h->log2r0,
+                                                      h->arena_d + c.word_off);
+        h->launches += 1;
+    }
+    rec(h, EV_E1, st);
+    BM_CUDA(cudaGetLastError());
+    BM_TRY(post_failures(h, offsets, tids, fails, F, st));
+    BM_CUDA(cudaGetLastError());
+    dfree(fails, st);
+    dfree(fail_ctr, st);
+    dfree(work, st);
+    dfree(work_off_d, st);
+    dfree(lr_d, st);
+    rec(h, EV_B1, st);
+    h->build_timed = true;
+    h->stats.launches_build = h->launches - l0;
+    return BATMAP_OK;
+}
+
+}  // namespace bm

@@ -1,0 +1,378 @@
+// capi.cu -- the extern "C" boundary declared in include/batmap.h.
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+
+using namespace bm;
+
+namespace {
+
+void set_pool_threshold(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
+void free_all(batmap_collection* h) {
+    cudaStream_t st = h->stream;
+    void* ptrs[] = {h->pos2orig_d, h->orig2pos_d, h->arena_d,   h->f_d,      h->fail_off_d, h->fail_tid_d,
+                    h->fidx_of_tid_d, h->ab_off_d, h->ab_pos_d, h->cand_d,   h->ctr_d,      h->key_d,
+                    h->val_d,     h->cub_tmp,    h->sel_arena_d, h->sel_idx_d, h->res_d};
+    for (void* p : ptrs) dfree(p, st);
+}
+
+bool full_selection(const batmap_collection* h, Selection* sel) {
+    sel->classes = h->classes;
+    sel->arena = h->arena_d;
+    sel->f = h->f_d;
+    sel->sel2pos = nullptr;
+    sel->sel2orig = h->pos2orig_d;
+    sel->n_sel = h->n;
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* batmap_last_error(void) { return get_error(); }
+
+const char* batmap_version(void) { return "batmap-b200 0.1 (sm_100a)"; }
+
+batmap_status batmap_build(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t n_transactions,
+                           const batmap_build_opts* opts, batmap_stream_t stream, batmap_handle* out) {
+    if (!out) {
+        set_error("out is NULL");
+        return BATMAP_E_INVALID;
+    }
+    *out = nullptr;
+    if (!offsets || (!tids && n_items > 0)) {
+        set_error("offsets/tids is NULL");
+        return BATMAP_E_INVALID;
+    }
+    if (n_items < 0 || n_transactions < 1) {
+        set_error("need n_items >= 0 and n_transactions >= 1");
+        return BATMAP_E_INVALID;
+    }
+    if (n_items >= (1ll << 31) || n_transactions >= (1ll << 31)) {
+        set_error("n_items and n_transactions must be < 2^31");
+        return BATMAP_E_OVERFLOW;
+    }
+    uint32_t r_min = (opts && opts->r_min) ? opts->r_min : 128u;
+    if (r_min < 4 || (r_min & (r_min - 1))) {
+        set_error("r_min must be a power of two >= 4 (got %u)", r_min);
+        return BATMAP_E_INVALID;
+    }
+    batmap_collection* h = new (std::nothrow) batmap_collection();
+    if (!h) {
+        set_error("host allocation failed");
+        return BATMAP_E_NOMEM;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    h->stream = st;
+    if (cudaGetDevice(&h->device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("no CUDA device available");
+        delete h;
+        return BATMAP_E_CUDA;
+    }
+    set_pool_threshold(h->device);
+    h->n = n_items;
+    h->m = n_transactions;
+    h->seed = opts ? opts->seed : 0;
+    h->r_min = r_min;
+    h->max_loop_opt = opts ? opts->max_loop : 0;
+    batmap_status rc = build_collection(h, offsets, tids, opts, st);
+    if (rc != BATMAP_OK) {
+        free_all(h);
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return BATMAP_OK;
+}
+
+batmap_status batmap_pair_supports_ex(batmap_handle h, const int32_t* items, int64_t n_sel, uint32_t threshold,
+                                      int32_t part, int32_t n_parts, uint32_t flags, batmap_triple* out,
+                                      int64_t capacity, int64_t* n_out, batmap_stream_t stream) {
+    if (!h || !n_out || (!out && capacity > 0) || capacity < 0) {
+        set_error("null handle / n_out / out");
+        return BATMAP_E_INVALID;
+    }
+    if (n_parts < 1 || part < 0 || part >= n_parts) {
+        set_error("need 0 <= part < n_parts");
+        return BATMAP_E_INVALID;
+    }
+    if (items && n_sel < 0) {
+        set_error("n_sel < 0");
+        return BATMAP_E_INVALID;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    h->stream = st;
+    const int64_t l0 = h->launches;
+    const bool cached = h->res_n >= 0 && h->res_items == items && h->res_nsel == (items ? n_sel : -1) &&
+                        h->res_thr == threshold && h->res_flags == flags && h->res_part == part &&
+                        h->res_nparts == n_parts;
+    if (!cached) {
+        h->res_n = -1;
+        rec(h, EV_P0, st);
+        Selection sel;
+        if (items) {
+            BM_TRY(gather_selection(h, items, n_sel, st, &sel));
+        } else {
+            full_selection(h, &sel);
+        }
+        int64_t n_cand = 0, n_res = 0;
+        h->stats.word_compares = h->stats.tile_compares = 0;
+        h->stats.k2_kind = h->stats.k2_grid = 0;
+        rec(h, EV_K20, st);  // re-recorded by run_intersect when a kernel runs
+        rec(h, EV_K21, st);
+        BM_TRY(run_intersect(h, sel, threshold, part, n_parts, flags, st, &n_cand));
+        rec(h, EV_K30, st);
+        BM_TRY(run_finalize(h, sel, n_cand, threshold, flags, st, &n_res));
+        rec(h, EV_P1, st);
+        h->pairs_timed = true;
+        h->stats.n_candidates = n_cand;
+        h->stats.n_results = n_res;
+        h->res_n = n_res;
+        h->res_items = items;
+        h->res_nsel = items ? n_sel : -1;
+        h->res_thr = threshold;
+        h->res_flags = flags;
+        h->res_part = part;
+        h->res_nparts = n_parts;
+    }
+    *n_out = h->res_n;
+    if (h->res_n > capacity) {
+        set_error("capacity %lld < %lld results", (long long)capacity, (long long)h->res_n);
+        return BATMAP_E_CAPACITY;
+    }
+    if (h->res_n > 0)
+        BM_CUDA(cudaMemcpyAsync(out, h->res_d, h->res_n * sizeof(batmap_triple), cudaMemcpyDeviceToDevice, st));
+    h->res_n = -1;  // consumed; the next call recomputes
+    h->stats.launches_pairs = h->launches - l0;
+    return BATMAP_OK;
+}
+
+batmap_status batmap_pair_supports(batmap_handle h, const int32_t* items, int64_t n_sel, uint32_t threshold,
+                                   batmap_triple* out, int64_t capacity, int64_t* n_out, batmap_stream_t stream) {
+    return batmap_pair_supports_ex(h, items, n_sel, threshold, 0, 1, 0u, out, capacity, n_out, stream);
+}
+
+batmap_status batmap_pair_supports_part(batmap_handle h, const int32_t* items, int64_t n_sel, uint32_t threshold,
+                                        int32_t part, int32_t n_parts, batmap_triple* out, int64_t capacity,
+                                        int64_t* n_out, batmap_stream_t stream) {
+    return batmap_pair_supports_ex(h, items, n_sel, threshold, part, n_parts, 0u, out, capacity, n_out, stream);
+}
+
+batmap_status batmap_info(batmap_handle h, batmap_info_t* info) {
+    if (!h || !info) {
+        set_error("null handle / info");
+        return BATMAP_E_INVALID;
+    }
+    info->s_shift = h->s;
+    info->n_classes = (int32_t)h->classes.size();
+    info->U = h->U;
+    info->r0 = h->r0;
+    info->n_items = h->n;
+    info->n_transactions = h->m;
+    info->arena_bytes = h->arena_bytes_raw;
+    info->n_failures = h->n_fail;
+    info->n_failed_tids = h->n_ftid;
+    return BATMAP_OK;
+}
+
+void batmap_destroy(batmap_handle h) {
+    if (!h) return;
+    free_all(h);
+    if (h->ev_ok)
+        for (int i = 0; i < EV_COUNT; ++i) cudaEventDestroy(h->ev[i]);
+    delete h;
+}
+
+static double ev_ms(batmap_collection* h, int a, int b) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(h->ev[b]) != cudaSuccess || cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.0;
+    }
+    return (double)ms;
+}
+
+batmap_status batmap_stats(batmap_handle h, batmap_stats_t* out) {
+    if (!h || !out) {
+        set_error("null handle / out");
+        return BATMAP_E_INVALID;
+    }
+    if (h->ev_ok && h->build_timed) {
+        h->stats.build_ms = ev_ms(h, EV_B0, EV_B1);
+        h->stats.k1_insert_ms = ev_ms(h, EV_I0, EV_I1);
+        h->stats.k1_encode_ms = ev_ms(h, EV_E0, EV_E1);
+    }
+    if (h->ev_ok && h->pairs_timed) {
+        h->stats.pairs_ms = ev_ms(h, EV_P0, EV_P1);
+        h->stats.k2_ms = ev_ms(h, EV_K20, EV_K21);
+        h->stats.k3_ms = ev_ms(h, EV_K30, EV_P1);
+    }
+    *out = h->stats;
+    return BATMAP_OK;
+}
+
+batmap_status batmap_sort_triples(batmap_triple* triples, int64_t n, batmap_stream_t stream) {
+    if (!triples && n > 0) {
+        set_error("null triples");
+        return BATMAP_E_INVALID;
+    }
+    return sort_triples(triples, n, reinterpret_cast<cudaStream_t>(stream));
+}
+
+batmap_status batmap_mine_host(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t n_transactions,
+                               const batmap_build_opts* opts, const int32_t* items, int64_t n_sel,
+                               uint32_t threshold, batmap_triple* out, int64_t capacity, int64_t* n_out,
+                               batmap_stream_t stream) {
+    if (!offsets || !n_out || (!out && capacity > 0) || n_items < 0) {
+        set_error("null argument");
+        return BATMAP_E_INVALID;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nnz = offsets[n_items];
+    int64_t* off_d = nullptr;
+    int32_t *tids_d = nullptr, *items_d = nullptr;
+    batmap_triple* out_d = nullptr;
+    batmap_handle h = nullptr;
+    batmap_status rc = BATMAP_OK;
+    auto cleanup = [&]() {
+        batmap_destroy(h);
+        dfree(off_d, st);
+        dfree(tids_d, st);
+        dfree(items_d, st);
+        dfree(out_d, st);
+    };
+    if ((rc = dalloc_t(&off_d, n_items + 1, st)) != BATMAP_OK || (rc = dalloc_t(&tids_d, nnz, st)) != BATMAP_OK ||
+        (items && (rc = dalloc_t(&items_d, n_sel, st)) != BATMAP_OK) ||
+        (rc = dalloc_t(&out_d, std::max<int64_t>(capacity, 1), st)) != BATMAP_OK) {
+        cleanup();
+        return rc;
+    }
+    if (cudaMemcpyAsync(off_d, offsets, (n_items + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        (nnz && cudaMemcpyAsync(tids_d, tids, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, st) != cudaSuccess) ||
+        (items && n_sel &&
+         cudaMemcpyAsync(items_d, items, n_sel * sizeof(int32_t), cudaMemcpyHostToDevice, st) != cudaSuccess)) {
+        set_error("H2D copy failed: %s", cudaGetErrorString(cudaGetLastError()));
+        cleanup();
+        return BATMAP_E_CUDA;
+    }
+    rc = batmap_build(off_d, tids_d, n_items, n_transactions, opts, stream, &h);
+    if (rc == BATMAP_OK)
+        rc = batmap_pair_supports(h, items ? items_d : nullptr, n_sel, threshold, out_d, capacity, n_out, stream);
+    if (rc == BATMAP_OK && *n_out > 0) {
+        if (cudaMemcpyAsync(out, out_d, *n_out * sizeof(batmap_triple), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            set_error("D2H copy failed: %s", cudaGetErrorString(cudaGetLastError()));
+            rc = BATMAP_E_CUDA;
+        }
+    }
+    cleanup();
+    return rc;
+}
+
+batmap_status batmap_export_entries(batmap_handle h, int32_t item, uint8_t* out, int64_t capacity, int64_t* r_out) {
+    if (!h || !out || !r_out || item < 0 || item >= h->n) {
+        set_error("bad handle / item / out");
+        return BATMAP_E_INVALID;
+    }
+    const int64_t pos = h->orig2pos_h[item];
+    const ClassInfo* c = nullptr;
+    for (const ClassInfo& ci : h->classes)
+        if (pos >= ci.first && pos < ci.first + ci.n) c = &ci;
+    *r_out = c->r;
+    if (capacity < 3ll * c->r) {
+        set_error("capacity %lld < 3 r = %lld", (long long)capacity, 3ll * c->r);
+        return BATMAP_E_CAPACITY;
+    }
+    const uint32_t* src = h->arena_d + c->word_off + (pos - c->first);
+    BM_CUDA(cudaMemcpy2DAsync(out, 4, src, (size_t)c->n_pad * 4, 4, (size_t)c->W, cudaMemcpyDeviceToHost, h->stream));
+    BM_CUDA(cudaStreamSynchronize(h->stream));
+    return BATMAP_OK;
+}
+
+batmap_status batmap_export_failures(batmap_handle h, int32_t* items, int32_t* tids, int64_t capacity,
+                                     int64_t* n_out) {
+    if (!h || !n_out || ((!items || !tids) && capacity > 0)) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    *n_out = h->n_fail;
+    if (capacity < h->n_fail) {
+        set_error("capacity %lld < %lld failures", (long long)capacity, (long long)h->n_fail);
+        return BATMAP_E_CAPACITY;
+    }
+    if (h->n_fail == 0) return BATMAP_OK;
+    std::vector<int64_t> off(h->n + 1);
+    std::vector<int32_t> ft(h->n_fail);
+    BM_CUDA(cudaMemcpyAsync(off.data(), h->fail_off_d, (h->n + 1) * 8, cudaMemcpyDeviceToHost, h->stream));
+    BM_CUDA(cudaMemcpyAsync(ft.data(), h->fail_tid_d, h->n_fail * 4, cudaMemcpyDeviceToHost, h->stream));
+    BM_CUDA(cudaStreamSynchronize(h->stream));
+    std::vector<std::pair<int32_t, int32_t>> rec;
+    rec.reserve(h->n_fail);
+    for (int64_t p = 0; p < h->n; ++p)
+        for (int64_t q = off[p]; q < off[p + 1]; ++q) rec.emplace_back(h->pos2orig_h[p], ft[q]);
+    std::sort(rec.begin(), rec.end());
+    for (size_t k = 0; k < rec.size(); ++k) {
+        items[k] = rec[k].first;
+        tids[k] = rec[k].second;
+    }
+    return BATMAP_OK;
+}
+
+batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n, uint32_t* out,
+                                 batmap_stream_t stream) {
+    if ((!x || !y || !out) && n > 0) {
+        set_error("null argument");
+        return BATMAP_E_INVALID;
+    }
+    return swar_device(x, y, n, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+batmap_status batmap_plan_tiles(int32_t n_classes, const int64_t* class_n, const int64_t* class_w, int32_t tile_m,
+                                int32_t part, int32_t n_parts, int32_t* tiles, int64_t capacity, int64_t* n_tiles,
+                                int64_t* work) {
+    if (n_classes < 0 || (n_classes && (!class_n || !class_w)) || !n_tiles || !work || n_parts < 1 || part < 0 ||
+        part >= n_parts || tile_m < 0) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    std::vector<ClassInfo> cls(n_classes);
+    int64_t first = 0;
+    for (int a = 0; a < n_classes; ++a) {
+        cls[a].first = first;
+        cls[a].n = (int32_t)class_n[a];
+        cls[a].W = (int32_t)class_w[a];
+        first += class_n[a];
+    }
+    TileList tl;
+    plan_tiles(cls, tile_m ? tile_m : 128, part, n_parts, &tl);
+    *n_tiles = (int64_t)tl.tiles.size();
+    *work = tl.work;
+    if (capacity < *n_tiles) {
+        set_error("capacity %lld < %lld tiles", (long long)capacity, (long long)*n_tiles);
+        return BATMAP_E_CAPACITY;
+    }
+    for (size_t k = 0; k < tl.tiles.size(); ++k) {
+        tiles[4 * k + 0] = tl.tiles[k].x;
+        tiles[4 * k + 1] = tl.tiles[k].y;
+        tiles[4 * k + 2] = tl.tiles[k].z;
+        tiles[4 * k + 3] = tl.tiles[k].w;
+    }
+    return BATMAP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// util.cu -- errors, allocation, π parameters.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace bm {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+const char* get_error() { return g_err; }
+
+batmap_status dalloc(void** p, size_t bytes, cudaStream_t s) {
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+        *p = nullptr;
+        return e == cudaErrorMemoryAllocation ? BATMAP_E_NOMEM : BATMAP_E_CUDA;
+    }
+    return BATMAP_OK;
+}
+
+void dfree(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+static uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Round keys k_{t,r} = (low32(splitmix64(seed + (4t + r)·φ)) | 1) mod 2^w  (reading #3).
+PiParams make_pi(uint64_t seed, int s, const uint32_t* table) {
+    PiParams P{};
+    P.s = (uint32_t)s;
+    P.w = (uint32_t)s + 7u;
+    P.U = 127u << s;
+    P.mask = (P.w >= 32) ? 0xFFFFFFFFu : ((1u << P.w) - 1u);
+    P.half = (P.w + 1u) / 2u;
+    for (int t = 0; t < 3; ++t)
+        for (int r = 0; r < 4; ++r) {
+            uint64_t z = splitmix64(seed + (uint64_t)(4 * t + r) * 0x9E3779B97F4A7C15ull);
+            P.key[t][r] = (((uint32_t)z) | 1u) & P.mask;
+        }
+    P.table = table;
+    return P;
+}
+
+}  // namespace bm

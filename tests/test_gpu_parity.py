@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path, called through the C-ABI, against the CPU oracle.
+
+The bar is bit-exact equality (integer work): the sorted (i, j, support) triples equal the
+definition oracle (sorted merge / horizontal counting, oracle/pairs.c); the BatMap bytes
+the build writes equal the step-by-step reference build (oracle/batmap_ref.py); the raw
+counts of the intersection kernels equal the reference wrap-around count.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import batmap_ref as br  # noqa: E402
+from workloads import make_config, uniform, zipf  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1102_1003_b200 import batmap
+
+    batmap.load_library()
+
+
+def _coll(off, tids, m, **kw):
+    from paper_1102_1003_b200 import Collection
+
+    return Collection(torch.as_tensor(off, dtype=torch.int64).cuda(), torch.as_tensor(tids, dtype=torch.int32).cuda(),
+                      m, **kw)
+
+
+def _np(t):
+    return t.cpu().numpy().astype(np.uint32).reshape(-1, 3)
+
+
+def _mixed(seed, n=24, m=20000):
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(n):
+        size = int(min(m - 1, max(1, round(rng.uniform(20, 300) * 2 ** rng.integers(0, 7) / 4))))
+        base = np.sort(rng.choice(m, size=size, replace=False))
+        if i and rng.random() < 0.5:
+            base = np.unique(np.concatenate([base, rows[-1][: size // 2]]))
+        rows.append(base.astype(np.int32))
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    return off, np.concatenate(rows), m
+
+
+# ----------------------------------------------------------------------------- device SWAR
+def test_swar_device_exhaustive():
+    from paper_1102_1003_b200 import swar_device
+
+    a = np.repeat(np.arange(256, dtype=np.uint64), 256)
+    b = np.tile(np.arange(256, dtype=np.uint64), 256)
+    rng = np.random.default_rng(1)
+    for lane in range(4):
+        sh = np.uint64(8 * lane)
+        keep = ~(np.uint64(0xFF) << sh) & np.uint64(0xFFFFFFFF)
+        x = (rng.integers(0, 2 ** 32, a.shape[0], dtype=np.uint64) & keep) | (a << sh)
+        y = (rng.integers(0, 2 ** 32, a.shape[0], dtype=np.uint64) & keep) | (b << sh)
+        ref = br.swar_count_np(x, y)
+        fast, paper = swar_device(torch.as_tensor(x.astype(np.uint32).view(np.int32)),
+                                  torch.as_tensor(y.astype(np.uint32).view(np.int32)))
+        np.testing.assert_array_equal(fast.cpu().numpy(), ref)
+        np.testing.assert_array_equal(paper.cpu().numpy(), ref)
+
+
+# ----------------------------------------------------------------------------- K1 bytes
+def test_golden_c6_build_and_counts(golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "c6_batmap.json")))
+    U = g["U"]
+    pi = np.array([[(a * x + c) % U for x in range(U)] for a, c in g["pi_affine"]], dtype=np.int32)
+    names = ["A", "B", "C"]
+    tids = np.concatenate([g["sets"][k] for k in names]).astype(np.int32)
+    off = np.zeros(4, np.int64)
+    off[1:] = np.cumsum([len(g["sets"][k]) for k in names])
+    c = _coll(off, tids, g["m"], r_min=g["r_min"], pi_table=torch.as_tensor(pi).cuda())
+    inf = c.info()
+    assert inf["s_shift"] == g["s"] and inf["r0"] == g["r0"]
+    for i, k in enumerate(names):
+        assert " ".join("%02X" % v for v in c.export_entries(i)) == g["bytes"][k]
+    assert c.failures().tolist() == [[0, 9]]
+    raw = _np(c.pair_supports(threshold=0, raw=True))
+    got = {(names[i], names[j]): s for i, j, s in raw.tolist()}
+    for pair, val in g["raw_counts"].items():
+        if pair[0] != pair[1]:
+            assert got[(pair[0], pair[1])] == val
+    sup = _np(c.pair_supports(threshold=0))
+    assert {(names[i], names[j]): s for i, j, s in sup.tolist()} == {(p[0], p[1]): v for p, v in g["supports"].items()}
+
+
+@pytest.mark.parametrize("seed,max_loop", [(0, 0), (1, 0), (2, 1), (3, 2)])
+def test_build_bytes_equal_reference(seed, max_loop):
+    off, tids = uniform(150, 12000, 0.03, 100 + seed)
+    c = _coll(off, tids, 12000, seed=seed, max_loop=max_loop)
+    ref = br.Collection(off, tids, 12000, seed=seed, r_min=128, max_loop=max_loop or None)
+    for i in range(ref.n):
+        np.testing.assert_array_equal(c.export_entries(i), ref.bytes[i], err_msg=f"item {i}")
+    assert c.failures().tolist() == [list(x) for x in ref.failures()]
+    if max_loop == 1:
+        assert len(ref.failures()) > 0
+
+
+def test_build_mixed_widths_bytes_and_raw_counts():
+    off, tids, m = _mixed(5)
+    c = _coll(off, tids, m, seed=9)
+    ref = br.Collection(off, tids, m, seed=9, r_min=128)
+    assert len(set(ref.r)) >= 4
+    for i in range(ref.n):
+        np.testing.assert_array_equal(c.export_entries(i), ref.bytes[i])
+    expect = np.array([(i, j, ref.raw_count(i, j)) for i in range(ref.n) for j in range(i + 1, ref.n)], np.uint32)
+    for simple in (False, True):
+        np.testing.assert_array_equal(_np(c.pair_supports(threshold=0, raw=True, simple=simple)), expect)
+
+
+# ----------------------------------------------------------------------------- end to end
+def _check_exact(off, tids, m, thr, items=None, **kw):
+    c = _coll(off, tids, m, **kw)
+    got = _np(c.pair_supports(items, threshold=thr))
+    ref = oracle.pairs_horizontal(off, tids, m, items=items, threshold=thr)
+    np.testing.assert_array_equal(got, ref)
+    return c, got
+
+
+def test_c1_exact_both_kernels():
+    w = make_config("C1")
+    c, got = _check_exact(w.offsets, w.tids, w.m, w.threshold)
+    np.testing.assert_array_equal(got, oracle.pairs_merge(w.offsets, w.tids, threshold=w.threshold))
+    np.testing.assert_array_equal(_np(c.pair_supports(threshold=w.threshold, simple=True)), got)
+    st = c.stats()
+    assert st["k2_kind"] == 2  # the last call used the simple kernel
+    c.pair_supports(threshold=w.threshold)
+    st = c.stats()
+    assert st["k2_kind"] == 1 and st["k2_ms"] > 0 and st["word_compares"] > 0
+
+
+def test_c1_threshold_zero_every_pair():
+    w = make_config("C1", scale_items=0.3)
+    _check_exact(w.offsets, w.tids, w.m, 0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_mixed_widths_exact_with_failures(seed):
+    off, tids, m = _mixed(seed, n=40)
+    for max_loop in (0, 1):
+        c, _ = _check_exact(off, tids, m, 1, seed=seed, max_loop=max_loop)
+        if max_loop == 1:
+            assert c.info()["n_failures"] > 0
+
+
+def test_colliding_pi_forces_failures_exact():
+    off, tids = uniform(60, 3000, 0.1, 5)
+    s, U = br.derive_params(3000)
+    pi = np.array([[(a * x + cc) % U for x in range(U)] for a, cc in [(1, 0), (5, 3), (11, 7)]], dtype=np.int32)
+    c, _ = _check_exact(off, tids, 3000, 1, pi_table=torch.as_tensor(pi).cuda())
+    assert c.info()["n_failures"] > 100
+
+
+def test_items_subset_and_parts():
+    w = make_config("C1")
+    rng = np.random.default_rng(3)
+    items = rng.choice(w.n, size=400, replace=False).astype(np.int32)
+    c, got = _check_exact(w.offsets, w.tids, w.m, 3, items=items)
+    parts = [_np(c.pair_supports(items, threshold=3, part=p, n_parts=3)) for p in range(3)]
+    allp = np.concatenate(parts)
+    allp = allp[np.lexsort((allp[:, 1], allp[:, 0]))]
+    np.testing.assert_array_equal(allp, got)
+    assert sum(len(p) for p in parts) == len(got)
+
+
+def test_edge_cases():
+    from paper_1102_1003_b200 import BatMapError, mine_host
+
+    # empty collection, single item, empty tidlists, threshold above m
+    c = _coll(np.zeros(1, np.int64), np.zeros(0, np.int32), 10)
+    assert c.pair_supports(threshold=0).shape == (0, 3)
+    c = _coll(np.array([0, 3], np.int64), np.array([1, 2, 3], np.int32), 10)
+    assert c.pair_supports(threshold=0).shape == (0, 3)
+    off = np.array([0, 0, 0, 2], np.int64)
+    c, got = _check_exact(off, np.array([0, 5], np.int32), 10, 0)
+    assert got.tolist() == [[0, 1, 0], [0, 2, 0], [1, 2, 0]]
+    w = make_config("C1", scale_items=0.2)
+    _check_exact(w.offsets, w.tids, w.m, w.m + 1)
+    # duplicate / out-of-range items are rejected
+    c = _coll(w.offsets, w.tids, w.m)
+    with pytest.raises(BatMapError):
+        c.pair_supports(np.array([1, 1], np.int32))
+    with pytest.raises(BatMapError):
+        c.pair_supports(np.array([w.n], np.int32))
+    # checked mode rejects unsorted / out-of-range tidlists
+    with pytest.raises(BatMapError):
+        _coll(np.array([0, 2], np.int64), np.array([5, 3], np.int32), 10, check=True)
+    with pytest.raises(BatMapError):
+        _coll(np.array([0, 1], np.int64), np.array([10], np.int32), 10, check=True)
+    # host entry point with the two-call capacity protocol
+    res = mine_host(w.offsets, w.tids, w.m, threshold=2, capacity=1)
+    np.testing.assert_array_equal(res, oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=2))
+
+
+def test_determinism_and_seed_independence():
+    w = make_config("C1")
+    a = _coll(w.offsets, w.tids, w.m, seed=1)
+    b = _coll(w.offsets, w.tids, w.m, seed=1)
+    for i in range(0, w.n, 97):
+        np.testing.assert_array_equal(a.export_entries(i), b.export_entries(i))
+    ra = _np(a.pair_supports(threshold=2))
+    np.testing.assert_array_equal(ra, _np(b.pair_supports(threshold=2)))
+    c = _coll(w.offsets, w.tids, w.m, seed=12345)
+    assert not np.array_equal(a.export_entries(0), c.export_entries(0))
+    np.testing.assert_array_equal(ra, _np(c.pair_supports(threshold=2)))
+
+
+def test_sort_triples():
+    from paper_1102_1003_b200 import sort_triples
+
+    rng = np.random.default_rng(0)
+    t = rng.integers(0, 1000, size=(5000, 3)).astype(np.int32)
+    d = sort_triples(torch.as_tensor(t).cuda())
+    ref = t[np.lexsort((t[:, 1], t[:, 0]))]
+    np.testing.assert_array_equal(d.cpu().numpy()[:, :2], ref[:, :2])
+
+
+# ----------------------------------------------------------------------------- full configs
+def test_c2_full_exact():
+    """The bench workload (BASELINE configs[1]) at full size, in the bench launch configuration."""
+    w = make_config("C2")
+    c, got = _check_exact(w.offsets, w.tids, w.m, w.threshold)
+    assert 1.2e5 < len(got) < 2.5e5
+    st = c.stats()
+    assert st["k2_kind"] == 1
+    # sampled merge cross-check of the horizontal oracle on the emitted pairs
+    sel = np.random.default_rng(0).choice(len(got), size=2000, replace=False)
+    np.testing.assert_array_equal(oracle.merge_list(w.offsets, w.tids, got[sel, 0], got[sel, 1]), got[sel, 2])
+
+
+def test_c3_full_exact():
+    w = make_config("C3")
+    _check_exact(w.offsets, w.tids, w.m, w.threshold)
+
+
+@pytest.mark.parametrize("name", ["C5_p0.001", "C5_p0.01"])
+def test_c5_exact(name):
+    w = make_config(name)
+    _check_exact(w.offsets, w.tids, w.m, w.threshold)
+
+
+def test_c4_zipf_exact():
+    w = make_config("C4")
+    c, got = _check_exact(w.offsets, w.tids, w.m, w.threshold)
+    assert c.info()["n_classes"] >= 6
