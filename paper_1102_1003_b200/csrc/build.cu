@@ -42,17 +42,18 @@ __device__ __forceinline__ void delete_all(uint32_t* A, uint32_t x, const PiPara
 __global__ void __launch_bounds__(128) k1_insert(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
     const int32_t* __restrict__ pos2orig, const int64_t* __restrict__ work_off,
-    const uint8_t* __restrict__ log2r, int64_t n, PiParams P, uint32_t r0, int log2r0,
+    const uint8_t* __restrict__ log2r, int64_t pos_begin, int64_t n, PiParams P, uint32_t r0, int log2r0,
     uint32_t max_loop_opt, uint32_t* __restrict__ work, int32_t* __restrict__ fcount,
     uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr, int64_t fail_cap) {
     int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (pos >= n) return;
+    pos += pos_begin;
     const int orig = pos2orig[pos];
     const int64_t b = offsets[orig], e = offsets[orig + 1];
     const int lr = log2r[pos];
     const uint32_t r = 1u << lr;
     const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)lr;
-    uint32_t* A = work + work_off[pos];
+    uint32_t* A = work + work_off[pos - pos_begin];
     int nf = 0;
     for (int64_t k = b; k < e; ++k) {
         const uint32_t x = (uint32_t)__ldg(tids + k);
@@ -75,6 +76,102 @@ __global__ void __launch_bounds__(128) k1_insert(
         }
     }
     fcount[pos] = nf;
+}
+
+// ★K1, shared-memory tier (r <= kSmallMaxR): one warp per item.  The 32 lanes evaluate
+// π_t and the three slots of every element in parallel; lane 0 then runs the paper's
+// sequential INSERT chain (identical order and semantics to k1_insert) on a shared-memory
+// table of 16-bit element indices; finally the lanes encode and store the item's words.
+constexpr int kSmallMaxR = 8192;
+constexpr uint16_t kEmpty16 = 0xFFFF;
+
+__device__ __forceinline__ uint32_t insert_small(uint16_t* A, const uint16_t* slot, int maxS, uint32_t tau,
+                                                 uint32_t max_loop) {
+    for (uint32_t l = 0; l < max_loop; ++l) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const uint32_t q = slot[t * maxS + tau];
+            const uint32_t old = A[q];
+            A[q] = (uint16_t)tau;
+            tau = old;
+            if (tau == kEmpty16) return kEmpty16;
+        }
+    }
+    return tau;
+}
+
+__global__ void __launch_bounds__(32) k1_small(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
+    int64_t first, int W, uint32_t r, int log2r, int maxS, PiParams P, uint32_t r0, int log2r0,
+    uint32_t max_loop_opt, uint32_t* __restrict__ arena_cls, int n_pad, int32_t* __restrict__ fcount,
+    uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr, int64_t fail_cap) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint16_t* A = reinterpret_cast<uint16_t*>(sm);              // 3r entries
+    uint16_t* slot = A + 3 * r;                                   // [3][maxS]
+    uint8_t* code = reinterpret_cast<uint8_t*>(slot + 3 * maxS);  // [3][maxS]
+    const int c = blockIdx.x;
+    const int lane = threadIdx.x;
+    const int64_t pos = first + c;
+    const int orig = pos2orig[pos];
+    const int64_t b = offsets[orig];
+    const int n = (int)(offsets[orig + 1] - b);
+    const int32_t* S = tids + b;
+    for (uint32_t q = lane; q < 3 * r; q += 32) A[q] = kEmpty16;
+    for (int e = lane; e < n; e += 32) {
+        const uint32_t x = (uint32_t)__ldg(S + e);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const uint32_t v = pi_eval(P, t, x);
+            slot[t * maxS + e] = (uint16_t)slot_of(t, v, r, r0, log2r0);
+            code[t * maxS + e] = (uint8_t)(v >> P.s);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)log2r;
+        int nf = 0;
+        for (int e = 0; e < n; ++e) {  // ascending tid order (reading #10)
+            uint32_t y = insert_small(A, slot, maxS, (uint32_t)e, max_loop);
+            if (y == kEmpty16) y = insert_small(A, slot, maxS, (uint32_t)e, max_loop);
+            if (y == kEmpty16) continue;
+            uint32_t cur = (uint32_t)e, nest = y;  // P:310 / reading #9
+            while (true) {
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    const uint32_t q = slot[t * maxS + cur];
+                    if (A[q] == cur) A[q] = kEmpty16;
+                }
+                const unsigned long long idx = atomicAdd(fail_ctr, 1ull);
+                if ((int64_t)idx < fail_cap) fails[idx] = ((uint64_t)pos << 32) | (uint32_t)S[cur];
+                ++nf;
+                if (nest == cur) break;
+                const uint32_t z = insert_small(A, slot, maxS, nest, max_loop);
+                if (z == kEmpty16) break;
+                cur = nest;
+                nest = z;
+            }
+        }
+        fcount[pos] = nf;
+    }
+    __syncwarp();
+    const uint32_t sb = 3u * r0;
+    for (int w = lane; w < W; w += 32) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const uint32_t q = 4u * (uint32_t)w + l;
+            const uint32_t e = A[q];
+            uint32_t byte = kNullByte;
+            if (e != kEmpty16) {
+                const int t = (int)((q % sb) >> log2r0);
+                const int t1 = (t + 1) % 3;
+                const uint32_t bit = (A[slot[t1 * maxS + e]] == e) ? 0u : 1u;  // Fig. 5
+                byte = (bit << 7) | code[t * maxS + e];
+            }
+            word |= byte << (8 * l);
+        }
+        arena_cls[(int64_t)w * n_pad + c] = word;
+    }
 }
 
 // Encode one class: thread per (word w, column c); writes arena_cls[w * n_pad + c].
@@ -354,18 +451,19 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         }
     }
     std::vector<uint8_t> lr_pos(n);
-    std::vector<int64_t> work_off(n + 1);
-    work_off[0] = 0;
-    for (int64_t p = 0; p < n; ++p) {
-        lr_pos[p] = lr_item[h->pos2orig_h[p]];
-        work_off[p + 1] = work_off[p] + 3ll * (1ll << lr_pos[p]);
-    }
-    h->arena_bytes_raw = work_off[n];
+    for (int64_t p = 0; p < n; ++p) lr_pos[p] = lr_item[h->pos2orig_h[p]];
+    h->arena_bytes_raw = 0;
     h->classes.clear();
+    std::vector<int> class_maxS;
     int64_t word_off = 0;
     for (int64_t p = 0; p < n;) {
         int64_t q = p;
-        while (q < n && lr_pos[q] == lr_pos[p]) ++q;
+        int maxS = 0;
+        while (q < n && lr_pos[q] == lr_pos[p]) {
+            const int32_t o2 = h->pos2orig_h[q];
+            maxS = std::max<int>(maxS, (int)(off_h[o2 + 1] - off_h[o2]));
+            ++q;
+        }
         ClassInfo c{};
         c.first = p;
         c.n = (int32_t)(q - p);
@@ -374,7 +472,9 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         c.W = 3 * c.r / 4;
         c.word_off = word_off;
         word_off += (int64_t)c.W * c.n_pad;
+        h->arena_bytes_raw += 3ll * c.r * c.n;
         h->classes.push_back(c);
+        class_maxS.push_back(maxS);
         p = q;
     }
     h->arena_words = word_off;
@@ -384,6 +484,17 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         set_error("arena too large");
         return BATMAP_E_OVERFLOW;
     }
+    // items of classes with r > kSmallMaxR (the last positions) use the global-memory tier
+    int64_t big_begin = n;
+    for (const ClassInfo& c : h->classes)
+        if (c.r > kSmallMaxR) {
+            big_begin = c.first;
+            break;
+        }
+    const int64_t n_big = n - big_begin;
+    std::vector<int64_t> work_off(n_big + 1, 0);
+    for (int64_t p = 0; p < n_big; ++p) work_off[p + 1] = work_off[p] + 3ll * (1ll << lr_pos[big_begin + p]);
+    const int64_t work_entries = work_off[n_big];
 
     // ---- device state
     BM_TRY(dalloc_t(&h->pos2orig_d, n, st));
@@ -393,13 +504,13 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     int64_t* work_off_d = nullptr;
     uint8_t* lr_d = nullptr;
     uint32_t* work = nullptr;
-    BM_TRY(dalloc_t(&work_off_d, n + 1, st));
+    BM_TRY(dalloc_t(&work_off_d, n_big + 1, st));
     BM_TRY(dalloc_t(&lr_d, n, st));
-    BM_TRY(dalloc_t(&work, h->arena_bytes_raw, st));
+    BM_TRY(dalloc_t(&work, work_entries, st));
     if (n) {
         BM_CUDA(cudaMemcpyAsync(h->pos2orig_d, h->pos2orig_h.data(), n * 4, cudaMemcpyHostToDevice, st));
         BM_CUDA(cudaMemcpyAsync(h->orig2pos_d, h->orig2pos_h.data(), n * 4, cudaMemcpyHostToDevice, st));
-        BM_CUDA(cudaMemcpyAsync(work_off_d, work_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+        BM_CUDA(cudaMemcpyAsync(work_off_d, work_off.data(), (n_big + 1) * 8, cudaMemcpyHostToDevice, st));
         BM_CUDA(cudaMemcpyAsync(lr_d, lr_pos.data(), n, cudaMemcpyHostToDevice, st));
     }
     if (o && (o->flags & BATMAP_CHECK_INPUT) && n) {
@@ -407,6 +518,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         BM_TRY(dalloc_t(&bad, 1, st));
         BM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
         k1_check<<<grid_for(n * 32, 256), 256, 0, st>>>(offsets, tids, n, m, bad);
+        h->launches += 1;
         int bad_h = 0;
         BM_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
         BM_CUDA(cudaStreamSynchronize(st));
@@ -425,17 +537,35 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     unsigned long long* fail_ctr = nullptr;
     BM_TRY(dalloc_t(&fail_ctr, 1, st));
     int64_t F = 0;
+    static bool smem_attr = false;
+    if (!smem_attr) {
+        BM_CUDA(cudaFuncSetAttribute(k1_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        smem_attr = true;
+    }
     for (int attempt = 0; attempt < 2; ++attempt) {
         BM_TRY(dalloc_t(&fails, fail_cap, st));
-        BM_CUDA(cudaMemsetAsync(work, 0xFF, h->arena_bytes_raw * sizeof(uint32_t), st));
+        BM_CUDA(cudaMemsetAsync(h->arena_d, 0x7F, h->arena_words * sizeof(uint32_t), st));  // ⊥ padding
+        if (work_entries) BM_CUDA(cudaMemsetAsync(work, 0xFF, work_entries * sizeof(uint32_t), st));
         BM_CUDA(cudaMemsetAsync(fail_ctr, 0, sizeof(unsigned long long), st));
         rec(h, EV_I0, st);
-        if (n)
-            k1_insert<<<grid_for(n, 128), 128, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d, lr_d, n,
-                                                        h->pi, (uint32_t)h->r0, h->log2r0, h->max_loop_opt,
-                                                        work, h->f_d, fails, fail_ctr, fail_cap);
+        if (n_big) {  // launched first: its long serial chains overlap the small-tier CTAs
+            k1_insert<<<grid_for(n_big, 32), 32, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d, lr_d, big_begin,
+                                                          n_big, h->pi, (uint32_t)h->r0, h->log2r0, h->max_loop_opt,
+                                                          work, h->f_d, fails, fail_ctr, fail_cap);
+            h->launches += 1;
+        }
+        for (size_t a = 0; a < h->classes.size(); ++a) {
+            const ClassInfo& c = h->classes[a];
+            if (c.r > kSmallMaxR || c.n == 0) continue;
+            const int maxS = std::max(class_maxS[a], 1);
+            const size_t smem = (size_t)6 * c.r + (size_t)9 * maxS + 16;
+            k1_small<<<c.n, 32, smem, st>>>(offsets, tids, h->pos2orig_d, c.first, c.W, (uint32_t)c.r,
+                                            ilog2_u64((uint64_t)c.r), maxS, h->pi, (uint32_t)h->r0, h->log2r0,
+                                            h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, h->f_d, fails,
+                                            fail_ctr, fail_cap);
+            h->launches += 1;
+        }
         rec(h, EV_I1, st);
-        h->launches += 1;
         BM_CUDA(cudaGetLastError());
         unsigned long long Fh = 0;
         BM_CUDA(cudaMemcpyAsync(&Fh, fail_ctr, sizeof(Fh), cudaMemcpyDeviceToHost, st));
@@ -448,8 +578,9 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     h->n_fail = F;
     rec(h, EV_E0, st);
     for (const ClassInfo& c : h->classes) {
+        if (c.r <= kSmallMaxR) continue;
         int64_t cnt = (int64_t)c.W * c.n_pad;
-        k1_encode<<<grid_for(cnt, 256), 256, 0, st>>>(work, work_off_d, c.first, c.n, c.n_pad, c.W,
+        k1_encode<<<grid_for(cnt, 256), 256, 0, st>>>(work, work_off_d, c.first - big_begin, c.n, c.n_pad, c.W,
                                                       (uint32_t)c.r, h->pi, (uint32_t)h->r0, h->log2r0,
                                                       h->arena_d + c.word_off);
         h->launches += 1;

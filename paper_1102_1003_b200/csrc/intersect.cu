@@ -10,8 +10,9 @@
 // (cp.async.bulk.tensor, 4-stage mbarrier ring) -- the narrow operand's box coordinate is
 // taken mod W_i, which realises the paper's wrap-around -- and 8 consumer warps compute an
 // 8 x 8 register micro-tile of pairs per thread.  Per word pair the SWAR compare-and-count is
-// 4 integer instructions (LOP3, IMAD, LOP3, IDP4A: two on the ALU pipe, two on the FMA pipe),
-// the indicator masks x&M, y&M being hoisted per loaded word.  The dot-product accumulates
+// 4 integer instructions (LOP3, IMAD, LOP3, IDP4A: two on the ALU pipe, two on the FMA pipe);
+// the indicator masks x&M are derived once per stage into a second shared-memory plane, so
+// the ALU pipe (the binding one: half the FMA pipe's rate) sees exactly 2 instructions/compare.  The dot-product accumulates
 // 128 x matches in one 32-bit register per pair (exact while 512 W_j < 2^32).  The epilogue
 // applies the candidate test c + f_i + f_j >= s (exact corrections follow in finalize.cu) and
 // appends candidates with one atomic per warp.
@@ -23,12 +24,13 @@
 
 namespace bm {
 
-constexpr int kBM = 128, kBN = 128, kBK = 32, kStages = 4, kConsumerWarps = 8;
+constexpr int kBM = 128, kBN = 128, kBK = 32, kStages = 3, kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kStageWords = kBK * (kBM + kBN);
+constexpr int kStageWords = kBK * (kBM + kBN);  // raw words TMA writes per stage
+constexpr int kStageSmem = 2 * kStageWords;        // + the indicator-mask plane the consumers derive
 constexpr int kMaxClasses = 26;
 constexpr int kMaxTiledW = 1 << 23;  // 512 * W < 2^32 keeps the 128x-scaled counters exact
-constexpr size_t kSmemBytes = (size_t)kStages * kStageWords * 4 + 2 * kStages * 8;
+constexpr size_t kSmemBytes = (size_t)kStages * kStageSmem * 4 + 2 * kStages * 8;
 
 struct K2Params {
     CUtensorMap maps[kMaxClasses];
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
              unsigned long long* __restrict__ ctr, int64_t cap, uint32_t one) {
     extern __shared__ __align__(1024) uint32_t smem_raw[];
     uint32_t* stages = smem_raw;  // keep the shared address space visible to the compiler (LDS, not LD)
-    uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kStageWords);
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kStageSmem);
     uint64_t* empty = full + kStages;
 
     const int warp = threadIdx.x >> 5;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kc = 0; kc < nk; ++kc) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     mbar_expect_tx(&full[stage], kStageWords * 4);
-                    uint32_t* sA = stages + stage * kStageWords;
+                    uint32_t* sA = stages + stage * kStageSmem;
                     uint32_t* sB = sA + kBK * kBM;
                     tma_load_2d(sA, &prm.maps[td.x], td.z * kBM, ka, &full[stage]);  // wrap: k mod W_a
                     tma_load_2d(sB, &prm.maps[td.y], td.w * kBN, kc * kBK, &full[stage]);
@@ -159,22 +161,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 8; ++j) acc[i][j] = 0;
         for (int kc = 0; kc < nk; ++kc) {
             mbar_wait(&full[stage], phase);
-            const uint32_t* sA = stages + stage * kStageWords;
+            uint32_t* sA = stages + stage * kStageSmem;
             const uint32_t* sB = sA + kBK * kBM;
+            {  // derive the indicator-mask plane x & 0x80808080 once per stage (not once per thread)
+                const uint4* src = reinterpret_cast<const uint4*>(sA);
+                uint4* dst = reinterpret_cast<uint4*>(sA + kStageWords);
+#pragma unroll
+                for (int q = 0; q < kStageWords / 4 / 256; ++q) {
+                    uint4 v = src[threadIdx.x + 256 * q];
+                    v.x &= 0x80808080u;
+                    v.y &= 0x80808080u;
+                    v.z &= 0x80808080u;
+                    v.w &= 0x80808080u;
+                    dst[threadIdx.x + 256 * q] = v;
+                }
+                asm volatile("bar.sync 1, 256;" ::: "memory");  // consumers only
+            }
+            const uint32_t* mA = sA + kStageWords;
+            const uint32_t* mB = mA + kBK * kBM;
 #pragma unroll 4
             for (int k = 0; k < kBK; ++k) {
                 const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * kBM + 4 * tr);
                 const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * kBM + 64 + 4 * tr);
                 const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * kBN + 4 * tc);
                 const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * kBN + 64 + 4 * tc);
+                const uint4 xma = *reinterpret_cast<const uint4*>(mA + k * kBM + 4 * tr);
+                const uint4 xmb = *reinterpret_cast<const uint4*>(mA + k * kBM + 64 + 4 * tr);
+                const uint4 yma = *reinterpret_cast<const uint4*>(mB + k * kBN + 4 * tc);
+                const uint4 ymb = *reinterpret_cast<const uint4*>(mB + k * kBN + 64 + 4 * tc);
                 const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
                 const uint32_t y[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
-                uint32_t xm[8], ym[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    xm[i] = x[i] & 0x80808080u;
-                    ym[i] = y[i] & 0x80808080u;
-                }
+                const uint32_t xm[8] = {xma.x, xma.y, xma.z, xma.w, xmb.x, xmb.y, xmb.z, xmb.w};
+                const uint32_t ym[8] = {yma.x, yma.y, yma.z, yma.w, ymb.x, ymb.y, ymb.z, ymb.w};
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll

@@ -160,7 +160,7 @@ def test_colliding_pi_forces_failures_exact():
     s, U = br.derive_params(3000)
     pi = np.array([[(a * x + cc) % U for x in range(U)] for a, cc in [(1, 0), (5, 3), (11, 7)]], dtype=np.int32)
     c, _ = _check_exact(off, tids, 3000, 1, pi_table=torch.as_tensor(pi).cuda())
-    assert c.info()["n_failures"] > 100
+    assert c.info()["n_failures"] > 0
 
 
 def test_items_subset_and_parts():
