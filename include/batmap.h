@@ -47,7 +47,10 @@ typedef struct CUstream_st* batmap_stream_t;   /* == cudaStream_t */
 typedef struct batmap_collection* batmap_handle; /* library-owned; free with batmap_destroy */
 
 /* Build flags */
-#define BATMAP_CHECK_INPUT 0x1u  /* validate on device: every tidlist strictly increasing, 0 <= tid < m */
+#define BATMAP_CHECK_INPUT 0x1u   /* validate on device: every tidlist strictly increasing, 0 <= tid < m */
+#define BATMAP_BUILD_SERIAL 0x2u  /* one thread runs each item's INSERTs in ascending tid order:
+                                     deterministic bytes, slower.  Default: the INSERTs of an item run
+                                     concurrently (atomic swaps); layout timing-dependent, supports identical */
 
 /* pair_supports flags (batmap_pair_supports_ex) */
 #define BATMAP_PAIRS_RAW 0x1u      /* test hook: emit the raw BatMap counts (no failure corrections) */
@@ -60,7 +63,7 @@ typedef struct batmap_collection* batmap_handle; /* library-owned; free with bat
  *             >= 128 every BatMap is a multiple of 32 words, which the tiled intersection
  *             kernel requires; smaller values fall back to the simple kernel.
  *   max_loop  MaxLoop rounds of INSERT.  0 => 16 + ceil(3 log2 r_i).
- *   flags     BATMAP_CHECK_INPUT.
+ *   flags     BATMAP_CHECK_INPUT | BATMAP_BUILD_SERIAL.
  *   pi_table  [device] test hook: 3 x U uint32 table replacing the mixer (row t-1 = π_t),
  *             each row a permutation of [0, U), U = 127 * 2^s.  NULL => seeded mixer.
  *             Read during batmap_build only.

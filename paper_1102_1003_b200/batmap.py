@@ -23,6 +23,7 @@ BATMAP_E_OVERFLOW = -5
 _NAMES = {0: "OK", -1: "E_INVALID", -2: "E_NOMEM", -3: "E_CUDA", -4: "E_CAPACITY", -5: "E_OVERFLOW"}
 
 BATMAP_CHECK_INPUT = 0x1
+BATMAP_BUILD_SERIAL = 0x2
 BATMAP_PAIRS_RAW = 0x1
 BATMAP_PAIRS_SIMPLE = 0x2
 
@@ -112,12 +113,12 @@ def _dptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
 
-def _opts(seed, r_min, max_loop, check, pi_table):
+def _opts(seed, r_min, max_loop, check, pi_table, serial=False):
     o = BuildOpts()
     o.seed = int(seed) & (2 ** 64 - 1)
     o.r_min = int(r_min)
     o.max_loop = int(max_loop)
-    o.flags = BATMAP_CHECK_INPUT if check else 0
+    o.flags = (BATMAP_CHECK_INPUT if check else 0) | (BATMAP_BUILD_SERIAL if serial else 0)
     o.pi_table = pi_table.data_ptr() if pi_table is not None else None
     return o
 
@@ -126,7 +127,7 @@ class Collection:
     """The BatMaps of one instance on the current CUDA device (batmap_build)."""
 
     def __init__(self, offsets, tids, n_transactions: int, *, seed: int = 0, r_min: int = 128,
-                 max_loop: int = 0, check: bool = False, pi_table=None, stream=None):
+                 max_loop: int = 0, check: bool = False, pi_table=None, serial: bool = False, stream=None):
         import torch
 
         lib = load_library()
@@ -138,7 +139,7 @@ class Collection:
         self.n_items = self._offsets.numel() - 1
         self.m = int(n_transactions)
         self._stream = stream
-        opts = _opts(seed, r_min, max_loop, check, self._pi)
+        opts = _opts(seed, r_min, max_loop, check, self._pi, serial)
         h = ctypes.c_void_p()
         _check(lib.batmap_build(_dptr(self._offsets), _dptr(self._tids), self.n_items, self.m,
                                 ctypes.byref(opts), _stream_ptr(stream), ctypes.byref(h)))

@@ -174,6 +174,170 @@ __global__ void __launch_bounds__(32) k1_small(
     }
 }
 
+// ★K1, concurrent tiers (default).  The paper's INSERT run by many threads of a CTA
+// at once on one item's tables: every swap "τ <-> A_t[h_t(τ)]" is an atomic exchange, so each
+// table slot holds at most one copy of any element and the number of copies in flight is
+// conserved.  A chain that exceeds MaxLoop rounds records its nestless element as failed; after
+// all chains end, the remaining copy of every failed element is deleted (P:310 with a
+// different attribution of failures, reading #9b) -- the failure set F is exact either way, and
+// the corrections of P:469-474 restore every lost occurrence.  The layout depends on thread
+// timing; the pair supports do not.  BATMAP_BUILD_SERIAL selects the deterministic
+// one-thread-per-item INSERT order instead (byte-identical to oracle/batmap_ref.py).
+constexpr int kConcThreads = 128;
+constexpr int kConcFailCap = 512;  // per-item failure list in shared memory (overflow -> global rescan)
+
+__device__ __forceinline__ void record_failure(uint32_t* fl, int* nfl, uint64_t* fails, unsigned long long* fail_ctr,
+                                               int64_t fail_cap, int64_t pos, uint32_t tid_val, uint32_t e,
+                                               int* overflow) {
+    const int k = atomicAdd(nfl, 1);
+    if (k < kConcFailCap) fl[k] = e;
+    else *overflow = 1;
+    const unsigned long long idx = atomicAdd(fail_ctr, 1ull);
+    if ((int64_t)idx < fail_cap) fails[idx] = ((uint64_t)pos << 32) | tid_val;
+}
+
+__global__ void __launch_bounds__(kConcThreads) k1_conc_small(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
+    int64_t first, int W, uint32_t r, int log2r, int maxS, PiParams P, uint32_t r0, int log2r0,
+    uint32_t max_loop_opt, uint32_t* __restrict__ arena_cls, int n_pad, int32_t* __restrict__ fcount,
+    uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr, int64_t fail_cap) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint32_t* A = reinterpret_cast<uint32_t*>(sm);                   // 3r entries (element index)
+    uint16_t* slot = reinterpret_cast<uint16_t*>(A + 3 * r);          // [3][maxS]
+    uint8_t* code = reinterpret_cast<uint8_t*>(slot + 3 * maxS);      // [3][maxS]
+    __shared__ uint32_t fl[kConcFailCap];
+    __shared__ int nfl, overflow;
+    const int c = blockIdx.x;
+    const int64_t pos = first + c;
+    const int orig = pos2orig[pos];
+    const int64_t b = offsets[orig];
+    const int n = (int)(offsets[orig + 1] - b);
+    const int32_t* S = tids + b;
+    if (threadIdx.x == 0) {
+        nfl = 0;
+        overflow = 0;
+    }
+    for (uint32_t q = threadIdx.x; q < 3 * r; q += blockDim.x) A[q] = kEmpty;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const uint32_t x = (uint32_t)__ldg(S + e);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const uint32_t v = pi_eval(P, t, x);
+            slot[t * maxS + e] = (uint16_t)slot_of(t, v, r, r0, log2r0);
+            code[t * maxS + e] = (uint8_t)(v >> P.s);
+        }
+    }
+    __syncthreads();
+    const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)log2r;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        for (int copy = 0; copy < 2; ++copy) {  // the insert procedure is called twice
+            uint32_t tau = (uint32_t)e;
+            for (uint32_t l = 0; l < max_loop && tau != kEmpty; ++l)
+#pragma unroll
+                for (int t = 0; t < 3 && tau != kEmpty; ++t) tau = atomicExch(&A[slot[t * maxS + tau]], tau);
+            if (tau != kEmpty)
+                record_failure(fl, &nfl, fails, fail_ctr, fail_cap, pos, (uint32_t)S[tau], tau, &overflow);
+        }
+    }
+    __syncthreads();
+    // delete every remaining copy of a failed element
+    const int nf = nfl;
+    if (!overflow) {
+        for (int k = threadIdx.x; k < nf; k += blockDim.x) {
+            const uint32_t e = fl[k];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) atomicCAS(&A[slot[t * maxS + e]], e, kEmpty);
+        }
+    } else {  // rare: many failures -- any element with fewer than two copies was recorded
+        for (int e = threadIdx.x; e < n; e += blockDim.x) {
+            int cnt = 0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) cnt += (A[slot[t * maxS + e]] == (uint32_t)e);
+            if (cnt == 1)
+#pragma unroll
+                for (int t = 0; t < 3; ++t) atomicCAS(&A[slot[t * maxS + e]], (uint32_t)e, kEmpty);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) fcount[pos] = nf;
+    const uint32_t sb = 3u * r0;
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const uint32_t q = 4u * (uint32_t)w + l;
+            const uint32_t e = A[q];
+            uint32_t byte = kNullByte;
+            if (e != kEmpty) {
+                const int t = (int)((q % sb) >> log2r0);
+                const int t1 = (t + 1) % 3;
+                const uint32_t bit = (A[slot[t1 * maxS + e]] == e) ? 0u : 1u;  // Fig. 5
+                byte = (bit << 7) | code[t * maxS + e];
+            }
+            word |= byte << (8 * l);
+        }
+        arena_cls[(int64_t)w * n_pad + c] = word;
+    }
+}
+
+// Concurrent tier for large tables (r > kSmallMaxR): the working table lives in global memory
+// (raw tids, atomics in L2); π is recomputed on every swap.  One CTA per item.
+__global__ void __launch_bounds__(256) k1_conc_global(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
+    const int64_t* __restrict__ work_off, int64_t pos_begin, PiParams P, uint32_t r, int log2r, uint32_t r0,
+    int log2r0, uint32_t max_loop_opt, uint32_t* __restrict__ work, int32_t* __restrict__ fcount,
+    uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr, int64_t fail_cap) {
+    __shared__ uint32_t fl[kConcFailCap];
+    __shared__ int nfl, overflow;
+    const int64_t pos = pos_begin + blockIdx.x;
+    const int orig = pos2orig[pos];
+    const int64_t b = offsets[orig];
+    const int n = (int)(offsets[orig + 1] - b);
+    const int32_t* S = tids + b;
+    uint32_t* A = work + work_off[blockIdx.x];
+    if (threadIdx.x == 0) {
+        nfl = 0;
+        overflow = 0;
+    }
+    __syncthreads();
+    const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)log2r;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const uint32_t x = (uint32_t)__ldg(S + e);
+        for (int copy = 0; copy < 2; ++copy) {
+            uint32_t tau = x;
+            for (uint32_t l = 0; l < max_loop && tau != kEmpty; ++l)
+#pragma unroll
+                for (int t = 0; t < 3 && tau != kEmpty; ++t)
+                    tau = atomicExch(&A[slot_of(t, pi_eval(P, t, tau), r, r0, log2r0)], tau);
+            if (tau != kEmpty) record_failure(fl, &nfl, fails, fail_ctr, fail_cap, pos, tau, tau, &overflow);
+        }
+    }
+    __syncthreads();
+    const int nf = nfl;
+    if (!overflow) {
+        for (int k = threadIdx.x; k < nf; k += blockDim.x) {
+            const uint32_t x = fl[k];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) atomicCAS(&A[slot_of(t, pi_eval(P, t, x), r, r0, log2r0)], x, kEmpty);
+        }
+    } else {
+        for (int e = threadIdx.x; e < n; e += blockDim.x) {
+            const uint32_t x = (uint32_t)S[e];
+            uint32_t q[3];
+            int cnt = 0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                q[t] = slot_of(t, pi_eval(P, t, x), r, r0, log2r0);
+                cnt += (A[q[t]] == x);
+            }
+            if (cnt == 1)
+#pragma unroll
+                for (int t = 0; t < 3; ++t) atomicCAS(&A[q[t]], x, kEmpty);
+        }
+    }
+    if (threadIdx.x == 0) fcount[pos] = nf;
+}
+
 // Encode one class: thread per (word w, column c); writes arena_cls[w * n_pad + c].
 __global__ void __launch_bounds__(256) k1_encode(
     const uint32_t* __restrict__ work, const int64_t* __restrict__ work_off, int64_t first, int n,
@@ -230,6 +394,25 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
 }
 
 __global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+// fail_off[p] = first index of position p in the sorted (pos << 32 | tid) list; f[p] = its count
+__global__ void k_fail_offsets(const uint64_t* __restrict__ keys, int64_t F, int64_t n, int64_t* __restrict__ off,
+                               int32_t* __restrict__ f) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > n) return;
+    auto lb = [&](uint64_t key) {
+        int64_t lo = 0, hi = F;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    const int64_t a = lb((uint64_t)p << 32);
+    off[p] = a;
+    if (p < n) f[p] = (int32_t)(lb((uint64_t)(p + 1) << 32) - a);
+}
 
 __global__ void k_fail_split(const uint64_t* __restrict__ keys, int64_t F, int32_t* __restrict__ tid,
                              int32_t* __restrict__ mark) {
@@ -297,17 +480,10 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
                                    uint64_t* fails, int64_t F, cudaStream_t st) {
     const int64_t n = h->n, m = h->m;
     BM_TRY(dalloc_t(&h->fail_off_d, n + 1, st));
-    {
-        size_t tb = 0;
-        BM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, h->f_d, h->fail_off_d, (int)std::max<int64_t>(n, 1), st));
-        BM_TRY(cub_tmp(h, tb, st));
-        if (n > 0) BM_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp, tb, h->f_d, h->fail_off_d, (int)n, st));
-        h->launches += 1;
-        k_set_i64<<<1, 1, 0, st>>>(h->fail_off_d + n, F);
-        h->launches += 1;
-    }
     BM_TRY(dalloc_t(&h->fidx_of_tid_d, m, st));
     if (F == 0) {
+        if (n) BM_CUDA(cudaMemsetAsync(h->f_d, 0, n * sizeof(int32_t), st));
+        BM_CUDA(cudaMemsetAsync(h->fail_off_d, 0, (n + 1) * sizeof(int64_t), st));
         k_fill_i32<<<grid_for(m, 256), 256, 0, st>>>(h->fidx_of_tid_d, m, -1);
         h->launches += 1;
         BM_TRY(dalloc_t(&h->fail_tid_d, 1, st));
@@ -315,11 +491,16 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
         BM_TRY(dalloc_t(&h->ab_pos_d, 1, st));
         BM_CUDA(cudaMemsetAsync(h->ab_off_d, 0, sizeof(int64_t), st));
         h->n_ftid = 0;
+        h->n_fail = 0;
         return BATMAP_OK;
     }
-    // sort F by (pos, tid)
+    // sort F by (pos, tid) and drop duplicates (the concurrent build may record an element twice)
     uint64_t* sorted = nullptr;
+    uint64_t* uniq = nullptr;
+    int* n_uniq_d = nullptr;
     BM_TRY(dalloc_t(&sorted, F, st));
+    BM_TRY(dalloc_t(&uniq, F, st));
+    BM_TRY(dalloc_t(&n_uniq_d, 1, st));
     int end_bit = 32 + std::max(1, ilog2_u64((uint64_t)n + 1));
     {
         size_t tb = 0;
@@ -327,7 +508,21 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
         BM_TRY(cub_tmp(h, tb, st));
         BM_CUDA(cub::DeviceRadixSort::SortKeys(h->cub_tmp, tb, fails, sorted, (int)F, 0, end_bit, st));
         h->launches += 1;
+        tb = 0;
+        BM_CUDA(cub::DeviceSelect::Unique(nullptr, tb, sorted, uniq, n_uniq_d, (int)F, st));
+        BM_TRY(cub_tmp(h, tb, st));
+        BM_CUDA(cub::DeviceSelect::Unique(h->cub_tmp, tb, sorted, uniq, n_uniq_d, (int)F, st));
+        h->launches += 1;
     }
+    int n_uniq = 0;
+    BM_CUDA(cudaMemcpyAsync(&n_uniq, n_uniq_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    F = n_uniq;
+    h->n_fail = F;
+    std::swap(sorted, uniq);
+    // per-item offsets and counts from the deduplicated list
+    k_fail_offsets<<<grid_for(n + 1, 256), 256, 0, st>>>(sorted, F, n, h->fail_off_d, h->f_d);
+    h->launches += 1;
     BM_TRY(dalloc_t(&h->fail_tid_d, F, st));
     int32_t *mark = nullptr, *rank = nullptr;
     BM_TRY(dalloc_t(&mark, m + 1, st));
@@ -394,6 +589,8 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     dfree(mark, st);
     dfree(rank, st);
     dfree(sorted, st);
+    dfree(uniq, st);
+    dfree(n_uniq_d, st);
     return BATMAP_OK;
 }
 
@@ -540,30 +737,55 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     static bool smem_attr = false;
     if (!smem_attr) {
         BM_CUDA(cudaFuncSetAttribute(k1_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        BM_CUDA(cudaFuncSetAttribute(k1_conc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         smem_attr = true;
     }
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 4; ++attempt) {
         BM_TRY(dalloc_t(&fails, fail_cap, st));
         BM_CUDA(cudaMemsetAsync(h->arena_d, 0x7F, h->arena_words * sizeof(uint32_t), st));  // ⊥ padding
         if (work_entries) BM_CUDA(cudaMemsetAsync(work, 0xFF, work_entries * sizeof(uint32_t), st));
         BM_CUDA(cudaMemsetAsync(fail_ctr, 0, sizeof(unsigned long long), st));
         rec(h, EV_I0, st);
-        if (n_big) {  // launched first: its long serial chains overlap the small-tier CTAs
-            k1_insert<<<grid_for(n_big, 32), 32, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d, lr_d, big_begin,
-                                                          n_big, h->pi, (uint32_t)h->r0, h->log2r0, h->max_loop_opt,
-                                                          work, h->f_d, fails, fail_ctr, fail_cap);
-            h->launches += 1;
-        }
-        for (size_t a = 0; a < h->classes.size(); ++a) {
-            const ClassInfo& c = h->classes[a];
-            if (c.r > kSmallMaxR || c.n == 0) continue;
-            const int maxS = std::max(class_maxS[a], 1);
-            const size_t smem = (size_t)6 * c.r + (size_t)9 * maxS + 16;
-            k1_small<<<c.n, 32, smem, st>>>(offsets, tids, h->pos2orig_d, c.first, c.W, (uint32_t)c.r,
-                                            ilog2_u64((uint64_t)c.r), maxS, h->pi, (uint32_t)h->r0, h->log2r0,
-                                            h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, h->f_d, fails,
-                                            fail_ctr, fail_cap);
-            h->launches += 1;
+        const bool serial = o && (o->flags & BATMAP_BUILD_SERIAL);
+        if (serial) {
+            if (n_big) {  // launched first: its long serial chains overlap the small-tier CTAs
+                k1_insert<<<grid_for(n_big, 32), 32, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d, lr_d,
+                                                              big_begin, n_big, h->pi, (uint32_t)h->r0, h->log2r0,
+                                                              h->max_loop_opt, work, h->f_d, fails, fail_ctr, fail_cap);
+                h->launches += 1;
+            }
+            for (size_t a = 0; a < h->classes.size(); ++a) {
+                const ClassInfo& c = h->classes[a];
+                if (c.r > kSmallMaxR || c.n == 0) continue;
+                const int maxS = std::max(class_maxS[a], 1);
+                const size_t smem = (size_t)6 * c.r + (size_t)9 * maxS + 16;
+                k1_small<<<c.n, 32, smem, st>>>(offsets, tids, h->pos2orig_d, c.first, c.W, (uint32_t)c.r,
+                                                ilog2_u64((uint64_t)c.r), maxS, h->pi, (uint32_t)h->r0, h->log2r0,
+                                                h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, h->f_d, fails,
+                                                fail_ctr, fail_cap);
+                h->launches += 1;
+            }
+        } else {
+            for (size_t a = 0; a < h->classes.size(); ++a) {  // big classes first (longest items)
+                const ClassInfo& c = h->classes[a];
+                if (c.r <= kSmallMaxR || c.n == 0) continue;
+                k1_conc_global<<<c.n, 256, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d + (c.first - big_begin),
+                                                    c.first, h->pi, (uint32_t)c.r, ilog2_u64((uint64_t)c.r),
+                                                    (uint32_t)h->r0, h->log2r0, h->max_loop_opt, work, h->f_d, fails,
+                                                    fail_ctr, fail_cap);
+                h->launches += 1;
+            }
+            for (size_t a = 0; a < h->classes.size(); ++a) {
+                const ClassInfo& c = h->classes[a];
+                if (c.r > kSmallMaxR || c.n == 0) continue;
+                const int maxS = std::max(class_maxS[a], 1);
+                const size_t smem = (size_t)12 * c.r + (size_t)9 * maxS + 16;
+                k1_conc_small<<<c.n, kConcThreads, smem, st>>>(
+                    offsets, tids, h->pos2orig_d, c.first, c.W, (uint32_t)c.r, ilog2_u64((uint64_t)c.r), maxS, h->pi,
+                    (uint32_t)h->r0, h->log2r0, h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, h->f_d, fails,
+                    fail_ctr, fail_cap);
+                h->launches += 1;
+            }
         }
         rec(h, EV_I1, st);
         BM_CUDA(cudaGetLastError());
@@ -573,7 +795,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         F = (int64_t)Fh;
         if (F <= fail_cap) break;
         dfree(fails, st);
-        fail_cap = F;
+        fail_cap = 2 * F + 1024;  // the concurrent build is not deterministic: leave headroom
     }
     h->n_fail = F;
     rec(h, EV_E0, st);

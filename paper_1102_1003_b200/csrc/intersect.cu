@@ -19,18 +19,27 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace bm {
 
-constexpr int kBM = 128, kBN = 128, kBK = 32, kStages = 3, kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kStageWords = kBK * (kBM + kBN);  // raw words TMA writes per stage
-constexpr int kStageSmem = 2 * kStageWords;        // + the indicator-mask plane the consumers derive
+constexpr int kBM = 128, kBN = 128, kBK = 32, kConsumerWarps = 8;
+constexpr int kThreads = kConsumerWarps * 32;
+// K2 variants: BK = words per k-chunk, STAGES = smem ring depth, MINB = CTAs per SM,
+// PF = explicit register prefetch of the next k step.
+template <int BK>
+struct Chunk {
+    static constexpr int kStageWords = BK * (kBM + kBN);  // raw words TMA writes per stage
+    static constexpr int kStageSmem = 2 * kStageWords;    // + the indicator-mask plane the consumers derive
+};
+template <int BK, int STAGES>
+constexpr size_t smem_bytes() {
+    return (size_t)STAGES * Chunk<BK>::kStageSmem * 4 + STAGES * 8;
+}
 constexpr int kMaxClasses = 26;
 constexpr int kMaxTiledW = 1 << 23;  // 512 * W < 2^32 keeps the 128x-scaled counters exact
-constexpr size_t kSmemBytes = (size_t)kStages * kStageSmem * 4 + 2 * kStages * 8;
 
 struct K2Params {
     CUtensorMap maps[kMaxClasses];
@@ -71,17 +80,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 }
 
 // SWAR compare-and-count step, 4 instructions: acc += 128 * matches.
-//   u = (x ^ y) | 0x80808080            LOP3   (ALU pipe)
-//   p = u * one - 0x01010101            IMAD   (FMA pipe; `one` == 1 at run time, so ptxas
-//                                               cannot turn it into an ALU-pipe IADD3)
-//   v = ~p & (xm | ym)                  LOP3   (ALU pipe; xm = x & M, ym = y & M hoisted; an
-//                                               explicit lop3, else ptxas recomputes (x|y)&M)
-//   acc = dp4a(v, 0x01010101, acc)      IDP4A  (FMA pipe): every byte of v is 0x80 or 0
-__device__ __forceinline__ uint32_t swar_step(uint32_t x, uint32_t y, uint32_t xm, uint32_t ym,
-                                              uint32_t acc, uint32_t one) {
-    uint32_t u = (x ^ y) | 0x80808080u;
-    uint32_t p, v, r;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(p) : "r"(u), "r"(one), "n"(0xFEFEFEFFu));
+//   u = (x ^ y) | 0x80808080            LOP3
+//   p = u - 0x01010101                  IADD3
+//   v = ~p & (xm | ym)                  LOP3 (xm = x & M, ym = y & M from the mask plane; an
+//                                             explicit lop3, else ptxas recomputes (x|y)&M per pair)
+//   acc = dp4a(v, 0x01010101, acc)      IDP4A: every byte of v is 0x80 or 0
+// (tools/swar_ubench.cu measured this mix at 0.96 of R_int = 32 compares/clk/SM without LDS.)
+__device__ __forceinline__ uint32_t swar_step(uint32_t x, uint32_t y, uint32_t xm, uint32_t ym, uint32_t acc) {
+    const uint32_t u = (x ^ y) | 0x80808080u;
+    const uint32_t p = u - 0x01010101u;
+    uint32_t v, r;
     asm("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v) : "r"(p), "r"(xm), "r"(ym));  // ~p & (xm | ym)
     asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "n"(0x01010101), "r"(acc));
     return r;
@@ -95,117 +103,156 @@ __device__ __forceinline__ uint32_t swar_paper(uint32_t x, uint32_t y) {
 }
 
 // ------------------------------------------------------------------ tiled kernel
-__global__ void __launch_bounds__(kThreads, 1)
+// Operands of one k step for a thread: 8 row words (x), 8 column words (y) and their masks.
+struct Ops {
+    uint4 xa, xb, ya, yb, ma, mb, na, nb;
+};
+
+__device__ __forceinline__ void load_ops(Ops& o, const uint32_t* sA, const uint32_t* sB, const uint32_t* mA,
+                                         const uint32_t* mB, int k, int tr, int tc) {
+    o.xa = *reinterpret_cast<const uint4*>(sA + k * kBM + 4 * tr);
+    o.xb = *reinterpret_cast<const uint4*>(sA + k * kBM + 64 + 4 * tr);
+    o.ya = *reinterpret_cast<const uint4*>(sB + k * kBN + 4 * tc);
+    o.yb = *reinterpret_cast<const uint4*>(sB + k * kBN + 64 + 4 * tc);
+    o.ma = *reinterpret_cast<const uint4*>(mA + k * kBM + 4 * tr);
+    o.mb = *reinterpret_cast<const uint4*>(mA + k * kBM + 64 + 4 * tr);
+    o.na = *reinterpret_cast<const uint4*>(mB + k * kBN + 4 * tc);
+    o.nb = *reinterpret_cast<const uint4*>(mB + k * kBN + 64 + 4 * tc);
+}
+
+__device__ __forceinline__ void compute_ops(const Ops& o, uint32_t (&acc)[8][8]) {
+    const uint32_t x[8] = {o.xa.x, o.xa.y, o.xa.z, o.xa.w, o.xb.x, o.xb.y, o.xb.z, o.xb.w};
+    const uint32_t y[8] = {o.ya.x, o.ya.y, o.ya.z, o.ya.w, o.yb.x, o.yb.y, o.yb.z, o.yb.w};
+    const uint32_t xm[8] = {o.ma.x, o.ma.y, o.ma.z, o.ma.w, o.mb.x, o.mb.y, o.mb.z, o.mb.w};
+    const uint32_t ym[8] = {o.na.x, o.na.y, o.na.z, o.na.w, o.nb.x, o.nb.y, o.nb.z, o.nb.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = swar_step(x[i], y[j], xm[i], ym[j], acc[i][j]);
+}
+
+// Per-CTA stream of k-chunks: the tiles blockIdx.x, blockIdx.x + gridDim.x, ... each split
+// into W_b / 32 chunks.  The narrow operand's chunk coordinate wraps mod W_a.
+template <int BK>
+struct ChunkCursor {
+    int t, kc, nk, ka, Wa;
+    int4 td;
+    __device__ __forceinline__ bool valid(int n_tiles) const { return t < n_tiles; }
+    __device__ __forceinline__ void load_tile(const K2Params& prm, const int4* tiles, int n_tiles) {
+        if (t < n_tiles) {
+            td = tiles[t];
+            nk = prm.cls_W[td.y] / BK;
+            Wa = prm.cls_W[td.x];
+            kc = 0;
+            ka = 0;
+        }
+    }
+    __device__ __forceinline__ void advance(const K2Params& prm, const int4* tiles, int n_tiles) {
+        ++kc;
+        ka += BK;
+        if (ka == Wa) ka = 0;
+        if (kc == nk) {
+            t += gridDim.x;
+            load_tile(prm, tiles, n_tiles);
+        }
+    }
+};
+
+template <int BK>
+__device__ __forceinline__ void issue_chunk(const K2Params& prm, const ChunkCursor<BK>& c, uint32_t* stages, int buf,
+                                            uint64_t* full) {
+    uint32_t* sA = stages + buf * Chunk<BK>::kStageSmem;
+    uint32_t* sB = sA + BK * kBM;
+    mbar_expect_tx(&full[buf], Chunk<BK>::kStageWords * 4);
+    tma_load_2d(sA, &prm.maps[c.td.x], c.td.z * kBM, c.ka, &full[buf]);  // B_i[w mod W_i]
+    tma_load_2d(sB, &prm.maps[c.td.y], c.td.w * kBN, c.kc * BK, &full[buf]);
+}
+
+// 256 threads = 8 warps; thread (tr, tc) owns rows {4tr..4tr+3, 64+4tr..+3} x cols {4tc.., 64+4tc..}
+// of the 128 x 128 tile.  Thread 0 also drives TMA: after the per-chunk barrier every warp has
+// finished the previous chunk, so that buffer is refilled with the chunk kStages-1 ahead.
+template <int BK, int STAGES, int MINB, bool PF>
+__global__ void __launch_bounds__(kThreads, MINB)
     k2_tiled(const __grid_constant__ K2Params prm, const int4* __restrict__ tiles, int n_tiles,
              const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f, Cand* __restrict__ out,
-             unsigned long long* __restrict__ ctr, int64_t cap, uint32_t one) {
+             unsigned long long* __restrict__ ctr, int64_t cap) {
     extern __shared__ __align__(1024) uint32_t smem_raw[];
     uint32_t* stages = smem_raw;  // keep the shared address space visible to the compiler (LDS, not LD)
-    uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kStageSmem);
-    uint64_t* empty = full + kStages;
+    constexpr int kStageWords = Chunk<BK>::kStageWords, kStageSmem = Chunk<BK>::kStageSmem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + STAGES * kStageSmem);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    ChunkCursor<BK> pre;  // prefetch cursor (meaningful in thread 0 only)
+    pre.t = blockIdx.x;
+    pre.load_tile(prm, tiles, n_tiles);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-        }
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int s = 0; s < STAGES - 1 && pre.valid(n_tiles); ++s) {
+            issue_chunk(prm, pre, stages, s, full);
+            pre.advance(prm, tiles, n_tiles);
+        }
     }
     __syncthreads();
 
-    if (warp == kConsumerWarps) {
-        // ===== TMA producer (one lane) =====
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-                const int4 td = tiles[t];
-                const int Wa = prm.cls_W[td.x], Wb = prm.cls_W[td.y];
-                const int nk = Wb / kBK;
-                int ka = 0;
-                for (int kc = 0; kc < nk; ++kc) {
-                    mbar_wait(&empty[stage], phase ^ 1u);
-                    mbar_expect_tx(&full[stage], kStageWords * 4);
-                    uint32_t* sA = stages + stage * kStageSmem;
-                    uint32_t* sB = sA + kBK * kBM;
-                    tma_load_2d(sA, &prm.maps[td.x], td.z * kBM, ka, &full[stage]);  // wrap: k mod W_a
-                    tma_load_2d(sB, &prm.maps[td.y], td.w * kBN, kc * kBK, &full[stage]);
-                    ka += kBK;
-                    if (ka == Wa) ka = 0;
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                }
-            }
-        }
-        return;
-    }
-
-    // ===== consumers: 8 warps, thread (tr, tc) owns rows {4tr..4tr+3, 64+4tr..} x cols {4tc.., 64+4tc..}
     const int tr = ((warp & 1) << 3) | (lane & 7);
     const int tc = ((warp >> 1) << 2) | (lane >> 3);
-    int stage = 0;
-    uint32_t phase = 0;
+    uint32_t g = 0;  // running chunk index of this CTA
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int4 td = tiles[t];
         const int a = td.x, b = td.y;
-        const int nk = prm.cls_W[b] / kBK;
+        const int nk = prm.cls_W[b] / BK;
         uint32_t acc[8][8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[i][j] = 0;
-        for (int kc = 0; kc < nk; ++kc) {
-            mbar_wait(&full[stage], phase);
-            uint32_t* sA = stages + stage * kStageSmem;
-            const uint32_t* sB = sA + kBK * kBM;
-            {  // derive the indicator-mask plane x & 0x80808080 once per stage (not once per thread)
+        for (int kc = 0; kc < nk; ++kc, ++g) {
+            const int buf = (int)(g % STAGES);
+            mbar_wait(&full[buf], (g / STAGES) & 1u);
+            uint32_t* sA = stages + buf * kStageSmem;
+            {  // derive the indicator-mask plane x & 0x80808080 once per chunk (not once per thread)
                 const uint4* src = reinterpret_cast<const uint4*>(sA);
                 uint4* dst = reinterpret_cast<uint4*>(sA + kStageWords);
 #pragma unroll
-                for (int q = 0; q < kStageWords / 4 / 256; ++q) {
-                    uint4 v = src[threadIdx.x + 256 * q];
+                for (int q = 0; q < kStageWords / 4 / kThreads; ++q) {
+                    uint4 v = src[threadIdx.x + kThreads * q];
                     v.x &= 0x80808080u;
                     v.y &= 0x80808080u;
                     v.z &= 0x80808080u;
                     v.w &= 0x80808080u;
-                    dst[threadIdx.x + 256 * q] = v;
+                    dst[threadIdx.x + kThreads * q] = v;
                 }
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // consumers only
             }
+            __syncthreads();  // masks visible; every warp is done with the previous chunk's buffer
+            if (threadIdx.x == 0 && pre.valid(n_tiles)) {
+                issue_chunk(prm, pre, stages, (int)((g + STAGES - 1) % STAGES), full);
+                pre.advance(prm, tiles, n_tiles);
+            }
+            const uint32_t* sB = sA + BK * kBM;
             const uint32_t* mA = sA + kStageWords;
-            const uint32_t* mB = mA + kBK * kBM;
-#pragma unroll 4
-            for (int k = 0; k < kBK; ++k) {
-                const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * kBM + 4 * tr);
-                const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * kBM + 64 + 4 * tr);
-                const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * kBN + 4 * tc);
-                const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * kBN + 64 + 4 * tc);
-                const uint4 xma = *reinterpret_cast<const uint4*>(mA + k * kBM + 4 * tr);
-                const uint4 xmb = *reinterpret_cast<const uint4*>(mA + k * kBM + 64 + 4 * tr);
-                const uint4 yma = *reinterpret_cast<const uint4*>(mB + k * kBN + 4 * tc);
-                const uint4 ymb = *reinterpret_cast<const uint4*>(mB + k * kBN + 64 + 4 * tc);
-                const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-                const uint32_t y[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
-                const uint32_t xm[8] = {xma.x, xma.y, xma.z, xma.w, xmb.x, xmb.y, xmb.z, xmb.w};
-                const uint32_t ym[8] = {yma.x, yma.y, yma.z, yma.w, ymb.x, ymb.y, ymb.z, ymb.w};
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[i][j] = swar_step(x[i], y[j], xm[i], ym[j], acc[i][j], one);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            if (++stage == kStages) {
-                stage = 0;
-                phase ^= 1u;
+            const uint32_t* mB = mA + BK * kBM;
+            if (PF) {
+                Ops cur, nxt;
+                load_ops(cur, sA, sB, mA, mB, 0, tr, tc);
+#pragma unroll 8
+                for (int k = 0; k < BK; ++k) {
+                    if (k + 1 < BK) load_ops(nxt, sA, sB, mA, mB, k + 1, tr, tc);  // software pipelining
+                    compute_ops(cur, acc);
+                    cur = nxt;
+                }
+            } else {
+#pragma unroll 2
+                for (int k = 0; k < BK; ++k) {
+                    Ops cur;
+                    load_ops(cur, sA, sB, mA, mB, k, tr, tc);
+                    compute_ops(cur, acc);
+                }
             }
         }
-        // ----- epilogue: candidate test and warp-aggregated append
+        // ----- epilogue: candidate test c + f_i + f_j >= thr and warp-aggregated append
         const int na = prm.cls_n[a], nb = prm.cls_n[b];
         const int fa = prm.cls_first[a], fb = prm.cls_first[b];
         int rows[8], cols[8];
@@ -301,7 +348,7 @@ __global__ void k_swar_selftest(const uint32_t* __restrict__ x, const uint32_t* 
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const uint32_t a = x[k], b = y[k];
-    out[k] = swar_step(a, b, a & 0x80808080u, b & 0x80808080u, 0u, one) >> 7;
+    out[k] = swar_step(a, b, a & 0x80808080u, b & 0x80808080u, 0u) >> 7;
     out[n + k] = swar_paper(a, b);
 }
 
@@ -345,6 +392,17 @@ void plan_tiles(const std::vector<ClassInfo>& cls, int tile_m, int part, int n_p
         }
 }
 
+// K2 variant (BATMAP_K2_VARIANT=0|1 overrides, for measurement): 0 = one CTA/SM, 32-word chunks,
+// register-prefetched operands; 1 = two CTAs/SM (16 warps/SM), 16-word chunks.
+static int k2_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("BATMAP_K2_VARIANT");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
 static batmap_status ensure_cand(batmap_collection* h, int64_t need, cudaStream_t st) {
     return ensure(&h->cand_d, &h->cand_cap, need, st);
 }
@@ -355,7 +413,7 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
     if (sel.n_sel < 2) return BATMAP_OK;
     bool simple = (flags & BATMAP_PAIRS_SIMPLE) != 0;
     for (const ClassInfo& c : sel.classes)
-        if (c.W % kBK != 0 || c.W >= kMaxTiledW) simple = true;
+        if (c.W % 32 != 0 || c.W >= kMaxTiledW) simple = true;
     if ((int)sel.classes.size() > kMaxClasses) simple = true;
     PFN_cuTensorMapEncodeTiled_v12000 enc = simple ? nullptr : tensor_map_encoder();
     if (!simple && !enc) simple = true;
@@ -376,7 +434,8 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         h->stats.word_compares = wc;
         h->stats.tile_compares = tl.work;
         h->stats.k2_kind = simple ? 2 : 1;
-        h->stats.k2_grid = simple ? (int32_t)n_tiles : (int32_t)std::min<int64_t>(n_tiles, h->num_sms);
+        h->stats.k2_grid = simple ? (int32_t)n_tiles
+                                  : (int32_t)std::min<int64_t>(n_tiles, (k2_variant() == 0 ? 1 : 2) * h->num_sms);
     }
     if (n_tiles == 0) return BATMAP_OK;
     int4* tiles_d = nullptr;
@@ -402,7 +461,7 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
             const ClassInfo& c = sel.classes[a];
             cuuint64_t dims[2] = {(cuuint64_t)c.n_pad, (cuuint64_t)c.W};
             cuuint64_t strides[1] = {(cuuint64_t)c.n_pad * 4};
-            cuuint32_t box[2] = {(cuuint32_t)kBM, (cuuint32_t)kBK};
+            cuuint32_t box[2] = {(cuuint32_t)kBM, (cuuint32_t)(k2_variant() == 0 ? 32 : 16)};
             cuuint32_t estr[2] = {1, 1};
             CUresult r = enc(&prm->maps[a], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
                              const_cast<uint32_t*>(sel.arena + c.word_off), dims, strides, box, estr,
@@ -420,7 +479,10 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         }
         static bool attr_set = false;
         if (!attr_set) {
-            BM_CUDA(cudaFuncSetAttribute(k2_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+            BM_CUDA(cudaFuncSetAttribute(k2_tiled<32, 3, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes<32, 3>()));
+            BM_CUDA(cudaFuncSetAttribute(k2_tiled<16, 3, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes<16, 3>()));
             attr_set = true;
         }
     }
@@ -432,10 +494,14 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         if (simple) {
             k2_simple<<<(unsigned)n_tiles, dim3(16, 16), 0, st>>>(sel.arena, scls_d, tiles_d, sel.f, threshold, use_f,
                                                                  h->cand_d, h->ctr_d, h->cand_cap);
-        } else {
+        } else if (k2_variant() == 0) {
             const int grid = (int)std::min<int64_t>(n_tiles, h->num_sms);
-            k2_tiled<<<grid, kThreads, kSmemBytes, st>>>(*prm, tiles_d, (int)n_tiles, sel.f, threshold, use_f,
-                                                         h->cand_d, h->ctr_d, h->cand_cap, 1u);
+            k2_tiled<32, 3, 1, true><<<grid, kThreads, smem_bytes<32, 3>(), st>>>(
+                *prm, tiles_d, (int)n_tiles, sel.f, threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
+        } else {
+            const int grid = (int)std::min<int64_t>(n_tiles, 2 * h->num_sms);
+            k2_tiled<16, 3, 2, false><<<grid, kThreads, smem_bytes<16, 3>(), st>>>(
+                *prm, tiles_d, (int)n_tiles, sel.f, threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
         }
         rec(h, EV_K21, st);
         cudaError_t le = cudaGetLastError();

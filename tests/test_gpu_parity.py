@@ -81,7 +81,7 @@ def test_golden_c6_build_and_counts(golden_dir):
     tids = np.concatenate([g["sets"][k] for k in names]).astype(np.int32)
     off = np.zeros(4, np.int64)
     off[1:] = np.cumsum([len(g["sets"][k]) for k in names])
-    c = _coll(off, tids, g["m"], r_min=g["r_min"], pi_table=torch.as_tensor(pi).cuda())
+    c = _coll(off, tids, g["m"], r_min=g["r_min"], pi_table=torch.as_tensor(pi).cuda(), serial=True)
     inf = c.info()
     assert inf["s_shift"] == g["s"] and inf["r0"] == g["r0"]
     for i, k in enumerate(names):
@@ -99,7 +99,7 @@ def test_golden_c6_build_and_counts(golden_dir):
 @pytest.mark.parametrize("seed,max_loop", [(0, 0), (1, 0), (2, 1), (3, 2)])
 def test_build_bytes_equal_reference(seed, max_loop):
     off, tids = uniform(150, 12000, 0.03, 100 + seed)
-    c = _coll(off, tids, 12000, seed=seed, max_loop=max_loop)
+    c = _coll(off, tids, 12000, seed=seed, max_loop=max_loop, serial=True)
     ref = br.Collection(off, tids, 12000, seed=seed, r_min=128, max_loop=max_loop or None)
     for i in range(ref.n):
         np.testing.assert_array_equal(c.export_entries(i), ref.bytes[i], err_msg=f"item {i}")
@@ -110,7 +110,7 @@ def test_build_bytes_equal_reference(seed, max_loop):
 
 def test_build_mixed_widths_bytes_and_raw_counts():
     off, tids, m = _mixed(5)
-    c = _coll(off, tids, m, seed=9)
+    c = _coll(off, tids, m, seed=9, serial=True)
     ref = br.Collection(off, tids, m, seed=9, r_min=128)
     assert len(set(ref.r)) >= 4
     for i in range(ref.n):
@@ -118,6 +118,49 @@ def test_build_mixed_widths_bytes_and_raw_counts():
     expect = np.array([(i, j, ref.raw_count(i, j)) for i in range(ref.n) for j in range(i + 1, ref.n)], np.uint32)
     for simple in (False, True):
         np.testing.assert_array_equal(_np(c.pair_supports(threshold=0, raw=True, simple=simple)), expect)
+
+
+def _check_layout_invariants(c, off, tids, m, seed, r_min=128):
+    """Any valid BatMap: every stored element in exactly two tables at its designated
+    slots with the right code, exactly one copy flagged (Fig. 5), |S| = stored + failed, and no
+    other non-⊥ entry."""
+    s, U = br.derive_params(m)
+    P = br.pi_table(seed, s)
+    fails = {}
+    for it, t in c.failures().tolist():
+        fails.setdefault(it, set()).add(t)
+    r0 = c.info()["r0"]
+    for i in range(len(off) - 1):
+        S = tids[off[i]:off[i + 1]].tolist()
+        ent = c.export_entries(i)
+        r = len(ent) // 3
+        assert r == br.table_range(len(S), s, r_min)
+        seen = np.zeros(len(ent), bool)
+        f = fails.get(i, set())
+        assert f <= set(S)
+        for x in S:
+            qs = [br.h(t, int(P[t - 1][x]), r, r0) for t in (1, 2, 3)]
+            here = [(t, q) for t, q in zip((1, 2, 3), qs)
+                    if ent[q] != br.NULL and (ent[q] & 0x7F) == (int(P[t - 1][x]) >> s)]
+            if x in f:
+                continue
+            assert len(here) == 2, (i, x, here)
+            bits = [ent[q] >> 7 for _, q in here]
+            (t1, _), (t2, _) = here
+            assert bits == [br.indicator(t1, t2), br.indicator(t2, t1)]
+            for _, q in here:
+                seen[q] = True
+        assert int((ent != br.NULL).sum()) == int(seen.sum())  # nothing else stored
+
+
+@pytest.mark.parametrize("max_loop", [0, 1])
+def test_concurrent_build_invariants(max_loop):
+    off, tids, m = _mixed(11, n=30)
+    c = _coll(off, tids, m, seed=4, max_loop=max_loop)
+    _check_layout_invariants(c, off, tids, m, 4)
+    if max_loop:
+        assert c.info()["n_failures"] > 0
+    np.testing.assert_array_equal(_np(c.pair_supports(threshold=0)), oracle.pairs_merge(off, tids, threshold=0))
 
 
 # ----------------------------------------------------------------------------- end to end
@@ -206,15 +249,17 @@ def test_edge_cases():
 
 def test_determinism_and_seed_independence():
     w = make_config("C1")
-    a = _coll(w.offsets, w.tids, w.m, seed=1)
-    b = _coll(w.offsets, w.tids, w.m, seed=1)
+    a = _coll(w.offsets, w.tids, w.m, seed=1, serial=True)
+    b = _coll(w.offsets, w.tids, w.m, seed=1, serial=True)
     for i in range(0, w.n, 97):
         np.testing.assert_array_equal(a.export_entries(i), b.export_entries(i))
     ra = _np(a.pair_supports(threshold=2))
     np.testing.assert_array_equal(ra, _np(b.pair_supports(threshold=2)))
-    c = _coll(w.offsets, w.tids, w.m, seed=12345)
+    c = _coll(w.offsets, w.tids, w.m, seed=12345, serial=True)
     assert not np.array_equal(a.export_entries(0), c.export_entries(0))
     np.testing.assert_array_equal(ra, _np(c.pair_supports(threshold=2)))
+    d = _coll(w.offsets, w.tids, w.m, seed=1)  # concurrent build: layout may differ, supports may not
+    np.testing.assert_array_equal(ra, _np(d.pair_supports(threshold=2)))
 
 
 def test_sort_triples():

@@ -1,34 +1,43 @@
-// tools/swar_ubench.cu -- microbenchmark of the K2 inner loop (8x8 register micro-tile,
-// operands from shared memory) for several SWAR instruction mixes.  Reports word-compares per
-// clock per SM.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o swar_ubench swar_ubench.cu
-#include <cstdio>
+// tools/swar_ubench.cu -- microbenchmark of the K2 inner loop (8x8 register micro-tile per
+// thread, operands from shared memory) for several SWAR instruction mixes and launch shapes.
+// Reports word-compares per clock per SM (R_int = 32).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o swar_ubench swar_ubench.cu
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
-#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s -> %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
+#define CK(x)                                                                  \
+    do {                                                                       \
+        cudaError_t e = (x);                                                   \
+        if (e != cudaSuccess) {                                                \
+            printf("%s -> %s\n", #x, cudaGetErrorString(e));                   \
+            exit(1);                                                           \
+        }                                                                      \
+    } while (0)
 
+// V: 0 = IMAD + IDP4A, 1 = IMAD + IMAD.HI, 2 = LEA.HI, 3 = paper POPC, 4 = IADD3 + IDP4A
 template <int V>
 __device__ __forceinline__ uint32_t step(uint32_t x, uint32_t y, uint32_t xm, uint32_t ym, uint32_t acc,
                                          uint32_t one, uint32_t sh25) {
     uint32_t u = (x ^ y) | 0x80808080u, p, v, r;
-    if (V == 0) {  // LOP3, IMAD, LOP3, IDP4A
+    if (V == 0) {
         asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(p) : "r"(u), "r"(one), "n"(0xFEFEFEFFu));
         asm("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v) : "r"(p), "r"(xm), "r"(ym));
         asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "n"(0x01010101), "r"(acc));
-    } else if (V == 1) {  // LOP3, IMAD, LOP3, IMAD.HI
+    } else if (V == 1) {
         asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(p) : "r"(u), "r"(one), "n"(0xFEFEFEFFu));
         asm("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v) : "r"(p), "r"(xm), "r"(ym));
         asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(sh25), "r"(acc));
-    } else if (V == 2) {  // LOP3, IMAD, LOP3, LEA.HI
+    } else if (V == 2) {
         asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(p) : "r"(u), "r"(one), "n"(0xFEFEFEFFu));
         asm("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v) : "r"(p), "r"(xm), "r"(ym));
         r = acc + (v >> 7);
-    } else if (V == 3) {  // paper literal with POPC
+    } else if (V == 3) {
         p = u - 0x01010101u;
         v = ~p & ((x | y) & 0x80808080u);
         r = acc + __popc(v);
-    } else {  // LOP3, IADD3, LOP3, IDP4A
+    } else {
         p = u - 0x01010101u;
         asm("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v) : "r"(p), "r"(xm), "r"(ym));
         asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "n"(0x01010101), "r"(acc));
@@ -36,16 +45,20 @@ __device__ __forceinline__ uint32_t step(uint32_t x, uint32_t y, uint32_t xm, ui
     return r;
 }
 
-template <int V>
-__global__ void __launch_bounds__(256, 1) bench(const uint32_t* __restrict__ g, int reps, uint32_t one, uint32_t sh25,
-                                                 uint32_t* out, unsigned long long* cycles) {
-    __shared__ __align__(16) uint32_t sA[32 * 128], sB[32 * 128];
-    for (int i = threadIdx.x; i < 32 * 128; i += blockDim.x) {
+// MASKS: 0 = compute x & M in registers per k, 1 = load from a second smem plane, 2 = no LDS in the
+// loop at all (register-resident operands perturbed per k: the compute ceiling)
+template <int V, int MASKS, int NT>
+__global__ void __launch_bounds__(NT, 1) bench(const uint32_t* __restrict__ g, int reps, uint32_t one,
+                                                uint32_t sh25, uint32_t* out, unsigned long long* cycles) {
+    __shared__ __align__(16) uint32_t sA[16 * 128], sB[16 * 128], mA[16 * 128], mB[16 * 128];
+    for (int i = threadIdx.x; i < 16 * 128; i += blockDim.x) {
         sA[i] = g[i];
         sB[i] = g[i + 32 * 128];
+        mA[i] = g[i] & 0x80808080u;
+        mB[i] = g[i + 32 * 128] & 0x80808080u;
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
     const int tr = ((warp & 1) << 3) | (lane & 7);
     const int tc = ((warp >> 1) << 2) | (lane >> 3);
     uint32_t acc[8][8];
@@ -53,22 +66,44 @@ __global__ void __launch_bounds__(256, 1) bench(const uint32_t* __restrict__ g, 
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    uint32_t x[8], y[8], xm[8], ym[8];
+    if (MASKS == 2) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            x[i] = sA[4 * tr + i];
+            y[i] = sB[4 * tc + i];
+            xm[i] = x[i] & 0x80808080u;
+            ym[i] = y[i] & 0x80808080u;
+        }
+    }
     __syncthreads();
     unsigned long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
 #pragma unroll 4
-        for (int k = 0; k < 32; ++k) {
-            const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * 128 + 4 * tr);
-            const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * 128 + 64 + 4 * tr);
-            const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * 128 + 4 * tc);
-            const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * 128 + 64 + 4 * tc);
-            const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-            const uint32_t y[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
-            uint32_t xm[8], ym[8];
+        for (int k = 0; k < 16; ++k) {
+            if (MASKS != 2) {
+                const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * 128 + 4 * tr);
+                const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * 128 + 64 + 4 * tr);
+                const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * 128 + 4 * tc);
+                const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * 128 + 64 + 4 * tc);
+                x[0] = xa.x; x[1] = xa.y; x[2] = xa.z; x[3] = xa.w; x[4] = xb.x; x[5] = xb.y; x[6] = xb.z; x[7] = xb.w;
+                y[0] = ya.x; y[1] = ya.y; y[2] = ya.z; y[3] = ya.w; y[4] = yb.x; y[5] = yb.y; y[6] = yb.z; y[7] = yb.w;
+                if (MASKS == 1) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(mA + k * 128 + 4 * tr);
+                    const uint4 b = *reinterpret_cast<const uint4*>(mA + k * 128 + 64 + 4 * tr);
+                    const uint4 c = *reinterpret_cast<const uint4*>(mB + k * 128 + 4 * tc);
+                    const uint4 d = *reinterpret_cast<const uint4*>(mB + k * 128 + 64 + 4 * tc);
+                    xm[0] = a.x; xm[1] = a.y; xm[2] = a.z; xm[3] = a.w; xm[4] = b.x; xm[5] = b.y; xm[6] = b.z; xm[7] = b.w;
+                    ym[0] = c.x; ym[1] = c.y; ym[2] = c.z; ym[3] = c.w; ym[4] = d.x; ym[5] = d.y; ym[6] = d.z; ym[7] = d.w;
+                } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                xm[i] = x[i] & 0x80808080u;
-                ym[i] = y[i] & 0x80808080u;
+                    for (int i = 0; i < 8; ++i) {
+                        xm[i] = x[i] & 0x80808080u;
+                        ym[i] = y[i] & 0x80808080u;
+                    }
+                }
+            } else {
+                x[k & 7] += one;  // perturb one operand per k so nothing is loop-invariant
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
@@ -87,16 +122,16 @@ __global__ void __launch_bounds__(256, 1) bench(const uint32_t* __restrict__ g, 
     if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
 
-template <int V>
+template <int V, int MASKS, int NT>
 void run(const char* name, const uint32_t* g, int sms, uint32_t* out, unsigned long long* cyc) {
     const int reps = 2000;
-    bench<V><<<sms, 256>>>(g, 10, 1u, 1u << 25, out, cyc);
+    bench<V, MASKS, NT><<<sms, NT>>>(g, 10, 1u, 1u << 25, out, cyc);
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    bench<V><<<sms, 256>>>(g, reps, 1u, 1u << 25, out, cyc);
+    bench<V, MASKS, NT><<<sms, NT>>>(g, reps, 1u, 1u << 25, out, cyc);
     cudaEventRecord(e1);
     CK(cudaDeviceSynchronize());
     float ms;
@@ -106,9 +141,10 @@ void run(const char* name, const uint32_t* g, int sms, uint32_t* out, unsigned l
     double mc = 0;
     for (auto v : c) mc += v;
     mc /= sms;
-    const double per_block = 128.0 * 128.0 * 32.0 * reps;  // word-compares per block
-    printf("{\"variant\": \"%s\", \"cmp_per_clk_per_sm\": %.2f, \"frac_of_32\": %.3f, \"tcmp_per_s\": %.3f, \"ms\": %.2f, \"eff_mhz\": %.0f}\n",
-           name, per_block / mc, per_block / mc / 32.0, per_block * sms / (ms * 1e-3) / 1e12, ms,
+    const double per_block = (double)NT * 64.0 * 16.0 * reps;  // word-compares per block
+    printf("{\"variant\": \"%s\", \"threads\": %d, \"cmp_per_clk_per_sm\": %.2f, \"frac_of_32\": %.3f, "
+           "\"tcmp_per_s\": %.3f, \"ms\": %.2f, \"eff_mhz\": %.0f}\n",
+           name, NT, per_block / mc, per_block / mc / 32.0, per_block * sms / (ms * 1e-3) / 1e12, ms,
            mc / (ms * 1e-3) / 1e6);
 }
 
@@ -118,20 +154,26 @@ int main() {
     std::vector<uint32_t> h(2 * 32 * 128);
     uint64_t z = 88172645463325252ull;
     for (auto& v : h) {
-        z ^= z << 13; z ^= z >> 7; z ^= z << 17;
+        z ^= z << 13;
+        z ^= z >> 7;
+        z ^= z << 17;
         v = (uint32_t)z & 0xFF7F7F7Fu;
         if ((z >> 40) & 1) v |= 0x00808080u;
     }
     uint32_t *g, *out;
     unsigned long long* cyc;
     CK(cudaMalloc(&g, h.size() * 4));
-    CK(cudaMalloc(&out, sms * 256 * 4));
+    CK(cudaMalloc(&out, sms * 512 * 4));
     CK(cudaMalloc(&cyc, sms * 8));
     CK(cudaMemcpy(g, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
-    run<0>("lop3_imad_lop3_idp4a", g, sms, out, cyc);
-    run<1>("lop3_imad_lop3_imadhi", g, sms, out, cyc);
-    run<2>("lop3_imad_lop3_leahi", g, sms, out, cyc);
-    run<3>("paper_popc", g, sms, out, cyc);
-    run<4>("lop3_iadd3_lop3_idp4a", g, sms, out, cyc);
+    run<0, 0, 256>("imad_idp4a/masks_in_regs", g, sms, out, cyc);
+    run<0, 1, 256>("imad_idp4a/masks_from_smem", g, sms, out, cyc);
+    run<0, 2, 256>("imad_idp4a/no_lds_ceiling", g, sms, out, cyc);
+    run<4, 1, 256>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run<4, 2, 256>("iadd3_idp4a/no_lds_ceiling", g, sms, out, cyc);
+    run<0, 1, 384>("imad_idp4a/masks_from_smem", g, sms, out, cyc);
+    run<1, 0, 256>("imad_imadhi/masks_in_regs", g, sms, out, cyc);
+    run<2, 0, 256>("imad_leahi/masks_in_regs", g, sms, out, cyc);
+    run<3, 0, 256>("paper_popc", g, sms, out, cyc);
     return 0;
 }
