@@ -194,12 +194,18 @@ def main():
     from paper_1102_1003_b200 import Collection, batmap, mine_host
     from paper_1102_1003_b200.dist import gather_triples
 
-    torch.cuda.set_device(local_rank)
+    # test hooks (not used by the driver): run several ranks on one GPU over gloo
+    dev_idx = int(os.environ.get("BENCH_FORCE_DEVICE", local_rank))
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(dev_idx)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
     n_gpus = world
     w = _workload(args.config, n_gpus, args.seed)
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", dev_idx)
     off_d = torch.as_tensor(w.offsets).to(dev)
     tids_d = torch.as_tensor(w.tids).to(dev)
     stream = torch.cuda.current_stream(dev)
@@ -209,10 +215,9 @@ def main():
         coll = Collection(off_d, tids_d, w.m, seed=1)
         res = coll.pair_supports(threshold=w.threshold, part=rank, n_parts=world)
         if world > 1:
-            allp = gather_triples(res)
+            allp = gather_triples(res if backend == "nccl" else res.cpu())
             if allp is not None:
-                batmap.sort_triples(allp)
-                res = allp
+                res = batmap.sort_triples(allp.to(dev))
         st = coll.stats()
         coll.close()
         return res, st
@@ -222,7 +227,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_idx)
     sampler.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     stats = []
@@ -240,7 +245,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = float(sum(step_ms))
     if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     n = w.n
