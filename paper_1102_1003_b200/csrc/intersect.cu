@@ -131,14 +131,17 @@ __device__ __forceinline__ void compute_ops(const Ops& o, uint32_t (&acc)[8][8])
         for (int j = 0; j < 8; ++j) acc[i][j] = swar_step(x[i], y[j], xm[i], ym[j], acc[i][j]);
 }
 
-// Per-CTA stream of k-chunks: the tiles blockIdx.x, blockIdx.x + gridDim.x, ... each split
-// into W_b / 32 chunks.  The narrow operand's chunk coordinate wraps mod W_a.
+// Per-CTA stream of k-chunks.  Tiles (sorted by cost, longest first) are claimed dynamically
+// from a global counter by the CTA's thread 0 -- longest-processing-time order, so the CTAs
+// finish within about one (short) tile of each other -- and each tile is split into W_b / BK
+// chunks.  The narrow operand's chunk coordinate wraps mod W_a (reading #18).
 template <int BK>
 struct ChunkCursor {
     int t, kc, nk, ka, Wa;
     int4 td;
     __device__ __forceinline__ bool valid(int n_tiles) const { return t < n_tiles; }
-    __device__ __forceinline__ void load_tile(const K2Params& prm, const int4* tiles, int n_tiles) {
+    __device__ __forceinline__ void claim(const K2Params& prm, const int4* tiles, int n_tiles, int* tile_ctr) {
+        t = atomicAdd(tile_ctr, 1);
         if (t < n_tiles) {
             td = tiles[t];
             nk = prm.cls_W[td.y] / BK;
@@ -147,160 +150,181 @@ struct ChunkCursor {
             ka = 0;
         }
     }
-    __device__ __forceinline__ void advance(const K2Params& prm, const int4* tiles, int n_tiles) {
+    __device__ __forceinline__ void advance(const K2Params& prm, const int4* tiles, int n_tiles, int* tile_ctr) {
         ++kc;
         ka += BK;
         if (ka == Wa) ka = 0;
-        if (kc == nk) {
-            t += gridDim.x;
-            load_tile(prm, tiles, n_tiles);
-        }
+        if (kc == nk) claim(prm, tiles, n_tiles, tile_ctr);
     }
 };
 
+// Thread 0: fill buffer `buf` with the cursor's next chunk (TMA), or post the end marker once.
 template <int BK>
-__device__ __forceinline__ void issue_chunk(const K2Params& prm, const ChunkCursor<BK>& c, uint32_t* stages, int buf,
-                                            uint64_t* full) {
-    uint32_t* sA = stages + buf * Chunk<BK>::kStageSmem;
-    uint32_t* sB = sA + BK * kBM;
-    mbar_expect_tx(&full[buf], Chunk<BK>::kStageWords * 4);
-    tma_load_2d(sA, &prm.maps[c.td.x], c.td.z * kBM, c.ka, &full[buf]);  // B_i[w mod W_i]
-    tma_load_2d(sB, &prm.maps[c.td.y], c.td.w * kBN, c.kc * BK, &full[buf]);
+__device__ __forceinline__ void issue_next(const K2Params& prm, ChunkCursor<BK>& c, const int4* tiles, int n_tiles,
+                                           int* tile_ctr, uint32_t* stages, int buf, uint64_t* full, int2* meta,
+                                           bool& end_sent) {
+    if (c.valid(n_tiles)) {
+        uint32_t* sA = stages + buf * Chunk<BK>::kStageSmem;
+        uint32_t* sB = sA + BK * kBM;
+        meta[buf] = make_int2(c.t, c.kc);  // published by the mbarrier's release/acquire
+        mbar_expect_tx(&full[buf], Chunk<BK>::kStageWords * 4);
+        tma_load_2d(sA, &prm.maps[c.td.x], c.td.z * kBM, c.ka, &full[buf]);  // B_i[w mod W_i]
+        tma_load_2d(sB, &prm.maps[c.td.y], c.td.w * kBN, c.kc * BK, &full[buf]);
+        c.advance(prm, tiles, n_tiles, tile_ctr);
+    } else if (!end_sent) {
+        meta[buf] = make_int2(-1, 0);
+        mbar_arrive(&full[buf]);
+        end_sent = true;
+    }
+}
+
+// Candidate test c + f_i + f_j >= thr for the thread's 8 x 8 pairs and warp-aggregated append.
+__device__ __forceinline__ void tile_epilogue(const K2Params& prm, const int4 td, int tr, int tc, int lane,
+                                              const uint32_t (&acc)[8][8], const int32_t* __restrict__ f,
+                                              uint32_t thr, uint32_t use_f, Cand* __restrict__ out,
+                                              unsigned long long* __restrict__ ctr, int64_t cap) {
+    const int a = td.x, b = td.y;
+    const int na = prm.cls_n[a], nb = prm.cls_n[b];
+    const int fa = prm.cls_first[a], fb = prm.cls_first[b];
+    int rows[8], cols[8];
+    uint32_t fr[8], fc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        rows[i] = td.z * kBM + (i < 4 ? 4 * tr + i : 64 + 4 * tr + (i - 4));
+        cols[i] = td.w * kBN + (i < 4 ? 4 * tc + i : 64 + 4 * tc + (i - 4));
+        fr[i] = (use_f && rows[i] < na) ? (uint32_t)__ldg(f + fa + rows[i]) : 0u;
+        fc[i] = (use_f && cols[i] < nb) ? (uint32_t)__ldg(f + fb + cols[i]) : 0u;
+    }
+    uint64_t mask = 0;
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const bool valid = rows[i] < na && cols[j] < nb && (a != b || rows[i] < cols[j]);
+            const uint64_t c = acc[i][j] >> 7;
+            if (valid && c + fr[i] + fc[j] >= thr) {
+                mask |= 1ull << (i * 8 + j);
+                ++cnt;
+            }
+        }
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    unsigned long long base = 0;
+    if (lane == 31 && incl > 0) base = atomicAdd(ctr, (unsigned long long)incl);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    unsigned long long at = base + (unsigned long long)(incl - cnt);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (mask >> (i * 8 + j) & 1) {
+                if ((int64_t)at < cap) {
+                    Cand cd;
+                    cd.i = (uint32_t)(fa + rows[i]);
+                    cd.j = (uint32_t)(fb + cols[j]);
+                    cd.c = acc[i][j] >> 7;
+                    out[at] = cd;
+                }
+                ++at;
+            }
 }
 
 // 256 threads = 8 warps; thread (tr, tc) owns rows {4tr..4tr+3, 64+4tr..+3} x cols {4tc.., 64+4tc..}
 // of the 128 x 128 tile.  Thread 0 also drives TMA: after the per-chunk barrier every warp has
-// finished the previous chunk, so that buffer is refilled with the chunk kStages-1 ahead.
+// finished the previous chunk, so that buffer is refilled with the chunk STAGES-1 ahead.
 template <int BK, int STAGES, int MINB, bool PF>
 __global__ void __launch_bounds__(kThreads, MINB)
-    k2_tiled(const __grid_constant__ K2Params prm, const int4* __restrict__ tiles, int n_tiles,
+    k2_tiled(const __grid_constant__ K2Params prm, const int4* __restrict__ tiles, int n_tiles, int* tile_ctr,
              const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f, Cand* __restrict__ out,
              unsigned long long* __restrict__ ctr, int64_t cap) {
     extern __shared__ __align__(1024) uint32_t smem_raw[];
     uint32_t* stages = smem_raw;  // keep the shared address space visible to the compiler (LDS, not LD)
     constexpr int kStageWords = Chunk<BK>::kStageWords, kStageSmem = Chunk<BK>::kStageSmem;
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + STAGES * kStageSmem);
+    __shared__ int2 meta[STAGES];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    ChunkCursor<BK> pre;  // prefetch cursor (meaningful in thread 0 only)
-    pre.t = blockIdx.x;
-    pre.load_tile(prm, tiles, n_tiles);
+    ChunkCursor<BK> pre;  // prefetch cursor (thread 0 only)
+    bool end_sent = false;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int s = 0; s < STAGES - 1 && pre.valid(n_tiles); ++s) {
-            issue_chunk(prm, pre, stages, s, full);
-            pre.advance(prm, tiles, n_tiles);
-        }
+        pre.claim(prm, tiles, n_tiles, tile_ctr);
+        for (int s = 0; s < STAGES - 1; ++s)
+            issue_next(prm, pre, tiles, n_tiles, tile_ctr, stages, s, full, meta, end_sent);
     }
     __syncthreads();
 
     const int tr = ((warp & 1) << 3) | (lane & 7);
     const int tc = ((warp >> 1) << 2) | (lane >> 3);
-    uint32_t g = 0;  // running chunk index of this CTA
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int4 td = tiles[t];
-        const int a = td.x, b = td.y;
-        const int nk = prm.cls_W[b] / BK;
-        uint32_t acc[8][8];
+    uint32_t acc[8][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = 0;
-        for (int kc = 0; kc < nk; ++kc, ++g) {
-            const int buf = (int)(g % STAGES);
-            mbar_wait(&full[buf], (g / STAGES) & 1u);
-            uint32_t* sA = stages + buf * kStageSmem;
-            {  // derive the indicator-mask plane x & 0x80808080 once per chunk (not once per thread)
-                const uint4* src = reinterpret_cast<const uint4*>(sA);
-                uint4* dst = reinterpret_cast<uint4*>(sA + kStageWords);
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    int4 td = make_int4(0, 0, 0, 0);
+    bool have_tile = false;
+    for (uint32_t g = 0;; ++g) {
+        const int buf = (int)(g % STAGES);
+        mbar_wait(&full[buf], (g / STAGES) & 1u);
+        const int2 mt = meta[buf];
+        if (mt.y == 0 && have_tile) {  // a new tile (or the end) begins: finish the previous one
+            tile_epilogue(prm, td, tr, tc, lane, acc, f, thr, use_f, out, ctr, cap);
 #pragma unroll
-                for (int q = 0; q < kStageWords / 4 / kThreads; ++q) {
-                    uint4 v = src[threadIdx.x + kThreads * q];
-                    v.x &= 0x80808080u;
-                    v.y &= 0x80808080u;
-                    v.z &= 0x80808080u;
-                    v.w &= 0x80808080u;
-                    dst[threadIdx.x + kThreads * q] = v;
-                }
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+        }
+        if (mt.x < 0) break;
+        if (mt.y == 0) {
+            td = tiles[mt.x];
+            have_tile = true;
+        }
+        uint32_t* sA = stages + buf * kStageSmem;
+        {  // derive the indicator-mask plane x & 0x80808080 once per chunk (not once per thread)
+            const uint4* src = reinterpret_cast<const uint4*>(sA);
+            uint4* dst = reinterpret_cast<uint4*>(sA + kStageWords);
+#pragma unroll
+            for (int q = 0; q < kStageWords / 4 / kThreads; ++q) {
+                uint4 v = src[threadIdx.x + kThreads * q];
+                v.x &= 0x80808080u;
+                v.y &= 0x80808080u;
+                v.z &= 0x80808080u;
+                v.w &= 0x80808080u;
+                dst[threadIdx.x + kThreads * q] = v;
             }
-            __syncthreads();  // masks visible; every warp is done with the previous chunk's buffer
-            if (threadIdx.x == 0 && pre.valid(n_tiles)) {
-                issue_chunk(prm, pre, stages, (int)((g + STAGES - 1) % STAGES), full);
-                pre.advance(prm, tiles, n_tiles);
-            }
-            const uint32_t* sB = sA + BK * kBM;
-            const uint32_t* mA = sA + kStageWords;
-            const uint32_t* mB = mA + BK * kBM;
-            if (PF) {
-                Ops cur, nxt;
-                load_ops(cur, sA, sB, mA, mB, 0, tr, tc);
+        }
+        __syncthreads();  // masks visible; every warp is done with the previous chunk's buffer
+        if (threadIdx.x == 0)
+            issue_next(prm, pre, tiles, n_tiles, tile_ctr, stages, (int)((g + STAGES - 1) % STAGES), full, meta,
+                       end_sent);
+        const uint32_t* sB = sA + BK * kBM;
+        const uint32_t* mA = sA + kStageWords;
+        const uint32_t* mB = mA + BK * kBM;
+        if (PF) {
+            Ops cur, nxt;
+            load_ops(cur, sA, sB, mA, mB, 0, tr, tc);
 #pragma unroll 8
-                for (int k = 0; k < BK; ++k) {
-                    if (k + 1 < BK) load_ops(nxt, sA, sB, mA, mB, k + 1, tr, tc);  // software pipelining
-                    compute_ops(cur, acc);
-                    cur = nxt;
-                }
-            } else {
+            for (int k = 0; k < BK; ++k) {
+                if (k + 1 < BK) load_ops(nxt, sA, sB, mA, mB, k + 1, tr, tc);  // software pipelining
+                compute_ops(cur, acc);
+                cur = nxt;
+            }
+        } else {
 #pragma unroll 2
-                for (int k = 0; k < BK; ++k) {
-                    Ops cur;
-                    load_ops(cur, sA, sB, mA, mB, k, tr, tc);
-                    compute_ops(cur, acc);
-                }
+            for (int k = 0; k < BK; ++k) {
+                Ops cur;
+                load_ops(cur, sA, sB, mA, mB, k, tr, tc);
+                compute_ops(cur, acc);
             }
         }
-        // ----- epilogue: candidate test c + f_i + f_j >= thr and warp-aggregated append
-        const int na = prm.cls_n[a], nb = prm.cls_n[b];
-        const int fa = prm.cls_first[a], fb = prm.cls_first[b];
-        int rows[8], cols[8];
-        uint32_t fr[8], fc[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            rows[i] = td.z * kBM + (i < 4 ? 4 * tr + i : 64 + 4 * tr + (i - 4));
-            cols[i] = td.w * kBN + (i < 4 ? 4 * tc + i : 64 + 4 * tc + (i - 4));
-            fr[i] = (use_f && rows[i] < na) ? (uint32_t)__ldg(f + fa + rows[i]) : 0u;
-            fc[i] = (use_f && cols[i] < nb) ? (uint32_t)__ldg(f + fb + cols[i]) : 0u;
-        }
-        uint64_t mask = 0;
-        int cnt = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const bool valid = rows[i] < na && cols[j] < nb && (a != b || rows[i] < cols[j]);
-                const uint64_t c = acc[i][j] >> 7;
-                if (valid && c + fr[i] + fc[j] >= thr) {
-                    mask |= 1ull << (i * 8 + j);
-                    ++cnt;
-                }
-            }
-        int incl = cnt;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            int v = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += v;
-        }
-        unsigned long long base = 0;
-        if (lane == 31 && incl > 0) base = atomicAdd(ctr, (unsigned long long)incl);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        unsigned long long at = base + (unsigned long long)(incl - cnt);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (mask >> (i * 8 + j) & 1) {
-                    if ((int64_t)at < cap) {
-                        Cand cd;
-                        cd.i = (uint32_t)(fa + rows[i]);
-                        cd.j = (uint32_t)(fb + cols[j]);
-                        cd.c = acc[i][j] >> 7;
-                        out[at] = cd;
-                    }
-                    ++at;
-                }
     }
 }
 
@@ -487,8 +511,9 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         }
     }
     batmap_status rc = BATMAP_OK;
+    int* tile_ctr = reinterpret_cast<int*>(h->ctr_d + 1);
     for (int attempt = 0; attempt < 2; ++attempt) {
-        BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, sizeof(unsigned long long), st));
+        BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, 2 * sizeof(unsigned long long), st));  // [1] = tile counter
         rec(h, EV_K20, st);
         h->launches += 1;
         if (simple) {
@@ -497,11 +522,11 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         } else if (k2_variant() == 0) {
             const int grid = (int)std::min<int64_t>(n_tiles, h->num_sms);
             k2_tiled<32, 3, 1, true><<<grid, kThreads, smem_bytes<32, 3>(), st>>>(
-                *prm, tiles_d, (int)n_tiles, sel.f, threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
+                *prm, tiles_d, (int)n_tiles, tile_ctr, sel.f, threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
         } else {
             const int grid = (int)std::min<int64_t>(n_tiles, 2 * h->num_sms);
             k2_tiled<16, 3, 2, false><<<grid, kThreads, smem_bytes<16, 3>(), st>>>(
-                *prm, tiles_d, (int)n_tiles, sel.f, threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
+                *prm, tiles_d, (int)n_tiles, tile_ctr, sel.f, threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
         }
         rec(h, EV_K21, st);
         cudaError_t le = cudaGetLastError();
