@@ -8,7 +8,7 @@ from .batmap import (  # noqa: F401
     Collection,
     load_library,
     mine_host,
-    plan_tiles,
+    plan_work,
     sort_triples,
     swar_device,
     version,

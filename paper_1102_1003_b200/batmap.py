@@ -80,7 +80,7 @@ def load_library():
         "batmap_export_entries": ([P, I32, P, I64, PI64], ctypes.c_int),
         "batmap_export_failures": ([P, P, P, I64, PI64], ctypes.c_int),
         "batmap_swar_device": ([P, P, I64, P, P], ctypes.c_int),
-        "batmap_plan_tiles": ([I32, P, P, I32, I32, I32, P, I64, PI64, PI64], ctypes.c_int),
+        "batmap_plan_work": ([I32, P, P, I32, I32, I32, P, I64, PI64, PI64, PI64], ctypes.c_int),
         "batmap_stats": ([P, ctypes.POINTER(Stats)], ctypes.c_int),
         "batmap_sort_triples": ([P, I64, P], ctypes.c_int),
     }
@@ -274,17 +274,18 @@ def swar_device(x, y, stream=None):
     return out[:n], out[n:2 * n]
 
 
-def plan_tiles(class_n, class_w, part: int = 0, n_parts: int = 1, tile_m: int = 0):
-    """Host-only planner view: (tiles int32 [T, 4] as (a, b, ti, tj), total work)."""
+def plan_work(class_n, class_w, part: int = 0, n_parts: int = 1, grid_cap: int = 0):
+    """Host-only planner view (batmap_plan_work): (items int32 [T, 8] = (a, b, ti, tj, k0, k1, R, acc),
+    word_compares, tile_compares) of `part`."""
     lib = load_library()
     cn = np.ascontiguousarray(class_n, dtype=np.int64)
     cw = np.ascontiguousarray(class_w, dtype=np.int64)
-    nt, work = ctypes.c_int64(0), ctypes.c_int64(0)
-    rc = lib.batmap_plan_tiles(cn.shape[0], cn.ctypes.data_as(ctypes.c_void_p), cw.ctypes.data_as(ctypes.c_void_p),
-                               tile_m, part, n_parts, None, 0, ctypes.byref(nt), ctypes.byref(work))
+    nt, wc, tcmp = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    args = (cn.shape[0], cn.ctypes.data_as(ctypes.c_void_p), cw.ctypes.data_as(ctypes.c_void_p), part, n_parts,
+            grid_cap)
+    rc = lib.batmap_plan_work(*args, None, 0, ctypes.byref(nt), ctypes.byref(wc), ctypes.byref(tcmp))
     _check(rc, ok=(BATMAP_OK, BATMAP_E_CAPACITY))
-    tiles = np.empty((max(nt.value, 1), 4), dtype=np.int32)
-    _check(lib.batmap_plan_tiles(cn.shape[0], cn.ctypes.data_as(ctypes.c_void_p), cw.ctypes.data_as(ctypes.c_void_p),
-                                 tile_m, part, n_parts, tiles.ctypes.data_as(ctypes.c_void_p), nt.value,
-                                 ctypes.byref(nt), ctypes.byref(work)))
-    return tiles[: nt.value], int(work.value)
+    items = np.empty((max(nt.value, 1), 8), dtype=np.int32)
+    _check(lib.batmap_plan_work(*args, items.ctypes.data_as(ctypes.c_void_p), nt.value, ctypes.byref(nt),
+                                ctypes.byref(wc), ctypes.byref(tcmp)))
+    return items[: nt.value], int(wc.value), int(tcmp.value)

@@ -4,6 +4,7 @@
 #include <new>
 
 #include "common.cuh"
+#include "plan.h"
 
 using namespace bm;
 
@@ -24,7 +25,8 @@ void free_all(batmap_collection* h) {
     cudaStream_t st = h->stream;
     void* ptrs[] = {h->pos2orig_d, h->orig2pos_d, h->arena_d,   h->f_d,      h->fail_off_d, h->fail_tid_d,
                     h->fidx_of_tid_d, h->ab_off_d, h->ab_pos_d, h->cand_d,   h->ctr_d,      h->key_d,
-                    h->val_d,     h->cub_tmp,    h->sel_arena_d, h->sel_idx_d, h->res_d};
+                    h->val_d,     h->cub_tmp,    h->sel_arena_d, h->sel_idx_d, h->res_d,
+                    h->virt_d,    h->cnt_d};
     for (void* p : ptrs) dfree(p, st);
 }
 
@@ -342,35 +344,48 @@ batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n
     return swar_device(x, y, n, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
-batmap_status batmap_plan_tiles(int32_t n_classes, const int64_t* class_n, const int64_t* class_w, int32_t tile_m,
-                                int32_t part, int32_t n_parts, int32_t* tiles, int64_t capacity, int64_t* n_tiles,
-                                int64_t* work) {
-    if (n_classes < 0 || (n_classes && (!class_n || !class_w)) || !n_tiles || !work || n_parts < 1 || part < 0 ||
-        part >= n_parts || tile_m < 0) {
+batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const int64_t* class_w, int32_t part,
+                               int32_t n_parts, int32_t grid_cap, int32_t* items, int64_t capacity, int64_t* n_items,
+                               int64_t* word_compares, int64_t* tile_compares) {
+    if (n_classes < 0 || (n_classes && (!class_n || !class_w)) || !n_items || !word_compares || !tile_compares ||
+        n_parts < 1 || part < 0 || part >= n_parts || grid_cap < 0) {
         set_error("bad arguments");
         return BATMAP_E_INVALID;
     }
     std::vector<ClassInfo> cls(n_classes);
     int64_t first = 0;
     for (int a = 0; a < n_classes; ++a) {
+        if (class_w[a] <= 0 || class_w[a] % kChunk || (a && class_w[a] < class_w[a - 1])) {
+            set_error("class_w must be ascending multiples of %d", kChunk);
+            return BATMAP_E_INVALID;
+        }
         cls[a].first = first;
         cls[a].n = (int32_t)class_n[a];
         cls[a].W = (int32_t)class_w[a];
+        cls[a].n_pad = (int32_t)((class_n[a] + kPadItems - 1) / kPadItems * kPadItems);
         first += class_n[a];
     }
-    TileList tl;
-    plan_tiles(cls, tile_m ? tile_m : 128, part, n_parts, &tl);
-    *n_tiles = (int64_t)tl.tiles.size();
-    *work = tl.work;
-    if (capacity < *n_tiles) {
-        set_error("capacity %lld < %lld tiles", (long long)capacity, (long long)*n_tiles);
+    Plan pl;
+    plan_work(cls, part, n_parts, grid_cap ? grid_cap : 2 * 148, true, true, &pl);
+    *n_items = (int64_t)pl.work.size();
+    *word_compares = pl.word_compares;
+    *tile_compares = pl.tile_compares;
+    if (capacity < *n_items) {
+        set_error("capacity %lld < %lld work items", (long long)capacity, (long long)*n_items);
         return BATMAP_E_CAPACITY;
     }
-    for (size_t k = 0; k < tl.tiles.size(); ++k) {
-        tiles[4 * k + 0] = tl.tiles[k].x;
-        tiles[4 * k + 1] = tl.tiles[k].y;
-        tiles[4 * k + 2] = tl.tiles[k].z;
-        tiles[4 * k + 3] = tl.tiles[k].w;
+    for (size_t k = 0; k < pl.work.size(); ++k) {
+        const Work& w = pl.work[k];
+        const Rect& r = pl.rects[w.rect];
+        int32_t* o = items + 8 * k;
+        o[0] = r.cls_a;
+        o[1] = r.cls_b;
+        o[2] = w.ti;
+        o[3] = w.tj;
+        o[4] = w.k0;
+        o[5] = w.k1;
+        o[6] = r.R;
+        o[7] = r.acc;
     }
     return BATMAP_OK;
 }

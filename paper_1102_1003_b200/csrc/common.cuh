@@ -154,6 +154,11 @@ struct batmap_collection {
     int64_t kv_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_tmp_bytes = 0;
+    // K2 scratch: virtual copies of wide classes, counters of accumulated rectangles
+    uint32_t* virt_d = nullptr;
+    int64_t virt_cap = 0;
+    uint32_t* cnt_d = nullptr;
+    int64_t cnt_cap = 0;
     // selection scratch
     uint32_t* sel_arena_d = nullptr;
     int64_t sel_arena_cap = 0;

@@ -4,48 +4,39 @@
 // W_i <= W_j words,   c_ij = sum_{w < W_j} SWAR(B_j[w], B_i[w mod W_i]),
 // SWAR(x, y) = #byte lanes with equal 7 element bits and (b_x OR b_y).
 //
-// How (B200): the pair triangle is split into width-class rectangles and then
-// into 128 x 128 tiles (symmetry cut p <= q).  A persistent CTA per SM walks its
-// tiles; one producer warp streams [32 words x 128 items] boxes of both operands with TMA
-// (cp.async.bulk.tensor, 4-stage mbarrier ring) -- the narrow operand's box coordinate is
-// taken mod W_i, which realises the paper's wrap-around -- and 8 consumer warps compute an
-// 8 x 8 register micro-tile of pairs per thread.  Per word pair the SWAR compare-and-count is
-// 4 integer instructions (LOP3, IMAD, LOP3, IDP4A: two on the ALU pipe, two on the FMA pipe);
-// the indicator masks x&M are derived once per stage into a second shared-memory plane, so
-// the ALU pipe (the binding one: half the FMA pipe's rate) sees exactly 2 instructions/compare.  The dot-product accumulates
-// 128 x matches in one 32-bit register per pair (exact while 512 W_j < 2^32).  The epilogue
-// applies the candidate test c + f_i + f_j >= s (exact corrections follow in finalize.cu) and
-// appends candidates with one atomic per warp.
+// How (B200): the planner (plan.cu) cuts the pair triangle into width-class rectangles
+// and 128 x 128 tiles (symmetry cut p <= q); skinny rectangles are
+// virtualised and long tiles split along k.  A persistent kernel, 2 CTAs x 8 warps per SM,
+// claims work items longest-first from a global counter; thread 0 of each CTA streams
+// [16 words x 128 items] boxes of both operands with TMA (cp.async.bulk.tensor, 3-stage mbarrier
+// ring) -- the narrow operand's box coordinate is taken mod W_i, which realises the paper's
+// wrap-around -- and every thread computes an 8 x 8 register micro-tile of pairs.  Per word pair
+// the SWAR compare-and-count is 4 integer instructions (LOP3, IADD, LOP3, IDP4A); the indicator
+// masks x & 0x80808080 are derived once per chunk into a second shared-memory plane, so the ALU
+// pipe (the binding one: half the FMA pipe's rate) sees exactly 2 instructions per compare.  The
+// dot product accumulates 128 x matches in one 32-bit register per pair (exact while
+// 512 W_j < 2^32).  Tiles of ordinary rectangles end in the candidate test c + f_i + f_j >= s
+// (exact corrections follow in finalize.cu) with one append per warp; tiles of accumulated
+// rectangles add their partial counts to global counters, thresholded by k2_acc_threshold.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
+#include "plan.h"
 
 namespace bm {
 
-constexpr int kBM = 128, kBN = 128, kBK = 32, kConsumerWarps = 8;
-constexpr int kThreads = kConsumerWarps * 32;
-// K2 variants: BK = words per k-chunk, STAGES = smem ring depth, MINB = CTAs per SM,
-// PF = explicit register prefetch of the next k step.
-template <int BK>
-struct Chunk {
-    static constexpr int kStageWords = BK * (kBM + kBN);  // raw words TMA writes per stage
-    static constexpr int kStageSmem = 2 * kStageWords;    // + the indicator-mask plane the consumers derive
-};
-template <int BK, int STAGES>
-constexpr size_t smem_bytes() {
-    return (size_t)STAGES * Chunk<BK>::kStageSmem * 4 + STAGES * 8;
-}
-constexpr int kMaxClasses = 26;
+constexpr int kBM = kTile, kBN = kTile, kBK = kChunk, kThreads = 256, kStages = 3, kMinBlocks = 2;
+constexpr int kStageWords = kBK * (kBM + kBN);  // raw words TMA writes per stage
+constexpr int kStageSmem = 2 * kStageWords;      // + the indicator-mask plane the consumers derive
+constexpr size_t kSmemBytes = (size_t)kStages * kStageSmem * 4 + kStages * 8;
+constexpr int kMaxMaps = 96;  // 12 KB of __grid_constant__ parameters (CUDA >= 12.1 allows 32 KB)
 constexpr int kMaxTiledW = 1 << 23;  // 512 * W < 2^32 keeps the 128x-scaled counters exact
 
-struct K2Params {
-    CUtensorMap maps[kMaxClasses];
-    int32_t cls_n[kMaxClasses];
-    int32_t cls_W[kMaxClasses];
-    int32_t cls_first[kMaxClasses];
+struct K2Maps {
+    CUtensorMap maps[kMaxMaps];  // classes, then virtual copies
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -131,83 +122,56 @@ __device__ __forceinline__ void compute_ops(const Ops& o, uint32_t (&acc)[8][8])
         for (int j = 0; j < 8; ++j) acc[i][j] = swar_step(x[i], y[j], xm[i], ym[j], acc[i][j]);
 }
 
-// Per-CTA stream of k-chunks.  Tiles (sorted by cost, longest first) are claimed dynamically
-// from a global counter by the CTA's thread 0 -- longest-processing-time order, so the CTAs
-// finish within about one (short) tile of each other -- and each tile is split into W_b / BK
-// chunks.  The narrow operand's chunk coordinate wraps mod W_a (reading #18).
-template <int BK>
-struct ChunkCursor {
-    int t, kc, nk, ka, Wa;
-    int4 td;
-    __device__ __forceinline__ bool valid(int n_tiles) const { return t < n_tiles; }
-    __device__ __forceinline__ void claim(const K2Params& prm, const int4* tiles, int n_tiles, int* tile_ctr) {
-        t = atomicAdd(tile_ctr, 1);
-        if (t < n_tiles) {
-            td = tiles[t];
-            nk = prm.cls_W[td.y] / BK;
-            Wa = prm.cls_W[td.x];
-            kc = 0;
-            ka = 0;
+// Per-CTA stream of k-chunks.  Work items (longest first) are claimed from a global counter by
+// thread 0 -- longest-processing-time order, so the CTAs finish within about one short item of
+// each other.  The narrow operand's chunk coordinate wraps mod W_a (reading #18).
+struct Cursor {
+    int w, kc, k1, ka, Wa, ti, tj, ma, mb, first;
+    __device__ __forceinline__ void claim(const Rect* rects, const Work* work, int n_work, int* ctr) {
+        w = atomicAdd(ctr, 1);
+        if (w < n_work) {
+            const Work wk = work[w];
+            const Rect& r = rects[wk.rect];
+            Wa = r.W_a;
+            ma = r.map_a;
+            mb = r.map_b;
+            ti = wk.ti;
+            tj = wk.tj;
+            kc = wk.k0;
+            k1 = wk.k1;
+            ka = (int)(((int64_t)kc * kBK) % Wa);
+            first = 1;
         }
-    }
-    __device__ __forceinline__ void advance(const K2Params& prm, const int4* tiles, int n_tiles, int* tile_ctr) {
-        ++kc;
-        ka += BK;
-        if (ka == Wa) ka = 0;
-        if (kc == nk) claim(prm, tiles, n_tiles, tile_ctr);
     }
 };
 
 // Thread 0: fill buffer `buf` with the cursor's next chunk (TMA), or post the end marker once.
-template <int BK>
-__device__ __forceinline__ void issue_next(const K2Params& prm, ChunkCursor<BK>& c, const int4* tiles, int n_tiles,
-                                           int* tile_ctr, uint32_t* stages, int buf, uint64_t* full, int2* meta,
-                                           bool& end_sent) {
-    if (c.valid(n_tiles)) {
-        uint32_t* sA = stages + buf * Chunk<BK>::kStageSmem;
-        uint32_t* sB = sA + BK * kBM;
-        meta[buf] = make_int2(c.t, c.kc);  // published by the mbarrier's release/acquire
-        mbar_expect_tx(&full[buf], Chunk<BK>::kStageWords * 4);
-        tma_load_2d(sA, &prm.maps[c.td.x], c.td.z * kBM, c.ka, &full[buf]);  // B_i[w mod W_i]
-        tma_load_2d(sB, &prm.maps[c.td.y], c.td.w * kBN, c.kc * BK, &full[buf]);
-        c.advance(prm, tiles, n_tiles, tile_ctr);
+__device__ __forceinline__ void issue_next(const K2Maps& prm, Cursor& c, const Rect* rects, const Work* work,
+                                           int n_work, int* ctr, uint32_t* stages, int buf, uint64_t* full,
+                                           int2* meta, bool& end_sent) {
+    if (c.w < n_work) {
+        uint32_t* sA = stages + buf * kStageSmem;
+        uint32_t* sB = sA + kBK * kBM;
+        meta[buf] = make_int2(c.w, c.first);  // published by the mbarrier's release/acquire
+        mbar_expect_tx(&full[buf], kStageWords * 4);
+        tma_load_2d(sA, &prm.maps[c.ma], c.ti * kBM, c.ka, &full[buf]);  // B_i[w mod W_i]
+        tma_load_2d(sB, &prm.maps[c.mb], c.tj * kBN, c.kc * kBK, &full[buf]);
+        c.first = 0;
+        ++c.kc;
+        c.ka += kBK;
+        if (c.ka == c.Wa) c.ka = 0;
+        if (c.kc == c.k1) c.claim(rects, work, n_work, ctr);
     } else if (!end_sent) {
-        meta[buf] = make_int2(-1, 0);
+        meta[buf] = make_int2(-1, 1);
         mbar_arrive(&full[buf]);
         end_sent = true;
     }
 }
 
-// Candidate test c + f_i + f_j >= thr for the thread's 8 x 8 pairs and warp-aggregated append.
-__device__ __forceinline__ void tile_epilogue(const K2Params& prm, const int4 td, int tr, int tc, int lane,
-                                              const uint32_t (&acc)[8][8], const int32_t* __restrict__ f,
-                                              uint32_t thr, uint32_t use_f, Cand* __restrict__ out,
-                                              unsigned long long* __restrict__ ctr, int64_t cap) {
-    const int a = td.x, b = td.y;
-    const int na = prm.cls_n[a], nb = prm.cls_n[b];
-    const int fa = prm.cls_first[a], fb = prm.cls_first[b];
-    int rows[8], cols[8];
-    uint32_t fr[8], fc[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        rows[i] = td.z * kBM + (i < 4 ? 4 * tr + i : 64 + 4 * tr + (i - 4));
-        cols[i] = td.w * kBN + (i < 4 ? 4 * tc + i : 64 + 4 * tc + (i - 4));
-        fr[i] = (use_f && rows[i] < na) ? (uint32_t)__ldg(f + fa + rows[i]) : 0u;
-        fc[i] = (use_f && cols[i] < nb) ? (uint32_t)__ldg(f + fb + cols[i]) : 0u;
-    }
-    uint64_t mask = 0;
-    int cnt = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const bool valid = rows[i] < na && cols[j] < nb && (a != b || rows[i] < cols[j]);
-            const uint64_t c = acc[i][j] >> 7;
-            if (valid && c + fr[i] + fc[j] >= thr) {
-                mask |= 1ull << (i * 8 + j);
-                ++cnt;
-            }
-        }
+__device__ __forceinline__ void append_candidates(uint64_t mask, int cnt, int lane, const int (&rows)[8],
+                                                  const int (&cols)[8], int fa, int fb, const uint32_t (&acc)[8][8],
+                                                  Cand* __restrict__ out, unsigned long long* __restrict__ ctr,
+                                                  int64_t cap) {
     int incl = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -234,31 +198,89 @@ __device__ __forceinline__ void tile_epilogue(const K2Params& prm, const int4 td
             }
 }
 
+// End of a work item: ordinary rectangles test c + f_i + f_j >= thr and append; accumulated ones
+// add the partial counts to their counters (4 adjacent virtual columns of one item pre-summed).
+__device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int tr, int tc, int lane,
+                                              const uint32_t (&acc)[8][8], uint32_t* __restrict__ cnt,
+                                              const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f,
+                                              Cand* __restrict__ out, unsigned long long* __restrict__ ctr,
+                                              int64_t cap) {
+    int rows[8], cols[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        rows[i] = ti * kBM + (i < 4 ? 4 * tr + i : 64 + 4 * tr + (i - 4));
+        cols[i] = tj * kBN + (i < 4 ? 4 * tc + i : 64 + 4 * tc + (i - 4));
+    }
+    if (r.acc) {
+        uint32_t* base = cnt + r.cnt_off;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (rows[i] >= r.n_rows) continue;
+            uint32_t* row = base + (int64_t)rows[i] * r.n_cols_real;
+            if (r.R >= 4) {  // columns 4g..4g+3 are 4 virtual columns of the same item
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    if (cols[4 * g] >= r.n_cols) continue;
+                    const uint32_t s = (acc[i][4 * g] >> 7) + (acc[i][4 * g + 1] >> 7) + (acc[i][4 * g + 2] >> 7) +
+                                       (acc[i][4 * g + 3] >> 7);
+                    if (s) atomicAdd(row + cols[4 * g] / r.R, s);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (cols[j] >= r.n_cols || (r.diag && rows[i] >= cols[j])) continue;
+                    const uint32_t s = acc[i][j] >> 7;
+                    if (s) atomicAdd(row + cols[j] / r.R, s);
+                }
+            }
+        }
+        return;
+    }
+    uint32_t fr[8], fc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        fr[i] = (use_f && rows[i] < r.n_rows) ? (uint32_t)__ldg(f + r.row_first + rows[i]) : 0u;
+        fc[i] = (use_f && cols[i] < r.n_cols) ? (uint32_t)__ldg(f + r.col_first + cols[i]) : 0u;
+    }
+    uint64_t mask = 0;
+    int n = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const bool valid = rows[i] < r.n_rows && cols[j] < r.n_cols && (!r.diag || rows[i] < cols[j]);
+            const uint64_t c = acc[i][j] >> 7;
+            if (valid && c + fr[i] + fc[j] >= thr) {
+                mask |= 1ull << (i * 8 + j);
+                ++n;
+            }
+        }
+    append_candidates(mask, n, lane, rows, cols, r.row_first, r.col_first, acc, out, ctr, cap);
+}
+
 // 256 threads = 8 warps; thread (tr, tc) owns rows {4tr..4tr+3, 64+4tr..+3} x cols {4tc.., 64+4tc..}
 // of the 128 x 128 tile.  Thread 0 also drives TMA: after the per-chunk barrier every warp has
-// finished the previous chunk, so that buffer is refilled with the chunk STAGES-1 ahead.
-template <int BK, int STAGES, int MINB, bool PF>
-__global__ void __launch_bounds__(kThreads, MINB)
-    k2_tiled(const __grid_constant__ K2Params prm, const int4* __restrict__ tiles, int n_tiles, int* tile_ctr,
-             const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f, Cand* __restrict__ out,
-             unsigned long long* __restrict__ ctr, int64_t cap) {
+// finished the previous chunk, so that buffer is refilled with the chunk kStages-1 ahead.
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    k2_tiled(const __grid_constant__ K2Maps prm, const Rect* __restrict__ rects, const Work* __restrict__ work,
+             int n_work, int* work_ctr, uint32_t* __restrict__ cnt, const int32_t* __restrict__ f, uint32_t thr,
+             uint32_t use_f, Cand* __restrict__ out, unsigned long long* __restrict__ ctr, int64_t cap) {
     extern __shared__ __align__(1024) uint32_t smem_raw[];
     uint32_t* stages = smem_raw;  // keep the shared address space visible to the compiler (LDS, not LD)
-    constexpr int kStageWords = Chunk<BK>::kStageWords, kStageSmem = Chunk<BK>::kStageSmem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(stages + STAGES * kStageSmem);
-    __shared__ int2 meta[STAGES];
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kStageSmem);
+    __shared__ int2 meta[kStages];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    ChunkCursor<BK> pre;  // prefetch cursor (thread 0 only)
+    Cursor pre;  // prefetch cursor (thread 0 only)
     bool end_sent = false;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        pre.claim(prm, tiles, n_tiles, tile_ctr);
-        for (int s = 0; s < STAGES - 1; ++s)
-            issue_next(prm, pre, tiles, n_tiles, tile_ctr, stages, s, full, meta, end_sent);
+        pre.claim(rects, work, n_work, work_ctr);
+        for (int s = 0; s < kStages - 1; ++s)
+            issue_next(prm, pre, rects, work, n_work, work_ctr, stages, s, full, meta, end_sent);
     }
     __syncthreads();
 
@@ -269,24 +291,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0;
-    int4 td = make_int4(0, 0, 0, 0);
-    bool have_tile = false;
+    int cur = -1;
     for (uint32_t g = 0;; ++g) {
-        const int buf = (int)(g % STAGES);
-        mbar_wait(&full[buf], (g / STAGES) & 1u);
+        const int buf = (int)(g % kStages);
+        mbar_wait(&full[buf], (g / kStages) & 1u);
         const int2 mt = meta[buf];
-        if (mt.y == 0 && have_tile) {  // a new tile (or the end) begins: finish the previous one
-            tile_epilogue(prm, td, tr, tc, lane, acc, f, thr, use_f, out, ctr, cap);
+        if (mt.y && cur >= 0) {  // a new work item (or the end) begins: finish the previous one
+            const Work wk = work[cur];
+            work_epilogue(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, thr, use_f, out, ctr, cap);
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[i][j] = 0;
         }
         if (mt.x < 0) break;
-        if (mt.y == 0) {
-            td = tiles[mt.x];
-            have_tile = true;
-        }
+        cur = mt.x;
         uint32_t* sA = stages + buf * kStageSmem;
         {  // derive the indicator-mask plane x & 0x80808080 once per chunk (not once per thread)
             const uint4* src = reinterpret_cast<const uint4*>(sA);
@@ -303,29 +322,66 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         __syncthreads();  // masks visible; every warp is done with the previous chunk's buffer
         if (threadIdx.x == 0)
-            issue_next(prm, pre, tiles, n_tiles, tile_ctr, stages, (int)((g + STAGES - 1) % STAGES), full, meta,
-                       end_sent);
-        const uint32_t* sB = sA + BK * kBM;
+            issue_next(prm, pre, rects, work, n_work, work_ctr, stages, (int)((g + kStages - 1) % kStages), full,
+                       meta, end_sent);
+        const uint32_t* sB = sA + kBK * kBM;
         const uint32_t* mA = sA + kStageWords;
-        const uint32_t* mB = mA + BK * kBM;
-        if (PF) {
-            Ops cur, nxt;
-            load_ops(cur, sA, sB, mA, mB, 0, tr, tc);
-#pragma unroll 8
-            for (int k = 0; k < BK; ++k) {
-                if (k + 1 < BK) load_ops(nxt, sA, sB, mA, mB, k + 1, tr, tc);  // software pipelining
-                compute_ops(cur, acc);
-                cur = nxt;
-            }
-        } else {
+        const uint32_t* mB = mA + kBK * kBM;
 #pragma unroll 2
-            for (int k = 0; k < BK; ++k) {
-                Ops cur;
-                load_ops(cur, sA, sB, mA, mB, k, tr, tc);
-                compute_ops(cur, acc);
+        for (int k = 0; k < kBK; ++k) {
+            Ops o;
+            load_ops(o, sA, sB, mA, mB, k, tr, tc);
+            compute_ops(o, acc);
+        }
+    }
+}
+
+// Accumulated rectangles: one CTA per owned tile row; candidate test on the summed counters.
+__global__ void __launch_bounds__(256) k2_acc_threshold(const AccUnit* __restrict__ units,
+                                                        const Rect* __restrict__ rects,
+                                                        const uint32_t* __restrict__ cnt,
+                                                        const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f,
+                                                        Cand* __restrict__ out, unsigned long long* __restrict__ ctr,
+                                                        int64_t cap) {
+    const AccUnit u = units[blockIdx.x];
+    const Rect r = rects[u.rect];
+    const int r0 = u.ti * kTile;
+    const int nr = min(kTile, r.n_rows - r0);
+    const int64_t total = (int64_t)nr * r.n_cols_real;
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+        const int row = r0 + (int)(e / r.n_cols_real);
+        const int col = (int)(e % r.n_cols_real);
+        if (r.diag && col <= row) continue;
+        const uint32_t c = cnt[r.cnt_off + (int64_t)row * r.n_cols_real + col];
+        uint64_t t = c;
+        if (use_f) t += (uint32_t)f[r.row_first + row] + (uint32_t)f[r.col_first + col];
+        if (t >= thr) {
+            const unsigned long long at = atomicAdd(ctr, 1ull);
+            if ((int64_t)at < cap) {
+                Cand cd;
+                cd.i = (uint32_t)(r.row_first + row);
+                cd.j = (uint32_t)(r.col_first + col);
+                cd.c = c;
+                out[at] = cd;
             }
         }
     }
+}
+
+// Virtual copy of class b for period W_a: dst[k * vpad + v] = word (rep W_a + k) of item j,
+// v = j R + rep; padding columns are ⊥ words.
+__global__ void k_virtualize(const uint32_t* __restrict__ src, int32_t src_npad, int32_t n_b, int32_t W_a, int32_t R,
+                             int32_t vpad, uint32_t* __restrict__ dst) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)W_a * vpad) return;
+    const int k = (int)(idx / vpad);
+    const int v = (int)(idx - (int64_t)k * vpad);
+    uint32_t word = kNullWord;
+    if (v < n_b * R) {
+        const int j = v / R, rep = v - (v / R) * R;
+        word = src[((int64_t)rep * W_a + k) * src_npad + j];
+    }
+    dst[idx] = word;
 }
 
 // ------------------------------------------------------------------ simple kernel (one thread per pair)
@@ -416,119 +472,159 @@ void plan_tiles(const std::vector<ClassInfo>& cls, int tile_m, int part, int n_p
         }
 }
 
-// K2 variant (BATMAP_K2_VARIANT=0|1 overrides, for measurement): 0 = one CTA/SM, 32-word chunks,
-// register-prefetched operands; 1 = two CTAs/SM (16 warps/SM), 16-word chunks.
-static int k2_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("BATMAP_K2_VARIANT");
-        v = e ? atoi(e) : 1;
-    }
-    return v;
-}
-
 static batmap_status ensure_cand(batmap_collection* h, int64_t need, cudaStream_t st) {
     return ensure(&h->cand_d, &h->cand_cap, need, st);
+}
+
+static bool env_off(const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] == '0';
+}
+
+static batmap_status encode_map(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const uint32_t* base,
+                                int64_t n_pad, int64_t W) {
+    cuuint64_t dims[2] = {(cuuint64_t)n_pad, (cuuint64_t)W};
+    cuuint64_t strides[1] = {(cuuint64_t)n_pad * 4};
+    cuuint32_t box[2] = {(cuuint32_t)kBM, (cuuint32_t)kBK};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return BATMAP_E_CUDA;
+    }
+    return BATMAP_OK;
+}
+
+static batmap_status run_simple(batmap_collection* h, const Selection& sel, uint32_t threshold, int part, int n_parts,
+                                uint32_t use_f, cudaStream_t st, int64_t* n_cand) {
+    TileList tl;
+    plan_tiles(sel.classes, 16, part, n_parts, &tl);
+    const int64_t n_tiles = (int64_t)tl.tiles.size();
+    int64_t wc = 0;
+    for (const int4& t : tl.tiles) {
+        const ClassInfo &A = sel.classes[t.x], &B = sel.classes[t.y];
+        const int64_t rows = std::min<int64_t>(16, A.n - (int64_t)t.z * 16);
+        const int64_t cols = std::min<int64_t>(16, B.n - (int64_t)t.w * 16);
+        wc += ((t.x == t.y && t.z == t.w) ? rows * (rows - 1) / 2 : rows * cols) * B.W;
+    }
+    h->stats.word_compares = wc;
+    h->stats.tile_compares = tl.work;
+    h->stats.k2_kind = 2;
+    h->stats.k2_grid = (int32_t)n_tiles;
+    if (n_tiles == 0) return BATMAP_OK;
+    std::vector<SimpleClass> sc(sel.classes.size());
+    for (size_t a = 0; a < sel.classes.size(); ++a)
+        sc[a] = {sel.classes[a].word_off, sel.classes[a].n, sel.classes[a].n_pad, sel.classes[a].W,
+                 (int32_t)sel.classes[a].first};
+    int4* tiles_d = nullptr;
+    SimpleClass* scls_d = nullptr;
+    BM_TRY(dalloc_t(&tiles_d, n_tiles, st));
+    BM_TRY(dalloc_t(&scls_d, (int64_t)sc.size(), st));
+    BM_CUDA(cudaMemcpyAsync(tiles_d, tl.tiles.data(), n_tiles * sizeof(int4), cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaMemcpyAsync(scls_d, sc.data(), sc.size() * sizeof(SimpleClass), cudaMemcpyHostToDevice, st));
+    batmap_status rc = BATMAP_OK;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, sizeof(unsigned long long), st));
+        rec(h, EV_K20, st);
+        k2_simple<<<(unsigned)n_tiles, dim3(16, 16), 0, st>>>(sel.arena, scls_d, tiles_d, sel.f, threshold, use_f,
+                                                             h->cand_d, h->ctr_d, h->cand_cap);
+        rec(h, EV_K21, st);
+        h->launches += 1;
+        BM_CUDA(cudaGetLastError());
+        unsigned long long cnt = 0;
+        BM_CUDA(cudaMemcpyAsync(&cnt, h->ctr_d, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        *n_cand = (int64_t)cnt;
+        if ((int64_t)cnt <= h->cand_cap) break;
+        rc = ensure_cand(h, (int64_t)cnt, st);
+        if (rc != BATMAP_OK) break;
+    }
+    dfree(tiles_d, st);
+    dfree(scls_d, st);
+    return rc;
 }
 
 batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t threshold, int part,
                             int n_parts, uint32_t flags, cudaStream_t st, int64_t* n_cand) {
     *n_cand = 0;
     if (sel.n_sel < 2) return BATMAP_OK;
-    bool simple = (flags & BATMAP_PAIRS_SIMPLE) != 0;
-    for (const ClassInfo& c : sel.classes)
-        if (c.W % 32 != 0 || c.W >= kMaxTiledW) simple = true;
-    if ((int)sel.classes.size() > kMaxClasses) simple = true;
-    PFN_cuTensorMapEncodeTiled_v12000 enc = simple ? nullptr : tensor_map_encoder();
-    if (!simple && !enc) simple = true;
-
-    TileList tl;
-    const int tm = simple ? 16 : kBM;
-    plan_tiles(sel.classes, tm, part, n_parts, &tl);
-    const int64_t n_tiles = (int64_t)tl.tiles.size();
-    {  // algorithmic work of this part: sum over its pairs of max(W_i, W_j)
-        int64_t wc = 0;
-        for (const int4& t : tl.tiles) {
-            const ClassInfo &A = sel.classes[t.x], &B = sel.classes[t.y];
-            const int64_t rows = std::min<int64_t>(tm, A.n - (int64_t)t.z * tm);
-            const int64_t cols = std::min<int64_t>(tm, B.n - (int64_t)t.w * tm);
-            const int64_t pairs = (t.x == t.y && t.z == t.w) ? rows * (rows - 1) / 2 : rows * cols;
-            wc += pairs * B.W;
-        }
-        h->stats.word_compares = wc;
-        h->stats.tile_compares = tl.work;
-        h->stats.k2_kind = simple ? 2 : 1;
-        h->stats.k2_grid = simple ? (int32_t)n_tiles
-                                  : (int32_t)std::min<int64_t>(n_tiles, (k2_variant() == 0 ? 1 : 2) * h->num_sms);
-    }
-    if (n_tiles == 0) return BATMAP_OK;
-    int4* tiles_d = nullptr;
-    BM_TRY(dalloc_t(&tiles_d, n_tiles, st));
-    BM_CUDA(cudaMemcpyAsync(tiles_d, tl.tiles.data(), n_tiles * sizeof(int4), cudaMemcpyHostToDevice, st));
     if (!h->ctr_d) BM_TRY(dalloc_t(&h->ctr_d, 2, st));
     if (h->cand_cap == 0) BM_TRY(ensure_cand(h, std::max<int64_t>(1 << 20, sel.n_sel * 16), st));
     const uint32_t use_f = (flags & BATMAP_PAIRS_RAW) ? 0u : 1u;
+    bool simple = (flags & BATMAP_PAIRS_SIMPLE) != 0;
+    for (const ClassInfo& c : sel.classes)
+        if (c.W % kBK != 0 || c.W >= kMaxTiledW || c.W < kBK) simple = true;
+    PFN_cuTensorMapEncodeTiled_v12000 enc = simple ? nullptr : tensor_map_encoder();
+    if (!enc) simple = true;
+    const int C = (int)sel.classes.size();
+    if (C > kMaxMaps) simple = true;
+    if (simple) return run_simple(h, sel, threshold, part, n_parts, use_f, st, n_cand);
 
-    SimpleClass* scls_d = nullptr;
-    K2Params* prm = nullptr;
-    if (simple) {
-        std::vector<SimpleClass> sc(sel.classes.size());
-        for (size_t a = 0; a < sel.classes.size(); ++a)
-            sc[a] = {sel.classes[a].word_off, sel.classes[a].n, sel.classes[a].n_pad, sel.classes[a].W,
-                     (int32_t)sel.classes[a].first};
-        BM_TRY(dalloc_t(&scls_d, (int64_t)sc.size(), st));
-        BM_CUDA(cudaMemcpyAsync(scls_d, sc.data(), sc.size() * sizeof(SimpleClass), cudaMemcpyHostToDevice, st));
-        BM_CUDA(cudaStreamSynchronize(st));  // sc is a host temporary
-    } else {
-        prm = new K2Params();
-        for (size_t a = 0; a < sel.classes.size(); ++a) {
-            const ClassInfo& c = sel.classes[a];
-            cuuint64_t dims[2] = {(cuuint64_t)c.n_pad, (cuuint64_t)c.W};
-            cuuint64_t strides[1] = {(cuuint64_t)c.n_pad * 4};
-            cuuint32_t box[2] = {(cuuint32_t)kBM, (cuuint32_t)(k2_variant() == 0 ? 32 : 16)};
-            cuuint32_t estr[2] = {1, 1};
-            CUresult r = enc(&prm->maps[a], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
-                             const_cast<uint32_t*>(sel.arena + c.word_off), dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) {
-                delete prm;
-                dfree(tiles_d, st);
-                set_error("cuTensorMapEncodeTiled failed (%d) for class %zu", (int)r, a);
-                return BATMAP_E_CUDA;
-            }
-            prm->cls_n[a] = c.n;
-            prm->cls_W[a] = c.W;
-            prm->cls_first[a] = (int32_t)c.first;
-        }
-        static bool attr_set = false;
-        if (!attr_set) {
-            BM_CUDA(cudaFuncSetAttribute(k2_tiled<32, 3, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_bytes<32, 3>()));
-            BM_CUDA(cudaFuncSetAttribute(k2_tiled<16, 3, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_bytes<16, 3>()));
-            attr_set = true;
-        }
-    }
-    batmap_status rc = BATMAP_OK;
-    int* tile_ctr = reinterpret_cast<int*>(h->ctr_d + 1);
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, 2 * sizeof(unsigned long long), st));  // [1] = tile counter
-        rec(h, EV_K20, st);
+    Plan pl;
+    const int grid_cap = kMinBlocks * h->num_sms;
+    plan_work(sel.classes, part, n_parts, grid_cap, !env_off("BATMAP_K2_VIRTUAL"), !env_off("BATMAP_K2_SPLIT"), &pl);
+    if (C + (int)pl.virt.size() > kMaxMaps) plan_work(sel.classes, part, n_parts, grid_cap, false, true, &pl);
+    const int64_t n_work = (int64_t)pl.work.size();
+    h->stats.word_compares = pl.word_compares;
+    h->stats.tile_compares = pl.tile_compares;
+    h->stats.k2_kind = 1;
+    h->stats.k2_grid = (int32_t)std::min<int64_t>(n_work, grid_cap);
+    if (n_work == 0) return BATMAP_OK;
+
+    // virtual copies of the wide classes of skinny rectangles
+    if (pl.virt_words) BM_TRY(ensure(&h->virt_d, &h->virt_cap, pl.virt_words, st));
+    for (const VirtCopy& v : pl.virt) {
+        const ClassInfo& B = sel.classes[v.cls_b];
+        const int64_t cnt = (int64_t)v.W_a * v.vpad;
+        k_virtualize<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(sel.arena + B.word_off, B.n_pad, B.n, v.W_a, v.R,
+                                                                    v.vpad, h->virt_d + v.dst_word_off);
         h->launches += 1;
-        if (simple) {
-            k2_simple<<<(unsigned)n_tiles, dim3(16, 16), 0, st>>>(sel.arena, scls_d, tiles_d, sel.f, threshold, use_f,
-                                                                 h->cand_d, h->ctr_d, h->cand_cap);
-        } else if (k2_variant() == 0) {
-            const int grid = (int)std::min<int64_t>(n_tiles, h->num_sms);
-            k2_tiled<32, 3, 1, true><<<grid, kThreads, smem_bytes<32, 3>(), st>>>(
-                *prm, tiles_d, (int)n_tiles, tile_ctr, sel.f, threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
-        } else {
-            const int grid = (int)std::min<int64_t>(n_tiles, 2 * h->num_sms);
-            k2_tiled<16, 3, 2, false><<<grid, kThreads, smem_bytes<16, 3>(), st>>>(
-                *prm, tiles_d, (int)n_tiles, tile_ctr, sel.f, threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
-        }
+    }
+    K2Maps* prm = new K2Maps();
+    batmap_status rc = BATMAP_OK;
+    for (int a = 0; a < C && rc == BATMAP_OK; ++a)
+        rc = encode_map(enc, &prm->maps[a], sel.arena + sel.classes[a].word_off, sel.classes[a].n_pad,
+                        sel.classes[a].W);
+    for (size_t k = 0; k < pl.virt.size() && rc == BATMAP_OK; ++k)
+        rc = encode_map(enc, &prm->maps[C + k], h->virt_d + pl.virt[k].dst_word_off, pl.virt[k].vpad, pl.virt[k].W_a);
+    if (rc != BATMAP_OK) {
+        delete prm;
+        return rc;
+    }
+    Rect* rects_d = nullptr;
+    Work* work_d = nullptr;
+    AccUnit* units_d = nullptr;
+    BM_TRY(dalloc_t(&rects_d, (int64_t)pl.rects.size(), st));
+    BM_TRY(dalloc_t(&work_d, n_work, st));
+    BM_TRY(dalloc_t(&units_d, (int64_t)std::max<size_t>(pl.units.size(), 1), st));
+    BM_CUDA(cudaMemcpyAsync(rects_d, pl.rects.data(), pl.rects.size() * sizeof(Rect), cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaMemcpyAsync(work_d, pl.work.data(), n_work * sizeof(Work), cudaMemcpyHostToDevice, st));
+    if (!pl.units.empty())
+        BM_CUDA(cudaMemcpyAsync(units_d, pl.units.data(), pl.units.size() * sizeof(AccUnit), cudaMemcpyHostToDevice,
+                                st));
+    if (pl.cnt_entries) BM_TRY(ensure(&h->cnt_d, &h->cnt_cap, pl.cnt_entries, st));
+    static bool attr_set = false;
+    if (!attr_set) {
+        BM_CUDA(cudaFuncSetAttribute(k2_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+        attr_set = true;
+    }
+    int* work_ctr = reinterpret_cast<int*>(h->ctr_d + 1);
+    const int grid = (int)std::min<int64_t>(n_work, grid_cap);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, 2 * sizeof(unsigned long long), st));  // [1] = work counter
+        if (pl.cnt_entries) BM_CUDA(cudaMemsetAsync(h->cnt_d, 0, pl.cnt_entries * sizeof(uint32_t), st));
+        rec(h, EV_K20, st);
+        k2_tiled<<<grid, kThreads, kSmemBytes, st>>>(*prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, sel.f,
+                                                     threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
         rec(h, EV_K21, st);
+        h->launches += 1;
+        if (!pl.units.empty()) {
+            k2_acc_threshold<<<(unsigned)pl.units.size(), 256, 0, st>>>(units_d, rects_d, h->cnt_d, sel.f, threshold,
+                                                                        use_f, h->cand_d, h->ctr_d, h->cand_cap);
+            h->launches += 1;
+        }
         cudaError_t le = cudaGetLastError();
         if (le != cudaSuccess) {
             set_error("intersection kernel launch: %s", cudaGetErrorString(le));
@@ -544,8 +640,9 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         if (rc != BATMAP_OK) break;
     }
     delete prm;
-    dfree(scls_d, st);
-    dfree(tiles_d, st);
+    dfree(rects_d, st);
+    dfree(work_d, st);
+    dfree(units_d, st);
     return rc;
 }
 

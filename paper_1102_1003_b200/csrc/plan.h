@@ -1,0 +1,59 @@
+// plan.h -- host-side work planner of ★K2 (shared by intersect.cu and the C ABI's plan hook).
+#pragma once
+
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace bm {
+
+constexpr int kTile = 128;   // tile edge in items (rows and columns)
+constexpr int kChunk = 16;   // words per k-chunk (the TMA box height)
+
+// A rectangle of the pair triangle: the rows are the items of class a (period W_a), the
+// columns those of class b.  A "virtualised" rectangle (R > 1) views each class-b BatMap of
+// W_b = R W_a words as R virtual columns of W_a words each (column v = j R + rep holds words
+// [rep W_a, (rep+1) W_a) of item j), so skinny rectangles (few wide items) tile densely:
+// c_ij = sum_rep c(i, (j, rep))  (the wrap-around of P:273-274 unrolled).
+struct Rect {
+    int32_t cls_a, cls_b;         // selection classes
+    int32_t map_a, map_b;         // tensor-map indices (map_b = virtual copy when R > 1)
+    int32_t W_a, W;               // row period; K length of the rectangle (words)
+    int32_t n_rows, n_cols;       // n_cols counts virtual columns when R > 1
+    int32_t row_first, col_first; // selection index of the first row / first real column item
+    int32_t diag, R;              // diag: a == b (pairs i < j only)
+    int32_t acc, n_cols_real;     // acc: partial counts accumulate into cnt[] (virtual or split-K)
+    int64_t cnt_off;              // offset of this rectangle's n_rows x n_cols_real counters
+};
+
+struct Work {   // one work item: tile (ti, tj) of a rectangle over k-chunks [k0, k1)
+    int32_t rect, ti, tj, k0, k1, pad;
+};
+
+struct AccUnit {  // a tile row (rect, ti) of an accumulated rectangle owned by this part
+    int32_t rect, ti;
+};
+
+struct VirtCopy {  // materialise class b's BatMaps as R virtual columns of period W_a
+    int32_t cls_b, W_a, R, vpad;
+    int64_t dst_word_off;  // into the virtual-copy scratch arena
+};
+
+struct Plan {
+    std::vector<Rect> rects;
+    std::vector<Work> work;       // this part's work items, longest first
+    std::vector<AccUnit> units;   // this part's tile rows of accumulated rectangles
+    std::vector<VirtCopy> virt;
+    int64_t virt_words = 0;
+    int64_t cnt_entries = 0;
+    int64_t word_compares = 0;    // algorithmic: sum over this part's pairs of max(W_i, W_j)
+    int64_t tile_compares = 0;    // executed: sum over work items of 128 x 128 x words
+};
+
+// grid_cap: CTAs the kernel keeps resident (the split-K target is ~4 work items per CTA).
+void plan_work(const std::vector<ClassInfo>& cls, int part, int n_parts, int grid_cap, bool allow_virtual,
+               bool allow_split, Plan* out);
+
+}  // namespace bm

@@ -68,53 +68,97 @@ def test_argument_errors_without_device():
     lib.batmap_destroy(None)
 
 
-def _all_tiles(class_n, tile_m):
-    out = set()
+def _collect(class_n, class_w, n_parts, grid_cap=0):
+    from paper_1102_1003_b200 import plan_work
+
+    parts = [plan_work(class_n, class_w, p, n_parts, grid_cap) for p in range(n_parts)]
+    return parts
+
+
+@pytest.mark.parametrize("class_n,class_w", [([1000], [96]), ([780, 220], [192, 384]),
+                                             ([2000, 40, 30, 20, 10, 5, 3, 1], [96 * 2 ** k for k in range(8)]),
+                                             ([300, 200, 120, 90, 50, 12], [96 * 2 ** k for k in range(6)]),
+                                             ([5], [96])])
+@pytest.mark.parametrize("n_parts", [1, 2, 3, 8])
+def test_plan_work_partition_exact(class_n, class_w, n_parts):
+    """Union over parts = every k-chunk of every tile of the pair triangle exactly once (P:464-467);
+    tile rows of accumulated rectangles stay on one part; algorithmic work adds up to
+    sum_{i<j} max(W_i, W_j)."""
+    parts = _collect(class_n, class_w, n_parts)
+    chunks = {}
+    rect_R = {}
+    row_part = {}
+    for p, (items, wc, tcmp) in enumerate(parts):
+        assert tcmp == int(sum((k1 - k0) * 16 * 128 * 128 for _, _, _, _, k0, k1, _, _ in items.tolist()))
+        for a, b, ti, tj, k0, k1, R, acc in items.tolist():
+            assert a <= b and k0 < k1
+            rect_R.setdefault((a, b), (R, acc))
+            assert rect_R[(a, b)] == (R, acc)
+            for k in range(k0, k1):
+                key = (a, b, ti, tj, k)
+                assert key not in chunks
+                chunks[key] = p
+            if acc:
+                assert row_part.setdefault((a, b, ti), p) == p
+    expect = set()
     C = len(class_n)
     for a in range(C):
         for b in range(a, C):
-            ta, tb = -(-class_n[a] // tile_m), -(-class_n[b] // tile_m)
+            if class_n[a] == 0 or class_n[b] == 0 or (a == b and class_n[a] < 2):
+                continue
+            R, _ = rect_R[(a, b)]
+            W = class_w[b] // R
+            ta = -(-class_n[a] // 128)
+            tb = -(-(class_n[b] * R) // 128)
             for i in range(ta):
                 for j in range(i if a == b else 0, tb):
-                    out.add((a, b, i, j))
-    return out
+                    for k in range(W // 16):
+                        expect.add((a, b, i, j, k))
+    assert set(chunks) == expect
+    wc_total = sum(wc for _, wc, _ in parts)
+    closed = sum(class_n[a] * class_n[b] * class_w[b] for a in range(C) for b in range(a + 1, C))
+    closed += sum(n * (n - 1) // 2 * w for n, w in zip(class_n, class_w))
+    assert wc_total == closed
 
 
-@pytest.mark.parametrize("class_n,class_w", [([1000], [192]), ([7800, 2200], [1536, 3072]),
-                                             ([99835, 40, 30, 20, 10, 5, 3, 1], [6144 * 2 ** k for k in range(8)]),
-                                             ([5], [96])])
-@pytest.mark.parametrize("n_parts", [1, 2, 3, 8])
-def test_plan_tiles_partition_exact(class_n, class_w, n_parts):
-    from paper_1102_1003_b200 import plan_tiles
-
-    seen = []
-    works = []
-    for part in range(n_parts):
-        tiles, work = plan_tiles(class_n, class_w, part, n_parts)
-        seen.extend(map(tuple, tiles.tolist()))
-        works.append(work)
-        assert work == sum(128 * 128 * class_w[t[1]] for t in tiles.tolist())
-    assert len(seen) == len(set(seen))
-    assert set(seen) == _all_tiles(class_n, 128)
-    # round-robin over cost-sorted tiles: parts differ by at most one (largest) tile
-    biggest = 128 * 128 * max(class_w)
-    assert max(works) - min(works) <= biggest
+def test_plan_work_virtual_and_split():
+    """Skinny rectangles are virtualised (R = W_b / W_a) and long tiles split along k."""
+    parts = _collect([99835, 1], [6144, 6144 * 256], 1)
+    items = parts[0][0]
+    skinny = items[(items[:, 0] == 0) & (items[:, 1] == 1)]
+    assert (skinny[:, 6] == 256).all() and (skinny[:, 7] == 1).all()
+    items = _collect([50, 40], [24576, 49152], 1)[0][0]  # few long tiles -> split-K
+    assert (items[:, 7] == 1).any() and (items[:, 5] - items[:, 4] < 49152 // 16).any()
 
 
-def test_plan_tiles_covers_every_pair_once():
-    """Tiles (a<=b, diagonal tiles upper-triangular) cover each unordered pair exactly once."""
-    from paper_1102_1003_b200 import plan_tiles
-
-    class_n = [37, 20, 5]
+def test_plan_work_covers_every_pair_once():
+    """Expanding the work items (virtual columns, k-chunks) covers every word compare of every pair
+    i < j exactly once: c_ij = sum_{w < W_j} SWAR(B_j[w], B_i[w mod W_i])."""
+    class_n, class_w = [130, 7, 3], [16, 64, 256]
     first = np.cumsum([0] + class_n)
-    tiles, _ = plan_tiles(class_n, [96, 192, 384], 0, 1, tile_m=16)
+    items = _collect(class_n, class_w, 1)[0][0]
     cover = {}
-    for a, b, i, j in tiles.tolist():
-        for r in range(i * 16, min(class_n[a], i * 16 + 16)):
-            for c in range(j * 16, min(class_n[b], j * 16 + 16)):
-                if a == b and r >= c:
+    for a, b, ti, tj, k0, k1, R, acc in items.tolist():
+        Wv = class_w[b] // R
+        for r in range(ti * 128, min(class_n[a], ti * 128 + 128)):
+            for v in range(tj * 128, min(class_n[b] * R, tj * 128 + 128)):
+                j, rep = divmod(v, R)
+                if a == b and r >= j:
                     continue
-                key = (first[a] + r, first[b] + c)
-                cover[key] = cover.get(key, 0) + 1
+                key = (first[a] + r, first[b] + j)
+                for k in range(k0 * 16, k1 * 16):
+                    w = rep * Wv + k  # word of B_j
+                    cover[(key, w)] = cover.get((key, w), 0) + 1
     n = sum(class_n)
-    assert len(cover) == n * (n - 1) // 2 and set(cover.values()) == {1}
+    pairs = {(i, j) for i in range(n) for j in range(i + 1, n)}
+    assert {k for k, _ in cover} == pairs
+    assert set(cover.values()) == {1}
+    width = {}
+    for a in range(3):
+        for r in range(class_n[a]):
+            width[first[a] + r] = class_w[a]
+    per_pair = {}
+    for (key, w) in cover:
+        per_pair[key] = per_pair.get(key, 0) + 1
+    for (i, j), cnt in per_pair.items():
+        assert cnt == max(width[i], width[j])

@@ -24,15 +24,15 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1102_1003_b200 import plan_tiles
+        from paper_1102_1003_b200 import plan_work
         from paper_1102_1003_b200.dist import gather_triples
         import oracle
         from workloads import uniform
 
         # 1) the planner's share of this rank: gather every rank's tiles and check exact cover
         class_n, class_w = [7800, 2200], [1536, 3072]
-        tiles, work = plan_tiles(class_n, class_w, rank, world)
-        t = torch.as_tensor(tiles.astype(np.int32).reshape(-1, 4)[:, :3].copy())
+        items, wc, work = plan_work(class_n, class_w, rank, world)
+        t = torch.as_tensor(items[:, :3].copy())
         allt = gather_triples(t)
         w = torch.tensor([work], dtype=torch.int64)
         ws = [torch.zeros_like(w) for _ in range(world)]
@@ -68,9 +68,9 @@ def test_gather_and_partition_world2():
         p.join(timeout=60)
     assert all(r[0] == "ok" for r in res), res
     r0 = [r for r in res if r[1] is not None and r[1] != -1][0]
-    from paper_1102_1003_b200 import plan_tiles
+    from paper_1102_1003_b200 import plan_work
 
-    n_all = len(plan_tiles([7800, 2200], [1536, 3072], 0, 1)[0])
+    n_all = len(plan_work([7800, 2200], [1536, 3072], 0, 1)[0])
     assert r0[1] == n_all  # the ranks' tile lists cover the triangle exactly once
     assert abs(r0[2][0] - r0[2][1]) <= 128 * 128 * 3072  # balanced within one tile
     assert r0[3] is True  # gathered triples == the full result
