@@ -114,6 +114,7 @@ def _cpu_baseline(w, target_s: float = 8.0):
     """The oracle (sorted merge, P:59 / P:609-611) as it stands, on a bounded row sample."""
     import oracle
 
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     n = w.n
     items = np.arange(n, dtype=np.int32)
     t0 = time.perf_counter()
@@ -136,7 +137,8 @@ def run_reference(args, rank, world):
         return 0
     import oracle
 
-    w = _workload(args.config, 1, args.seed)
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))  # torchrun exports OMP_NUM_THREADS=1
+    w = _workload(args.config, world, args.seed)
     n = w.n
     items = np.arange(n, dtype=np.int32)
     # each step: a bounded row sample (~2-4 s) of the same workload
@@ -158,8 +160,8 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{w.name}: uniform n={w.n}, m={w.m}, p={w.meta.get('p')}, s={w.threshold}",
-                   "sample_rows": rows},
+        "config": {"workload": f"{w.name}: uniform tidlists, n={n} items (C2 n x sqrt(N)), m={w.m} transactions, "
+                               f"p={w.meta.get('p')}, threshold s={w.threshold}", "sample_rows": rows},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                          "sample": f"sorted-merge oracle, first {rows} of {n} items x all later items "
                                    f"({pairs} pair intersections) per step"},
