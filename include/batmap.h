@@ -205,6 +205,22 @@ batmap_status batmap_stats(batmap_handle h, batmap_stats_t* out);
  */
 batmap_status batmap_sort_triples(batmap_triple* triples, int64_t n, batmap_stream_t stream);
 
+/*
+ * batmap_dense_pair_supports -- NEXT-1 comparison path, NOT the BatMap method: the same triples
+ * computed from dense bitmaps, i.e. the integer matrix product X^T X of the
+ * m x n 0/1 incidence matrix on the tensor cores (cuBLASLt int8 GEMM, int32 accumulation, upper
+ * triangle in row blocks), thresholded and sorted by (i, j).  No handle, no failures.
+ *   offsets, tids [device] CSR as in batmap_build (valid tidlists assumed);
+ *   items [device] distinct caller ids or NULL (all); out [device] capacity records;
+ *   n_out [host] (set also on E_CAPACITY); gemm_ms [host] or NULL: device time of GEMM+threshold.
+ * Memory: n_sel x m bytes for X (E_NOMEM above 48 GB) plus one 512 MB block of X^T X.
+ * cuBLASLt is loaded on first use; E_CUDA if it cannot be loaded.
+ */
+batmap_status batmap_dense_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                                         int64_t n_transactions, const int32_t* items, int64_t n_sel,
+                                         uint32_t threshold, batmap_triple* out, int64_t capacity,
+                                         int64_t* n_out, double* gemm_ms, batmap_stream_t stream);
+
 /* ---------------------------------------------------------------- inspection / test hooks */
 
 /*

@@ -6,6 +6,7 @@ its thin binding (``batmap``), the multi-GPU gather (``dist``) and the build scr
 from .batmap import (  # noqa: F401
     BatMapError,
     Collection,
+    dense_pair_supports,
     load_library,
     mine_host,
     plan_work,

@@ -232,4 +232,8 @@ batmap_status run_finalize(batmap_collection* h, const Selection& sel, int64_t n
 batmap_status gather_selection(batmap_collection* h, const int32_t* items_d, int64_t n_sel,
                                cudaStream_t st, Selection* sel);
 batmap_status sort_triples(batmap_triple* t, int64_t n, cudaStream_t st);
+// dense.cu
+batmap_status dense_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t m,
+                                  const int32_t* items, int64_t n_sel, uint32_t threshold, batmap_triple* out,
+                                  int64_t capacity, int64_t* n_out, double* gemm_ms, cudaStream_t st);
 }  // namespace bm

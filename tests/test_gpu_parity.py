@@ -300,3 +300,28 @@ def test_c4_zipf_exact():
     w = make_config("C4")
     c, got = _check_exact(w.offsets, w.tids, w.m, w.threshold)
     assert c.info()["n_classes"] >= 6
+
+
+# ----------------------------------------------------------------------------- NEXT-1 dense bitmaps
+def _dense(off, tids, m, thr, items=None):
+    from paper_1102_1003_b200 import dense_pair_supports
+
+    t, ms = dense_pair_supports(torch.as_tensor(off).cuda(), torch.as_tensor(tids).cuda(), m, items=items, threshold=thr)
+    return _np(t), ms
+
+
+def test_dense_xtx_exact_small_and_subset():
+    w = make_config("C1", scale_items=0.3)
+    got, _ = _dense(w.offsets, w.tids, w.m, 0)
+    np.testing.assert_array_equal(got, oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=0))
+    w = make_config("C1")
+    items = np.random.default_rng(5).choice(w.n, size=333, replace=False).astype(np.int32)
+    got, _ = _dense(w.offsets, w.tids, w.m, 2, items=items)
+    np.testing.assert_array_equal(got, oracle.pairs_horizontal(w.offsets, w.tids, w.m, items=items, threshold=2))
+
+
+def test_dense_xtx_c2_equals_batmap():
+    w = make_config("C2")
+    got, ms = _dense(w.offsets, w.tids, w.m, w.threshold)
+    np.testing.assert_array_equal(got, oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=w.threshold))
+    assert ms > 0

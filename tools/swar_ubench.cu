@@ -47,8 +47,8 @@ __device__ __forceinline__ uint32_t step(uint32_t x, uint32_t y, uint32_t xm, ui
 
 // MASKS: 0 = compute x & M in registers per k, 1 = load from a second smem plane, 2 = no LDS in the
 // loop at all (register-resident operands perturbed per k: the compute ceiling)
-template <int V, int MASKS, int NT>
-__global__ void __launch_bounds__(NT, 1) bench(const uint32_t* __restrict__ g, int reps, uint32_t one,
+template <int V, int MASKS, int NT, int MINB = 1, int UNR = 4, int SYNC = 0>
+__global__ void __launch_bounds__(NT, MINB) bench(const uint32_t* __restrict__ g, int reps, uint32_t one,
                                                 uint32_t sh25, uint32_t* out, unsigned long long* cycles) {
     __shared__ __align__(16) uint32_t sA[16 * 128], sB[16 * 128], mA[16 * 128], mB[16 * 128];
     for (int i = threadIdx.x; i < 16 * 128; i += blockDim.x) {
@@ -79,7 +79,18 @@ __global__ void __launch_bounds__(NT, 1) bench(const uint32_t* __restrict__ g, i
     __syncthreads();
     unsigned long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
-#pragma unroll 4
+        if (SYNC) {  // per-chunk mask transform + barrier, as in k2_tiled
+            for (int i = threadIdx.x; i < 16 * 128 / 4; i += NT) {
+                uint4 v = reinterpret_cast<const uint4*>(sA)[i];
+                v.x &= 0x80808080u; v.y &= 0x80808080u; v.z &= 0x80808080u; v.w &= 0x80808080u;
+                reinterpret_cast<uint4*>(mA)[i] = v;
+                uint4 w = reinterpret_cast<const uint4*>(sB)[i];
+                w.x &= 0x80808080u; w.y &= 0x80808080u; w.z &= 0x80808080u; w.w &= 0x80808080u;
+                reinterpret_cast<uint4*>(mB)[i] = w;
+            }
+            __syncthreads();
+        }
+#pragma unroll UNR
         for (int k = 0; k < 16; ++k) {
             if (MASKS != 2) {
                 const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * 128 + 4 * tr);
@@ -122,16 +133,17 @@ __global__ void __launch_bounds__(NT, 1) bench(const uint32_t* __restrict__ g, i
     if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
 
-template <int V, int MASKS, int NT>
+template <int V, int MASKS, int NT, int MINB = 1, int UNR = 4, int SYNC = 0>
 void run(const char* name, const uint32_t* g, int sms, uint32_t* out, unsigned long long* cyc) {
     const int reps = 2000;
-    bench<V, MASKS, NT><<<sms, NT>>>(g, 10, 1u, 1u << 25, out, cyc);
+    sms *= MINB;  // MINB CTAs per SM
+    bench<V, MASKS, NT, MINB, UNR, SYNC><<<sms, NT>>>(g, 10, 1u, 1u << 25, out, cyc);
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    bench<V, MASKS, NT><<<sms, NT>>>(g, reps, 1u, 1u << 25, out, cyc);
+    bench<V, MASKS, NT, MINB, UNR, SYNC><<<sms, NT>>>(g, reps, 1u, 1u << 25, out, cyc);
     cudaEventRecord(e1);
     CK(cudaDeviceSynchronize());
     float ms;
@@ -142,10 +154,10 @@ void run(const char* name, const uint32_t* g, int sms, uint32_t* out, unsigned l
     for (auto v : c) mc += v;
     mc /= sms;
     const double per_block = (double)NT * 64.0 * 16.0 * reps;  // word-compares per block
-    printf("{\"variant\": \"%s\", \"threads\": %d, \"cmp_per_clk_per_sm\": %.2f, \"frac_of_32\": %.3f, "
-           "\"tcmp_per_s\": %.3f, \"ms\": %.2f, \"eff_mhz\": %.0f}\n",
-           name, NT, per_block / mc, per_block / mc / 32.0, per_block * sms / (ms * 1e-3) / 1e12, ms,
-           mc / (ms * 1e-3) / 1e6);
+    printf("{\"variant\": \"%s%s\", \"threads\": %d, \"ctas_per_sm\": %d, \"unroll\": %d, \"cmp_per_clk_per_sm\": %.2f, "
+           "\"frac_of_32\": %.3f, \"tcmp_per_s\": %.3f, \"ms\": %.2f, \"eff_mhz\": %.0f}\n",
+           name, SYNC ? "+sync" : "", NT, MINB, UNR, MINB * per_block / mc, MINB * per_block / mc / 32.0,
+           per_block * sms / (ms * 1e-3) / 1e12, ms, mc / (ms * 1e-3) / 1e6);
 }
 
 int main() {
@@ -163,17 +175,12 @@ int main() {
     uint32_t *g, *out;
     unsigned long long* cyc;
     CK(cudaMalloc(&g, h.size() * 4));
-    CK(cudaMalloc(&out, sms * 512 * 4));
-    CK(cudaMalloc(&cyc, sms * 8));
+    CK(cudaMalloc(&out, 4 * sms * 512 * 4));
+    CK(cudaMalloc(&cyc, 4 * sms * 8));
     CK(cudaMemcpy(g, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
-    run<0, 0, 256>("imad_idp4a/masks_in_regs", g, sms, out, cyc);
-    run<0, 1, 256>("imad_idp4a/masks_from_smem", g, sms, out, cyc);
-    run<0, 2, 256>("imad_idp4a/no_lds_ceiling", g, sms, out, cyc);
-    run<4, 1, 256>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
-    run<4, 2, 256>("iadd3_idp4a/no_lds_ceiling", g, sms, out, cyc);
-    run<0, 1, 384>("imad_idp4a/masks_from_smem", g, sms, out, cyc);
-    run<1, 0, 256>("imad_imadhi/masks_in_regs", g, sms, out, cyc);
-    run<2, 0, 256>("imad_leahi/masks_in_regs", g, sms, out, cyc);
-    run<3, 0, 256>("paper_popc", g, sms, out, cyc);
+    run<4, 1, 256, 2, 2>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run<4, 1, 256, 2, 2, 1>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run<4, 1, 256, 1, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run<4, 1, 256, 1, 4, 1>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
     return 0;
 }
