@@ -789,6 +789,8 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         }
         rec(h, EV_I1, st);
         BM_CUDA(cudaGetLastError());
+        // plan the intersection of the full selection on the host while the build kernels run
+        if (attempt == 0) BM_TRY(prepare_full_k2(h, 0, 1, st));
         unsigned long long Fh = 0;
         BM_CUDA(cudaMemcpyAsync(&Fh, fail_ctr, sizeof(Fh), cudaMemcpyDeviceToHost, st));
         BM_CUDA(cudaStreamSynchronize(st));

@@ -111,6 +111,10 @@ struct Selection {
 
 }  // namespace bm
 
+namespace bm {
+struct K2Prepared;
+}
+
 struct batmap_collection {
     int device = 0;
     int num_sms = 148;
@@ -154,9 +158,8 @@ struct batmap_collection {
     int64_t kv_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_tmp_bytes = 0;
-    // K2 scratch: virtual copies of wide classes, counters of accumulated rectangles
-    uint32_t* virt_d = nullptr;
-    int64_t virt_cap = 0;
+    // K2: plan of the full selection prepared during the build; counters of accumulated rectangles
+    bm::K2Prepared* k2prep = nullptr;
     uint32_t* cnt_d = nullptr;
     int64_t cnt_cap = 0;
     // selection scratch
@@ -226,6 +229,8 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
                             int64_t* n_cand);
 batmap_status swar_device(const uint32_t* x, const uint32_t* y, int64_t n, uint32_t* out,
                           cudaStream_t st);
+batmap_status prepare_full_k2(batmap_collection* h, int part, int n_parts, cudaStream_t st);
+void destroy_k2(K2Prepared* kp, cudaStream_t st);
 // finalize.cu
 batmap_status run_finalize(batmap_collection* h, const Selection& sel, int64_t n_cand,
                            uint32_t threshold, uint32_t flags, cudaStream_t st, int64_t* n_res);

@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0;
     int cur = -1;
+    bool warp_active = true;
     for (uint32_t g = 0;; ++g) {
         const int buf = (int)(g % kStages);
         mbar_wait(&full[buf], (g / kStages) & 1u);
@@ -305,6 +306,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
                 for (int j = 0; j < 8; ++j) acc[i][j] = 0;
         }
         if (mt.x < 0) break;
+        if (mt.y) {
+            // ragged edge tiles: a warp whose rows (from 32 (warp & 1)) or columns (from 16 (warp >> 1))
+            // all lie beyond the rectangle skips the compute, leaving its issue slots to the other CTA
+            const Work wk = work[mt.x];
+            const Rect& r = rects[wk.rect];
+            warp_active = 32 * (warp & 1) < r.n_rows - wk.ti * kBM && 16 * (warp >> 1) < r.n_cols - wk.tj * kBN;
+        }
         cur = mt.x;
         uint32_t* sA = stages + buf * kStageSmem;
         {  // derive the indicator-mask plane x & 0x80808080 once per chunk (not once per thread)
@@ -327,11 +335,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         const uint32_t* sB = sA + kBK * kBM;
         const uint32_t* mA = sA + kStageWords;
         const uint32_t* mB = mA + kBK * kBM;
+        if (warp_active) {
 #pragma unroll 2
-        for (int k = 0; k < kBK; ++k) {
-            Ops o;
-            load_ops(o, sA, sB, mA, mB, k, tr, tc);
-            compute_ops(o, acc);
+            for (int k = 0; k < kBK; ++k) {
+                Ops o;
+                load_ops(o, sA, sB, mA, mB, k, tr, tc);
+                compute_ops(o, acc);
+            }
         }
     }
 }
@@ -546,6 +556,91 @@ static batmap_status run_simple(batmap_collection* h, const Selection& sel, uint
     return rc;
 }
 
+struct K2Prepared {
+    int part = -1, n_parts = -1;
+    Plan pl;
+    K2Maps* prm = nullptr;
+    Rect* rects_d = nullptr;
+    Work* work_d = nullptr;
+    AccUnit* units_d = nullptr;
+    uint32_t* virt_d = nullptr;
+};
+
+void release_k2(K2Prepared* kp, cudaStream_t st) {
+    if (!kp) return;
+    delete kp->prm;
+    kp->prm = nullptr;
+    dfree(kp->rects_d, st);
+    dfree(kp->work_d, st);
+    dfree(kp->units_d, st);
+    dfree(kp->virt_d, st);
+    kp->rects_d = nullptr;
+    kp->work_d = nullptr;
+    kp->units_d = nullptr;
+    kp->virt_d = nullptr;
+}
+
+void destroy_k2(K2Prepared* kp, cudaStream_t st) {
+    release_k2(kp, st);
+    delete kp;
+}
+
+// Host planning + device copies of the plan + tensor maps (no dependence on the arena contents).
+batmap_status prepare_k2(batmap_collection* h, const Selection& sel, int part, int n_parts, cudaStream_t st,
+                         K2Prepared* kp) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return BATMAP_E_CUDA;
+    }
+    const int C = (int)sel.classes.size();
+    kp->part = part;
+    kp->n_parts = n_parts;
+    const int grid_cap = kMinBlocks * h->num_sms;
+    plan_work(sel.classes, part, n_parts, grid_cap, !env_off("BATMAP_K2_VIRTUAL"), !env_off("BATMAP_K2_SPLIT"),
+              &kp->pl);
+    if (C + (int)kp->pl.virt.size() > kMaxMaps) plan_work(sel.classes, part, n_parts, grid_cap, false, true, &kp->pl);
+    const Plan& pl = kp->pl;
+    if (pl.work.empty()) return BATMAP_OK;
+    if (pl.virt_words) BM_TRY(dalloc_t(&kp->virt_d, pl.virt_words, st));
+    kp->prm = new K2Maps();
+    for (int a = 0; a < C; ++a)
+        BM_TRY(encode_map(enc, &kp->prm->maps[a], sel.arena + sel.classes[a].word_off, sel.classes[a].n_pad,
+                          sel.classes[a].W));
+    for (size_t k = 0; k < pl.virt.size(); ++k)
+        BM_TRY(encode_map(enc, &kp->prm->maps[C + k], kp->virt_d + pl.virt[k].dst_word_off, pl.virt[k].vpad,
+                          pl.virt[k].W_a));
+    BM_TRY(dalloc_t(&kp->rects_d, (int64_t)pl.rects.size(), st));
+    BM_TRY(dalloc_t(&kp->work_d, (int64_t)pl.work.size(), st));
+    BM_TRY(dalloc_t(&kp->units_d, (int64_t)std::max<size_t>(pl.units.size(), 1), st));
+    BM_CUDA(cudaMemcpyAsync(kp->rects_d, pl.rects.data(), pl.rects.size() * sizeof(Rect), cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaMemcpyAsync(kp->work_d, pl.work.data(), pl.work.size() * sizeof(Work), cudaMemcpyHostToDevice, st));
+    if (!pl.units.empty())
+        BM_CUDA(cudaMemcpyAsync(kp->units_d, pl.units.data(), pl.units.size() * sizeof(AccUnit),
+                                cudaMemcpyHostToDevice, st));
+    return BATMAP_OK;
+}
+
+// Called by batmap_build once the classes are known: plan the full selection for (part, n_parts).
+batmap_status prepare_full_k2(batmap_collection* h, int part, int n_parts, cudaStream_t st) {
+    if (h->n < 2 || (int)h->classes.size() > kMaxMaps) return BATMAP_OK;
+    for (const ClassInfo& c : h->classes)
+        if (c.W % kBK != 0 || c.W >= kMaxTiledW || c.W < kBK) return BATMAP_OK;
+    Selection sel;
+    sel.classes = h->classes;
+    sel.arena = h->arena_d;
+    sel.n_sel = h->n;
+    K2Prepared* kp = new K2Prepared();
+    batmap_status rc = prepare_k2(h, sel, part, n_parts, st, kp);
+    if (rc != BATMAP_OK) {
+        destroy_k2(kp, st);
+        return rc;
+    }
+    if (h->k2prep) destroy_k2(h->k2prep, st);
+    h->k2prep = kp;
+    return BATMAP_OK;
+}
+
 batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t threshold, int part,
                             int n_parts, uint32_t flags, cudaStream_t st, int64_t* n_cand) {
     *n_cand = 0;
@@ -562,54 +657,50 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
     if (C > kMaxMaps) simple = true;
     if (simple) return run_simple(h, sel, threshold, part, n_parts, use_f, st, n_cand);
 
-    Plan pl;
+    // the plan of the full selection is prepared (host planning, H2D, tensor maps) while the build
+    // kernels run, and reused; item subsets are planned here
+    K2Prepared* kp = nullptr;
+    K2Prepared local;
+    if (!sel.sel2pos && h->k2prep && h->k2prep->part == part && h->k2prep->n_parts == n_parts) {
+        kp = h->k2prep;
+    } else {
+        const batmap_status prc = prepare_k2(h, sel, part, n_parts, st, &local);
+        if (prc != BATMAP_OK) {
+            release_k2(&local, st);
+            return prc;
+        }
+        kp = &local;
+    }
+    const Plan& pl = kp->pl;
     const int grid_cap = kMinBlocks * h->num_sms;
-    plan_work(sel.classes, part, n_parts, grid_cap, !env_off("BATMAP_K2_VIRTUAL"), !env_off("BATMAP_K2_SPLIT"), &pl);
-    if (C + (int)pl.virt.size() > kMaxMaps) plan_work(sel.classes, part, n_parts, grid_cap, false, true, &pl);
     const int64_t n_work = (int64_t)pl.work.size();
     h->stats.word_compares = pl.word_compares;
     h->stats.tile_compares = pl.tile_compares;
     h->stats.k2_kind = 1;
     h->stats.k2_grid = (int32_t)std::min<int64_t>(n_work, grid_cap);
-    if (n_work == 0) return BATMAP_OK;
-
-    // virtual copies of the wide classes of skinny rectangles
-    if (pl.virt_words) BM_TRY(ensure(&h->virt_d, &h->virt_cap, pl.virt_words, st));
+    if (n_work == 0) {
+        if (kp == &local) release_k2(&local, st);
+        return BATMAP_OK;
+    }
+    // virtual copies of the wide classes of skinny rectangles (after the build kernels wrote the arena)
     for (const VirtCopy& v : pl.virt) {
         const ClassInfo& B = sel.classes[v.cls_b];
         const int64_t cnt = (int64_t)v.W_a * v.vpad;
         k_virtualize<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(sel.arena + B.word_off, B.n_pad, B.n, v.W_a, v.R,
-                                                                    v.vpad, h->virt_d + v.dst_word_off);
+                                                                    v.vpad, kp->virt_d + v.dst_word_off);
         h->launches += 1;
     }
-    K2Maps* prm = new K2Maps();
-    batmap_status rc = BATMAP_OK;
-    for (int a = 0; a < C && rc == BATMAP_OK; ++a)
-        rc = encode_map(enc, &prm->maps[a], sel.arena + sel.classes[a].word_off, sel.classes[a].n_pad,
-                        sel.classes[a].W);
-    for (size_t k = 0; k < pl.virt.size() && rc == BATMAP_OK; ++k)
-        rc = encode_map(enc, &prm->maps[C + k], h->virt_d + pl.virt[k].dst_word_off, pl.virt[k].vpad, pl.virt[k].W_a);
-    if (rc != BATMAP_OK) {
-        delete prm;
-        return rc;
-    }
-    Rect* rects_d = nullptr;
-    Work* work_d = nullptr;
-    AccUnit* units_d = nullptr;
-    BM_TRY(dalloc_t(&rects_d, (int64_t)pl.rects.size(), st));
-    BM_TRY(dalloc_t(&work_d, n_work, st));
-    BM_TRY(dalloc_t(&units_d, (int64_t)std::max<size_t>(pl.units.size(), 1), st));
-    BM_CUDA(cudaMemcpyAsync(rects_d, pl.rects.data(), pl.rects.size() * sizeof(Rect), cudaMemcpyHostToDevice, st));
-    BM_CUDA(cudaMemcpyAsync(work_d, pl.work.data(), n_work * sizeof(Work), cudaMemcpyHostToDevice, st));
-    if (!pl.units.empty())
-        BM_CUDA(cudaMemcpyAsync(units_d, pl.units.data(), pl.units.size() * sizeof(AccUnit), cudaMemcpyHostToDevice,
-                                st));
     if (pl.cnt_entries) BM_TRY(ensure(&h->cnt_d, &h->cnt_cap, pl.cnt_entries, st));
     static bool attr_set = false;
     if (!attr_set) {
         BM_CUDA(cudaFuncSetAttribute(k2_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
         attr_set = true;
     }
+    const K2Maps* prm = kp->prm;
+    Rect* rects_d = kp->rects_d;
+    Work* work_d = kp->work_d;
+    AccUnit* units_d = kp->units_d;
+    batmap_status rc = BATMAP_OK;
     int* work_ctr = reinterpret_cast<int*>(h->ctr_d + 1);
     const int grid = (int)std::min<int64_t>(n_work, grid_cap);
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -639,10 +730,7 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         rc = ensure_cand(h, (int64_t)cnt, st);
         if (rc != BATMAP_OK) break;
     }
-    delete prm;
-    dfree(rects_d, st);
-    dfree(work_d, st);
-    dfree(units_d, st);
+    if (kp == &local) release_k2(&local, st);
     return rc;
 }
 
