@@ -45,6 +45,30 @@ __device__ __forceinline__ uint32_t step(uint32_t x, uint32_t y, uint32_t xm, ui
     return r;
 }
 
+
+// Explicitly scheduled 8x8 step: a software pipeline over the 64 pairs in which every ALU op
+// (LOP3) is followed by an FMA-pipe op (IADD / IDP4A), kept in order by asm volatile.
+__device__ __forceinline__ void step_pipelined(const uint32_t (&x)[8], const uint32_t (&y)[8], const uint32_t (&xm)[8],
+                                               const uint32_t (&ym)[8], uint32_t (&acc)[8][8]) {
+    uint32_t u[64], p[64], v[64];
+#pragma unroll
+    for (int q = 0; q < 64 + 3; ++q) {
+        if (q < 64) {
+            const int i = q >> 3, j = q & 7;
+            asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[q]) : "r"(x[i]), "r"(y[j]));  // (a^b)|c
+        }
+        if (q >= 1 && q - 1 < 64) asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - 1]) : "r"(u[q - 1]));
+        if (q >= 2 && q - 2 < 64) {
+            const int i = (q - 2) >> 3, j = (q - 2) & 7;
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v[q - 2]) : "r"(p[q - 2]), "r"(xm[i]), "r"(ym[j]));
+        }
+        if (q >= 3) {
+            const int i = (q - 3) >> 3, j = (q - 3) & 7;
+            asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;" : "+r"(acc[i][j]) : "r"(v[q - 3]));
+        }
+    }
+}
+
 // MASKS: 0 = compute x & M in registers per k, 1 = load from a second smem plane, 2 = no LDS in the
 // loop at all (register-resident operands perturbed per k: the compute ceiling)
 template <int V, int MASKS, int NT, int MINB = 1, int UNR = 4, int SYNC = 0>
@@ -116,10 +140,14 @@ __global__ void __launch_bounds__(NT, MINB) bench(const uint32_t* __restrict__ g
             } else {
                 x[k & 7] += one;  // perturb one operand per k so nothing is loop-invariant
             }
+            if (V == 5) {
+                step_pipelined(x, y, xm, ym, acc);
+            } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = step<V>(x[i], y[j], xm[i], ym[j], acc[i][j], one, sh25);
+                    for (int j = 0; j < 8; ++j) acc[i][j] = step<V>(x[i], y[j], xm[i], ym[j], acc[i][j], one, sh25);
+            }
         }
     }
     __syncthreads();
@@ -179,8 +207,11 @@ int main() {
     CK(cudaMalloc(&cyc, 4 * sms * 8));
     CK(cudaMemcpy(g, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
     run<4, 1, 256, 2, 2>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
-    run<4, 1, 256, 2, 2, 1>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run<5, 1, 256, 2, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
+    run<5, 1, 256, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
+    run<5, 1, 512, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
+    run<4, 1, 512, 1, 2>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
     run<4, 1, 256, 1, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
-    run<4, 1, 256, 1, 4, 1>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run<5, 1, 256, 2, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
     return 0;
 }
