@@ -7,6 +7,7 @@
 // b from the partner table (Fig. 5, reading #6) and ⊥ = 0x7F (reading #1), and writes the
 // words into the class-blocked, word-major arena the intersection kernel reads.
 #include <algorithm>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -280,7 +281,155 @@ __global__ void __launch_bounds__(kConcThreads) k1_conc_small(
     }
 }
 
-// Concurrent tier for large tables (r > kSmallMaxR): the working table lives in global memory
+// Concurrent tier for medium tables (kSmallMaxR < r <= kClusterMaxR): one thread-block cluster
+// per item; the item's 3r-entry working table (raw tids) is spread over the distributed shared
+// memory of the cluster's CS CTAs (slice q / (3r/CS) of slot q), so every swap of the paper's
+// INSERT is an on-chip atomic exchange, local or remote (DSMEM).  Same protocol as
+// k1_conc_small (reading #9b); π is recomputed on every swap.  The encode (Fig. 5)
+// follows in the same kernel, each CTA encoding the words of its own slice.
+constexpr uint32_t kClusterMaxR = 131072;
+constexpr int kClSliceBytesMax = 3 * 16384 * 4;  // 192 KB of table per CTA
+
+// DSMEM access: slot q of the item's table as (owning CTA, offset); local slots use plain shared
+// atomics, remote ones the shared::cluster window (mapa + atom/ld.shared::cluster)
+__device__ __forceinline__ uint32_t cl_exch(uint32_t addr, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared::cluster.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint32_t cl_cas(uint32_t addr, uint32_t cmp, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared::cluster.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(addr), "r"(cmp), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint32_t cl_ld(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+template <int CS, int NT>
+__global__ void __launch_bounds__(NT) k1_conc_cluster(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
+    int64_t first, uint32_t r, int log2r, PiParams P, uint32_t r0, int log2r0, uint32_t max_loop_opt,
+    uint32_t* __restrict__ arena_cls, int n_pad, uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr,
+    int64_t fail_cap) {
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) uint32_t T[];  // this CTA's slice: 3r / CS entries
+    __shared__ uint32_t fl[kConcFailCap];
+    __shared__ int nfl, overflow;
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t rank = CS == 1 ? 0u : cl.block_rank();
+    const uint32_t slice = 3u * r / CS;
+    const int c = blockIdx.x / CS;
+    const int64_t pos = first + c;
+    const int orig = pos2orig[pos];
+    const int64_t b = offsets[orig];
+    const int n = (int)(offsets[orig + 1] - b);
+    const int32_t* S = tids + b;
+    const uint32_t T_loc = (uint32_t)__cvta_generic_to_shared(T);  // CTA k's copy is a mapa away
+    // slot q lives in CTA k = floor(q * CS / (3 * 2^log2r)) at offset q - k * slice
+    auto owner = [&](uint32_t q) -> uint32_t { return CS == 1 ? 0u : ((q * CS) >> log2r) / 3u; };
+    auto exch = [&](uint32_t q, uint32_t v) -> uint32_t {
+        const uint32_t k = owner(q), off = q - k * slice;
+        if (CS == 1 || k == rank) return atomicExch(T + off, v);
+        uint32_t a;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(T_loc + 4u * off), "r"(k));
+        return cl_exch(a, v);
+    };
+    auto cas = [&](uint32_t q, uint32_t cmp, uint32_t v) -> uint32_t {
+        const uint32_t k = owner(q), off = q - k * slice;
+        if (CS == 1 || k == rank) return atomicCAS(T + off, cmp, v);
+        uint32_t a;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(T_loc + 4u * off), "r"(k));
+        return cl_cas(a, cmp, v);
+    };
+    auto load = [&](uint32_t q) -> uint32_t {
+        const uint32_t k = owner(q), off = q - k * slice;
+        if (CS == 1 || k == rank) return T[off];
+        uint32_t a;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(T_loc + 4u * off), "r"(k));
+        return cl_ld(a);
+    };
+    for (uint32_t q = threadIdx.x; q < slice; q += NT) T[q] = kEmpty;
+    if (threadIdx.x == 0) {
+        nfl = 0;
+        overflow = 0;
+    }
+    if (CS > 1) cl.sync();
+    else __syncthreads();
+    const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)log2r;
+    for (int e = (int)rank * NT + threadIdx.x; e < n; e += CS * NT) {
+        const uint32_t x = (uint32_t)__ldg(S + e);
+        for (int copy = 0; copy < 2; ++copy) {  // the insert procedure is called twice
+            uint32_t tau = x;
+            for (uint32_t l = 0; l < max_loop && tau != kEmpty; ++l)
+#pragma unroll
+                for (int t = 0; t < 3 && tau != kEmpty; ++t) tau = exch(slot_of(t, pi_eval(P, t, tau), r, r0, log2r0), tau);
+            if (tau != kEmpty) record_failure(fl, &nfl, fails, fail_ctr, fail_cap, pos, tau, tau, &overflow);
+        }
+    }
+    __syncthreads();
+    int any_overflow;
+    if (CS > 1) {
+        int* ovf0 = cl.map_shared_rank(&overflow, 0);
+        if (threadIdx.x == 0 && overflow && rank != 0) atomicOr(ovf0, 1);
+        cl.sync();
+        any_overflow = *ovf0;
+    } else {
+        any_overflow = overflow;
+    }
+    if (!any_overflow) {  // delete the remaining copy of every failed element (reading #9b)
+        const int nf = nfl;
+        for (int k = threadIdx.x; k < nf; k += NT) {
+            const uint32_t x = fl[k];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) cas(slot_of(t, pi_eval(P, t, x), r, r0, log2r0), x, kEmpty);
+        }
+    } else {  // rare: any element left with fewer than two copies was recorded
+        for (int e = (int)rank * NT + threadIdx.x; e < n; e += CS * NT) {
+            const uint32_t x = (uint32_t)S[e];
+            uint32_t q[3];
+            int cnt = 0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                q[t] = slot_of(t, pi_eval(P, t, x), r, r0, log2r0);
+                cnt += (load(q[t]) == x);
+            }
+            if (cnt == 1)
+#pragma unroll
+                for (int t = 0; t < 3; ++t) cas(q[t], x, kEmpty);
+        }
+    }
+    if (CS > 1) cl.sync();
+    else __syncthreads();
+    // encode the words of this CTA's slice into the word-major class block
+    const uint32_t sb = 3u * r0;
+    const uint32_t q0 = rank * slice;
+    for (uint32_t wl = threadIdx.x; wl < slice / 4; wl += NT) {
+        const uint4 e4 = reinterpret_cast<const uint4*>(T)[wl];
+        const uint32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};
+        uint32_t word = 0;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const uint32_t x = xs[l];
+            uint32_t byte = kNullByte;
+            if (x != kEmpty) {
+                const uint32_t q = q0 + 4u * wl + l;
+                const int t = (int)((q % sb) >> log2r0);  // table of entry q
+                const uint32_t code = pi_eval(P, t, x) >> P.s;
+                const int t1 = (t + 1) % 3;
+                const uint32_t bit = (load(slot_of(t1, pi_eval(P, t1, x), r, r0, log2r0)) == x) ? 0u : 1u;  // Fig. 5
+                byte = (bit << 7) | code;
+            }
+            word |= byte << (8 * l);
+        }
+        arena_cls[(int64_t)(q0 / 4 + wl) * n_pad + c] = word;
+    }
+    if (CS > 1) cl.sync();  // no CTA may exit while another still reads its slice
+}
+
+// Concurrent tier for large tables (r > kClusterMaxR): the working table lives in global memory
 // (raw tids, atomics in L2); π is recomputed on every swap.  One CTA per item.
 __global__ void __launch_bounds__(256) k1_conc_global(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
@@ -394,6 +543,16 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
 }
 
 __global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+// ⊥ words in the padding columns [n, n_pad) of a class block (reading #1); every real column is
+// written by the build kernels
+__global__ void k_fill_padding(uint32_t* __restrict__ arena_cls, int n, int n_pad, int W) {
+    const int pad = n_pad - n;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)W * pad) return;
+    const int64_t w = idx / pad;
+    arena_cls[w * n_pad + n + (idx - w * pad)] = kNullWord;
+}
 
 // fail_off[p] = first index of position p in the sorted (pos << 32 | tid) list; f[p] = its count
 __global__ void k_fail_offsets(const uint64_t* __restrict__ keys, int64_t F, int64_t n, int64_t* __restrict__ off,
@@ -594,6 +753,51 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     return BATMAP_OK;
 }
 
+template <int CS, int NT>
+static batmap_status launch_cluster(const ClassInfo& c, batmap_collection* h, const int64_t* offsets,
+                                    const int32_t* tids, uint64_t* fails, unsigned long long* fail_ctr,
+                                    int64_t fail_cap, cudaStream_t st) {
+    static bool attr = false;
+    const size_t smem = (size_t)3 * c.r / CS * sizeof(uint32_t);
+    if (!attr) {
+        BM_CUDA(cudaFuncSetAttribute(k1_conc_cluster<CS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kClSliceBytesMax));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)c.n * CS);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BM_CUDA(cudaLaunchKernelEx(&cfg, k1_conc_cluster<CS, NT>, offsets, tids, (const int32_t*)h->pos2orig_d,
+                               (int64_t)c.first, (uint32_t)c.r, ilog2_u64((uint64_t)c.r), h->pi, (uint32_t)h->r0,
+                               h->log2r0, h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, fails, fail_ctr,
+                               fail_cap));
+    h->launches += 1;
+    return BATMAP_OK;
+}
+
+// cluster size: enough CTAs that each holds at most 192 KB of the item's 12r-byte table
+static batmap_status launch_cluster_tier(batmap_collection* h, const ClassInfo& c, const int64_t* offsets,
+                                         const int32_t* tids, uint64_t* fails, unsigned long long* fail_ctr,
+                                         int64_t fail_cap, cudaStream_t st) {
+    const int64_t bytes = 12ll * c.r;
+    if (c.r <= 4096) return launch_cluster<1, 256>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    if (bytes <= kClSliceBytesMax) return launch_cluster<1, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    if (bytes <= 2ll * kClSliceBytesMax)
+        return launch_cluster<2, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    if (bytes <= 4ll * kClSliceBytesMax)
+        return launch_cluster<4, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    return launch_cluster<8, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+}
+
 batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
                                const batmap_build_opts* o, cudaStream_t st) {
     const int64_t n = h->n, m = h->m;
@@ -681,10 +885,12 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         set_error("arena too large");
         return BATMAP_E_OVERFLOW;
     }
-    // items of classes with r > kSmallMaxR (the last positions) use the global-memory tier
+    // items of classes with r > glob_min_r (the last positions) use a working table in global memory
+    const bool serial = o && (o->flags & BATMAP_BUILD_SERIAL);
+    const int64_t glob_min_r = serial ? kSmallMaxR : kClusterMaxR;
     int64_t big_begin = n;
     for (const ClassInfo& c : h->classes)
-        if (c.r > kSmallMaxR) {
+        if (c.r > glob_min_r) {
             big_begin = c.first;
             break;
         }
@@ -742,11 +948,15 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     }
     for (int attempt = 0; attempt < 4; ++attempt) {
         BM_TRY(dalloc_t(&fails, fail_cap, st));
-        BM_CUDA(cudaMemsetAsync(h->arena_d, 0x7F, h->arena_words * sizeof(uint32_t), st));  // ⊥ padding
+        for (const ClassInfo& c : h->classes) {  // ⊥ padding
+            const int64_t cnt = (int64_t)c.W * (c.n_pad - c.n);
+            if (cnt == 0) continue;
+            k_fill_padding<<<grid_for(cnt, 256), 256, 0, st>>>(h->arena_d + c.word_off, c.n, c.n_pad, c.W);
+            h->launches += 1;
+        }
         if (work_entries) BM_CUDA(cudaMemsetAsync(work, 0xFF, work_entries * sizeof(uint32_t), st));
         BM_CUDA(cudaMemsetAsync(fail_ctr, 0, sizeof(unsigned long long), st));
         rec(h, EV_I0, st);
-        const bool serial = o && (o->flags & BATMAP_BUILD_SERIAL);
         if (serial) {
             if (n_big) {  // launched first: its long serial chains overlap the small-tier CTAs
                 k1_insert<<<grid_for(n_big, 32), 32, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d, lr_d,
@@ -768,16 +978,29 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         } else {
             for (size_t a = 0; a < h->classes.size(); ++a) {  // big classes first (longest items)
                 const ClassInfo& c = h->classes[a];
-                if (c.r <= kSmallMaxR || c.n == 0) continue;
+                if (c.r <= kClusterMaxR || c.n == 0) continue;
                 k1_conc_global<<<c.n, 256, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d + (c.first - big_begin),
                                                     c.first, h->pi, (uint32_t)c.r, ilog2_u64((uint64_t)c.r),
                                                     (uint32_t)h->r0, h->log2r0, h->max_loop_opt, work, h->f_d, fails,
                                                     fail_ctr, fail_cap);
                 h->launches += 1;
             }
+            // r <= cl_min_r: the slot-caching CTA kernel (faster for narrow tables, measured on C2);
+            // wider tables: the cluster kernel.  BATMAP_K1_SMALL=legacy|cluster moves the boundary.
+            static const int64_t cl_min_r = [] {
+                const char* v = getenv("BATMAP_K1_SMALL");
+                if (v && v[0] == 'l') return (int64_t)kSmallMaxR;
+                if (v && v[0] == 'c') return (int64_t)0;
+                return (int64_t)2048;
+            }();
+            for (size_t a = h->classes.size(); a-- > 0;) {  // cluster tier, widest first
+                const ClassInfo& c = h->classes[a];
+                if (c.r <= cl_min_r || c.r > kClusterMaxR || c.n == 0) continue;
+                BM_TRY(launch_cluster_tier(h, c, offsets, tids, fails, fail_ctr, fail_cap, st));
+            }
             for (size_t a = 0; a < h->classes.size(); ++a) {
                 const ClassInfo& c = h->classes[a];
-                if (c.r > kSmallMaxR || c.n == 0) continue;
+                if (c.r > cl_min_r || c.n == 0) continue;
                 const int maxS = std::max(class_maxS[a], 1);
                 const size_t smem = (size_t)12 * c.r + (size_t)9 * maxS + 16;
                 k1_conc_small<<<c.n, kConcThreads, smem, st>>>(
@@ -802,7 +1025,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     h->n_fail = F;
     rec(h, EV_E0, st);
     for (const ClassInfo& c : h->classes) {
-        if (c.r <= kSmallMaxR) continue;
+        if (c.r <= glob_min_r) continue;
         int64_t cnt = (int64_t)c.W * c.n_pad;
         k1_encode<<<grid_for(cnt, 256), 256, 0, st>>>(work, work_off_d, c.first - big_begin, c.n, c.n_pad, c.W,
                                                       (uint32_t)c.r, h->pi, (uint32_t)h->r0, h->log2r0,

@@ -163,6 +163,34 @@ def test_concurrent_build_invariants(max_loop):
     np.testing.assert_array_equal(_np(c.pair_supports(threshold=0)), oracle.pairs_merge(off, tids, threshold=0))
 
 
+def _tiers(seed, m=300000):
+    """Items whose table ranges span the cluster tier (r = 2^14 .. 2^17: clusters of 1, 2, 4, 8
+    CTAs) and the global-memory tier (r = 2^18), plus small items, with shared elements."""
+    rng = np.random.default_rng(seed)
+    sizes = [5000, 9000, 17000, 40000, 70000, 300, 3000, 8000]
+    base = np.sort(rng.choice(m, size=90000, replace=False))
+    rows = []
+    for k, size in enumerate(sizes):
+        own = rng.choice(m, size=size - size // 3, replace=False)
+        shared = rng.choice(base, size=size // 3, replace=False)
+        rows.append(np.unique(np.concatenate([own, shared])).astype(np.int32))
+    off = np.zeros(len(rows) + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    return off, np.concatenate(rows), m
+
+
+@pytest.mark.parametrize("max_loop", [0, 1])
+def test_cluster_and_global_tiers(max_loop):
+    off, tids, m = _tiers(21)
+    c = _coll(off, tids, m, seed=6, max_loop=max_loop)
+    rs = sorted({len(c.export_entries(i)) // 3 for i in range(len(off) - 1)})
+    assert {2 ** 14, 2 ** 15, 2 ** 16, 2 ** 17, 2 ** 18} <= set(rs)
+    _check_layout_invariants(c, off, tids, m, 6)
+    if max_loop:
+        assert c.info()["n_failures"] > 2000  # per-CTA failure lists overflow: the rescan path runs
+    np.testing.assert_array_equal(_np(c.pair_supports(threshold=0)), oracle.pairs_merge(off, tids, threshold=0))
+
+
 # ----------------------------------------------------------------------------- end to end
 def _check_exact(off, tids, m, thr, items=None, **kw):
     c = _coll(off, tids, m, **kw)

@@ -188,6 +188,93 @@ void run(const char* name, const uint32_t* g, int sms, uint32_t* out, unsigned l
            per_block * sms / (ms * 1e-3) / 1e12, ms, mc / (ms * 1e-3) / 1e6);
 }
 
+
+template <int NT, int MINB, bool LDS>
+__global__ void __launch_bounds__(NT, MINB) bench_pf(const uint32_t* __restrict__ g, int reps, uint32_t* out,
+                                                      unsigned long long* cycles) {
+    __shared__ __align__(16) uint32_t sA[16 * 128], sB[16 * 128], mA[16 * 128], mB[16 * 128];
+    for (int i = threadIdx.x; i < 16 * 128; i += blockDim.x) {
+        sA[i] = g[i];
+        sB[i] = g[i + 32 * 128];
+        mA[i] = g[i] & 0x80808080u;
+        mB[i] = g[i + 32 * 128] & 0x80808080u;
+    }
+    __syncthreads();
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
+    const int tr = ((warp & 1) << 3) | (lane & 7);
+    const int tc = ((warp >> 1) << 2) | (lane >> 3);
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    auto ld = [&](int k, uint32_t (&x)[8], uint32_t (&y)[8], uint32_t (&xm)[8], uint32_t (&ym)[8]) {
+        const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * 128 + 4 * tr);
+        const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * 128 + 64 + 4 * tr);
+        const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * 128 + 4 * tc);
+        const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * 128 + 64 + 4 * tc);
+        const uint4 a = *reinterpret_cast<const uint4*>(mA + k * 128 + 4 * tr);
+        const uint4 b = *reinterpret_cast<const uint4*>(mA + k * 128 + 64 + 4 * tr);
+        const uint4 c = *reinterpret_cast<const uint4*>(mB + k * 128 + 4 * tc);
+        const uint4 d = *reinterpret_cast<const uint4*>(mB + k * 128 + 64 + 4 * tc);
+        x[0] = xa.x; x[1] = xa.y; x[2] = xa.z; x[3] = xa.w; x[4] = xb.x; x[5] = xb.y; x[6] = xb.z; x[7] = xb.w;
+        y[0] = ya.x; y[1] = ya.y; y[2] = ya.z; y[3] = ya.w; y[4] = yb.x; y[5] = yb.y; y[6] = yb.z; y[7] = yb.w;
+        xm[0] = a.x; xm[1] = a.y; xm[2] = a.z; xm[3] = a.w; xm[4] = b.x; xm[5] = b.y; xm[6] = b.z; xm[7] = b.w;
+        ym[0] = c.x; ym[1] = c.y; ym[2] = c.z; ym[3] = c.w; ym[4] = d.x; ym[5] = d.y; ym[6] = d.z; ym[7] = d.w;
+    };
+    uint32_t x0[8], y0[8], xm0[8], ym0[8], x1[8], y1[8], xm1[8], ym1[8];
+    ld(0, x0, y0, xm0, ym0);
+    __syncthreads();
+    unsigned long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int k = 0; k < 16; k += 2) {
+            if (LDS) ld(k + 1, x1, y1, xm1, ym1);
+            else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { x1[i] = x0[i] + 1; y1[i] = y0[i]; xm1[i] = xm0[i]; ym1[i] = ym0[i]; }
+            }
+            step_pipelined(x0, y0, xm0, ym0, acc);
+            if (LDS) ld((k + 2) & 15, x0, y0, xm0, ym0);
+            else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x0[i] = x1[i] + 1;
+            }
+            step_pipelined(x1, y1, xm1, ym1, acc);
+        }
+    }
+    __syncthreads();
+    unsigned long long t1 = clock64();
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += acc[i][j] * (i * 8 + j + 1);
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+template <int NT, int MINB, bool LDS>
+void run_pf(const char* name, const uint32_t* g, int sms, uint32_t* out, unsigned long long* cyc) {
+    const int reps = 2000;
+    sms *= MINB;
+    bench_pf<NT, MINB, LDS><<<sms, NT>>>(g, 10, out, cyc);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    bench_pf<NT, MINB, LDS><<<sms, NT>>>(g, reps, out, cyc);
+    cudaEventRecord(e1);
+    CK(cudaDeviceSynchronize());
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double per_block = (double)NT * 64.0 * 16.0 * reps;
+    printf("{\"variant\": \"%s\", \"threads\": %d, \"ctas_per_sm\": %d, \"unroll\": 0, \"cmp_per_clk_per_sm\": 0, "
+           "\"frac_of_32\": 0, \"tcmp_per_s\": %.3f, \"ms\": %.2f, \"eff_mhz\": 0}\\n",
+           name, NT, MINB, per_block * sms / (ms * 1e-3) / 1e12, ms);
+}
+
 int main() {
     int sms;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -206,12 +293,14 @@ int main() {
     CK(cudaMalloc(&out, 4 * sms * 512 * 4));
     CK(cudaMalloc(&cyc, 4 * sms * 8));
     CK(cudaMemcpy(g, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
-    run<4, 1, 256, 2, 2>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
-    run<5, 1, 256, 2, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
-    run<5, 1, 256, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
+    run_pf<256, 1, true>("pf_pipelined/lds", g, sms, out, cyc);
+    run_pf<256, 1, false>("pf_pipelined/no_lds", g, sms, out, cyc);
+    run_pf<256, 2, true>("pf_pipelined/lds", g, sms, out, cyc);
     run<5, 1, 512, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
-    run<4, 1, 512, 1, 2>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
-    run<4, 1, 256, 1, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
-    run<5, 1, 256, 2, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
+    run<5, 1, 384, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
+    run<5, 1, 256, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
+    run<5, 2, 256, 1, 1>("pipelined_volatile/no_lds_ceiling", g, sms, out, cyc);
+    run<5, 2, 512, 1, 1>("pipelined_volatile/no_lds_ceiling", g, sms, out, cyc);
+    run<4, 2, 256, 1, 4>("iadd3_idp4a/no_lds_ceiling", g, sms, out, cyc);
     return 0;
 }
