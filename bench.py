@@ -194,7 +194,7 @@ def main():
     import torch.distributed as dist
 
     from paper_1102_1003_b200 import Collection, batmap, mine_host
-    from paper_1102_1003_b200.dist import gather_triples
+    from paper_1102_1003_b200.dist import build_distributed, gather_triples
 
     # test hooks (not used by the driver): run several ranks on one GPU over gloo
     dev_idx = int(os.environ.get("BENCH_FORCE_DEVICE", local_rank))
@@ -214,7 +214,10 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
-        coll = Collection(off_d, tids_d, w.m, seed=1)
+        if world > 1:  # sharded build + all_gather of the BatMaps
+            coll = build_distributed(off_d, tids_d, w.m, seed=1)
+        else:
+            coll = Collection(off_d, tids_d, w.m, seed=1)
         res = coll.pair_supports(threshold=w.threshold, part=rank, n_parts=world)
         if world > 1:
             allp = gather_triples(res if backend == "nccl" else res.cpu())

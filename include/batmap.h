@@ -142,6 +142,45 @@ batmap_status batmap_pair_supports_part(batmap_handle h, const int32_t* items, i
                                         batmap_triple* out, int64_t capacity, int64_t* n_out,
                                         batmap_stream_t stream);
 
+/*
+ * Sharded build for multi-GPU runs (the paper is single-GPU).
+ * Every BatMap depends on its own tidlist only, so part `part` of `n_parts`
+ * builds the BatMaps of a contiguous share of each width class (columns
+ * [n_c*part/n_parts, n_c*(part+1)/n_parts) of class c, n_c its item count) and records
+ * the failures of those items; the parts then exchange their shares (an all_gather of
+ * batmap_shard_export's buffers, done by the caller, e.g. torch.distributed over NCCL)
+ * and batmap_shard_import completes the handle, after which it is identical in use to a
+ * batmap_build handle.  Until then batmap_pair_supports* return E_INVALID.
+ *
+ * batmap_build_shard -- arguments as batmap_build plus 0 <= part < n_parts.  The CSR must
+ *   be the full collection on every part (the same arrays on every rank).
+ * batmap_shard_sizes -- words (uint32) of part p's share of the BatMaps (any p: the layout
+ *   is computed identically on every rank) and, for p == this part, its number of
+ *   failure records (else -1).
+ * batmap_shard_export -- [device] words_out <- this part's share, as a packed
+ *   [class][word][column] array; [device] fails_out <- its failure records (opaque uint64).
+ *   E_CAPACITY if a buffer is smaller than batmap_shard_sizes reports.
+ * batmap_shard_import -- [device] words_all = n_parts blocks of stride_words words, block p
+ *   = part p's export; [device] fails_all = n_parts blocks of stride_fails records, block p
+ *   holding n_fails[p] ([host] int64[n_parts]) records; offsets/tids [device] the same CSR
+ *   as the build (A_b of the failed transactions is rebuilt from it).  Copies the
+ *   other parts' BatMaps into place, merges F and derives f_i, Fail(i) and A_b exactly as a
+ *   whole build does; synchronises `stream`.  E_INVALID on a handle that is not a pending
+ *   shard, NULL buffers, or counts that do not fit the strides or disagree with this part.
+ */
+batmap_status batmap_build_shard(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                                 int64_t n_transactions, const batmap_build_opts* opts,
+                                 int32_t part, int32_t n_parts, batmap_stream_t stream,
+                                 batmap_handle* out);
+batmap_status batmap_shard_sizes(batmap_handle h, int32_t part, int64_t* words, int64_t* n_fail);
+batmap_status batmap_shard_export(batmap_handle h, uint32_t* words_out, int64_t words_capacity,
+                                  uint64_t* fails_out, int64_t fails_capacity,
+                                  batmap_stream_t stream);
+batmap_status batmap_shard_import(batmap_handle h, const int64_t* offsets, const int32_t* tids,
+                                  const uint32_t* words_all, int64_t stride_words,
+                                  const uint64_t* fails_all, const int64_t* n_fails,
+                                  int64_t stride_fails, batmap_stream_t stream);
+
 /* General form: flags = BATMAP_PAIRS_RAW | BATMAP_PAIRS_SIMPLE (test hooks), else 0. */
 batmap_status batmap_pair_supports_ex(batmap_handle h, const int32_t* items, int64_t n_sel,
                                       uint32_t threshold, int32_t part, int32_t n_parts,

@@ -69,6 +69,11 @@ def load_library():
     PI64 = ctypes.POINTER(ctypes.c_int64)
     sig = {
         "batmap_build": ([P, P, I64, I64, ctypes.POINTER(BuildOpts), P, ctypes.POINTER(P)], ctypes.c_int),
+        "batmap_build_shard": ([P, P, I64, I64, ctypes.POINTER(BuildOpts), I32, I32, P, ctypes.POINTER(P)],
+                               ctypes.c_int),
+        "batmap_shard_sizes": ([P, I32, PI64, PI64], ctypes.c_int),
+        "batmap_shard_export": ([P, P, I64, P, I64, P], ctypes.c_int),
+        "batmap_shard_import": ([P, P, P, P, I64, P, PI64, I64, P], ctypes.c_int),
         "batmap_pair_supports": ([P, P, I64, U32, P, I64, PI64, P], ctypes.c_int),
         "batmap_pair_supports_part": ([P, P, I64, U32, I32, I32, P, I64, PI64, P], ctypes.c_int),
         "batmap_pair_supports_ex": ([P, P, I64, U32, I32, I32, U32, P, I64, PI64, P], ctypes.c_int),
@@ -129,7 +134,10 @@ class Collection:
     """The BatMaps of one instance on the current CUDA device (batmap_build)."""
 
     def __init__(self, offsets, tids, n_transactions: int, *, seed: int = 0, r_min: int = 128,
-                 max_loop: int = 0, check: bool = False, pi_table=None, serial: bool = False, stream=None):
+                 max_loop: int = 0, check: bool = False, pi_table=None, serial: bool = False, stream=None,
+                 part: int = 0, n_parts: int = 1):
+        """part/n_parts > 1: sharded build (batmap_build_shard) -- complete it with shard_export on
+        every part, an all_gather, and shard_import (see dist.build_distributed)."""
         import torch
 
         lib = load_library()
@@ -143,11 +151,34 @@ class Collection:
         self._stream = stream
         opts = _opts(seed, r_min, max_loop, check, self._pi, serial)
         h = ctypes.c_void_p()
-        _check(lib.batmap_build(_dptr(self._offsets), _dptr(self._tids), self.n_items, self.m,
-                                ctypes.byref(opts), _stream_ptr(stream), ctypes.byref(h)))
+        self.part, self.n_parts = int(part), int(n_parts)
+        _check(lib.batmap_build_shard(_dptr(self._offsets), _dptr(self._tids), self.n_items, self.m,
+                                      ctypes.byref(opts), self.part, self.n_parts, _stream_ptr(stream),
+                                      ctypes.byref(h)))
         self._h = h
         self._last_k = 1 << 16
-        # the input CSR is not retained by the library
+        # the input CSR is not retained by the library (a shard keeps it until shard_import)
+        if self.n_parts == 1:
+            self._offsets = self._tids = None
+
+    # ------------------------------------------------------------------ sharded build
+    def shard_sizes(self, part: int):
+        """(words of part `part`'s share, failure records of this part or -1)."""
+        w, f = ctypes.c_int64(), ctypes.c_int64()
+        _check(load_library().batmap_shard_sizes(self._h, int(part), ctypes.byref(w), ctypes.byref(f)))
+        return w.value, f.value
+
+    def shard_export(self, words_out, fails_out, stream=None):
+        """Write this part's share (int32/uint32 device tensor) and failure records (int64)."""
+        _check(load_library().batmap_shard_export(self._h, _dptr(words_out), words_out.numel(), _dptr(fails_out),
+                                                  fails_out.numel(), _stream_ptr(stream)))
+
+    def shard_import(self, words_all, stride_words: int, fails_all, n_fails, stride_fails: int, stream=None):
+        """Complete the handle from every part's export (blocks of the given strides)."""
+        nf = (ctypes.c_int64 * self.n_parts)(*[int(x) for x in n_fails])
+        _check(load_library().batmap_shard_import(self._h, _dptr(self._offsets), _dptr(self._tids), _dptr(words_all),
+                                                  int(stride_words), _dptr(fails_all), nf, int(stride_fails),
+                                                  _stream_ptr(stream)))
         self._offsets = self._tids = None
 
     def close(self):

@@ -487,19 +487,16 @@ __global__ void __launch_bounds__(256) k1_conc_global(
     if (threadIdx.x == 0) fcount[pos] = nf;
 }
 
-// Encode one class: thread per (word w, column c); writes arena_cls[w * n_pad + c].
+// Encode columns [0, n) of one class block: thread per (word w, column c); writes
+// arena_cls[w * n_pad + c] (padding columns are filled by k_fill_padding).
 __global__ void __launch_bounds__(256) k1_encode(
     const uint32_t* __restrict__ work, const int64_t* __restrict__ work_off, int64_t first, int n,
     int n_pad, int W, uint32_t r, PiParams P, uint32_t r0, int log2r0,
     uint32_t* __restrict__ arena_cls) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)W * n_pad) return;
-    const int w = (int)(idx / n_pad);
-    const int c = (int)(idx - (int64_t)w * n_pad);
-    if (c >= n) {
-        arena_cls[idx] = kNullWord;
-        return;
-    }
+    if (idx >= (int64_t)W * n) return;
+    const int w = (int)(idx / n);
+    const int c = (int)(idx - (int64_t)w * n);
     const uint32_t* A = work + work_off[first + c];
     const uint4 q4 = *reinterpret_cast<const uint4*>(A + 4 * (int64_t)w);
     const uint32_t xs[4] = {q4.x, q4.y, q4.z, q4.w};
@@ -522,7 +519,7 @@ __global__ void __launch_bounds__(256) k1_encode(
         }
         word |= byte << (8 * lane);  // little-endian lanes (reading #17)
     }
-    arena_cls[idx] = word;
+    arena_cls[(int64_t)w * n_pad + c] = word;
 }
 
 __global__ void k1_check(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
@@ -799,7 +796,7 @@ static batmap_status launch_cluster_tier(batmap_collection* h, const ClassInfo& 
 }
 
 batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
-                               const batmap_build_opts* o, cudaStream_t st) {
+                               const batmap_build_opts* o, int part, int n_parts, cudaStream_t st) {
     const int64_t n = h->n, m = h->m;
     const int64_t l0 = h->launches;
     rec(h, EV_B0, st);
@@ -899,6 +896,16 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     for (int64_t p = 0; p < n_big; ++p) work_off[p + 1] = work_off[p] + 3ll * (1ll << lr_pos[big_begin + p]);
     const int64_t work_entries = work_off[n_big];
 
+    // this part's share of every class: columns [n*part/n_parts, n*(part+1)/n_parts) (sharded build,
+    // SURVEY §8(e)(ii)); the whole class when n_parts == 1
+    auto view = [&](const ClassInfo& c) {
+        ClassInfo v = c;
+        const int64_t c0 = (int64_t)c.n * part / n_parts, c1 = (int64_t)c.n * (part + 1) / n_parts;
+        v.first = c.first + c0;
+        v.n = (int32_t)(c1 - c0);
+        v.word_off = c.word_off + c0;
+        return v;
+    };
     // ---- device state
     BM_TRY(dalloc_t(&h->pos2orig_d, n, st));
     BM_TRY(dalloc_t(&h->orig2pos_d, n, st));
@@ -958,14 +965,17 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         BM_CUDA(cudaMemsetAsync(fail_ctr, 0, sizeof(unsigned long long), st));
         rec(h, EV_I0, st);
         if (serial) {
-            if (n_big) {  // launched first: its long serial chains overlap the small-tier CTAs
-                k1_insert<<<grid_for(n_big, 32), 32, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d, lr_d,
-                                                              big_begin, n_big, h->pi, (uint32_t)h->r0, h->log2r0,
-                                                              h->max_loop_opt, work, h->f_d, fails, fail_ctr, fail_cap);
+            for (size_t a = 0; a < h->classes.size(); ++a) {  // launched first: long serial chains overlap
+                const ClassInfo c = view(h->classes[a]);
+                if (c.r <= kSmallMaxR || c.n == 0) continue;
+                k1_insert<<<grid_for(c.n, 32), 32, 0, st>>>(offsets, tids, h->pos2orig_d,
+                                                            work_off_d + (c.first - big_begin), lr_d, c.first, c.n,
+                                                            h->pi, (uint32_t)h->r0, h->log2r0, h->max_loop_opt, work,
+                                                            h->f_d, fails, fail_ctr, fail_cap);
                 h->launches += 1;
             }
             for (size_t a = 0; a < h->classes.size(); ++a) {
-                const ClassInfo& c = h->classes[a];
+                const ClassInfo c = view(h->classes[a]);
                 if (c.r > kSmallMaxR || c.n == 0) continue;
                 const int maxS = std::max(class_maxS[a], 1);
                 const size_t smem = (size_t)6 * c.r + (size_t)9 * maxS + 16;
@@ -977,7 +987,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
             }
         } else {
             for (size_t a = 0; a < h->classes.size(); ++a) {  // big classes first (longest items)
-                const ClassInfo& c = h->classes[a];
+                const ClassInfo c = view(h->classes[a]);
                 if (c.r <= kClusterMaxR || c.n == 0) continue;
                 k1_conc_global<<<c.n, 256, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d + (c.first - big_begin),
                                                     c.first, h->pi, (uint32_t)c.r, ilog2_u64((uint64_t)c.r),
@@ -994,12 +1004,12 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
                 return (int64_t)2048;
             }();
             for (size_t a = h->classes.size(); a-- > 0;) {  // cluster tier, widest first
-                const ClassInfo& c = h->classes[a];
+                const ClassInfo c = view(h->classes[a]);
                 if (c.r <= cl_min_r || c.r > kClusterMaxR || c.n == 0) continue;
                 BM_TRY(launch_cluster_tier(h, c, offsets, tids, fails, fail_ctr, fail_cap, st));
             }
             for (size_t a = 0; a < h->classes.size(); ++a) {
-                const ClassInfo& c = h->classes[a];
+                const ClassInfo c = view(h->classes[a]);
                 if (c.r > cl_min_r || c.n == 0) continue;
                 const int maxS = std::max(class_maxS[a], 1);
                 const size_t smem = (size_t)12 * c.r + (size_t)9 * maxS + 16;
@@ -1013,7 +1023,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         rec(h, EV_I1, st);
         BM_CUDA(cudaGetLastError());
         // plan the intersection of the full selection on the host while the build kernels run
-        if (attempt == 0) BM_TRY(prepare_full_k2(h, 0, 1, st));
+        if (attempt == 0) BM_TRY(prepare_full_k2(h, part, n_parts, st));
         unsigned long long Fh = 0;
         BM_CUDA(cudaMemcpyAsync(&Fh, fail_ctr, sizeof(Fh), cudaMemcpyDeviceToHost, st));
         BM_CUDA(cudaStreamSynchronize(st));
@@ -1024,9 +1034,10 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     }
     h->n_fail = F;
     rec(h, EV_E0, st);
-    for (const ClassInfo& c : h->classes) {
-        if (c.r <= glob_min_r) continue;
-        int64_t cnt = (int64_t)c.W * c.n_pad;
+    for (const ClassInfo& cl : h->classes) {
+        const ClassInfo c = view(cl);
+        if (c.r <= glob_min_r || c.n == 0) continue;
+        int64_t cnt = (int64_t)c.W * c.n;
         k1_encode<<<grid_for(cnt, 256), 256, 0, st>>>(work, work_off_d, c.first - big_begin, c.n, c.n_pad, c.W,
                                                       (uint32_t)c.r, h->pi, (uint32_t)h->r0, h->log2r0,
                                                       h->arena_d + c.word_off);
@@ -1034,7 +1045,16 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     }
     rec(h, EV_E1, st);
     BM_CUDA(cudaGetLastError());
-    BM_TRY(post_failures(h, offsets, tids, fails, F, st));
+    if (n_parts == 1) {
+        BM_TRY(post_failures(h, offsets, tids, fails, F, st));
+    } else {  // sharded: keep this part's failure records for the exchange (batmap_shard_import)
+        BM_TRY(dalloc_t(&h->shard_fails_d, std::max<int64_t>(F, 1), st));
+        if (F) BM_CUDA(cudaMemcpyAsync(h->shard_fails_d, fails, F * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+        h->shard_n_fail = F;
+        h->shard_part = part;
+        h->shard_n_parts = n_parts;
+        h->shard_pending = true;
+    }
     BM_CUDA(cudaGetLastError());
     dfree(fails, st);
     dfree(fail_ctr, st);
@@ -1044,6 +1064,65 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     rec(h, EV_B1, st);
     h->build_timed = true;
     h->stats.launches_build = h->launches - l0;
+    return BATMAP_OK;
+}
+
+// Words of part p's share of the arena (all classes, in class order, each [W][c1 - c0]).
+int64_t shard_words(const batmap_collection* h, int p, int n_parts) {
+    int64_t words = 0;
+    for (const ClassInfo& c : h->classes) {
+        const int64_t c0 = (int64_t)c.n * p / n_parts, c1 = (int64_t)c.n * (p + 1) / n_parts;
+        words += (c1 - c0) * c.W;
+    }
+    return words;
+}
+
+// Copy part p's columns between the arena and a packed [class][W][cols] buffer (2-D DMA copies).
+batmap_status shard_copy(batmap_collection* h, int p, int n_parts, uint32_t* packed, bool to_arena,
+                         cudaStream_t st) {
+    int64_t off = 0;
+    for (const ClassInfo& c : h->classes) {
+        const int64_t c0 = (int64_t)c.n * p / n_parts, c1 = (int64_t)c.n * (p + 1) / n_parts;
+        if (c1 == c0) continue;
+        uint32_t* a = h->arena_d + c.word_off + c0;
+        uint32_t* b = packed + off;
+        const size_t wb = (size_t)(c1 - c0) * 4, pitch_a = (size_t)c.n_pad * 4;
+        if (to_arena)
+            BM_CUDA(cudaMemcpy2DAsync(a, pitch_a, b, wb, wb, (size_t)c.W, cudaMemcpyDeviceToDevice, st));
+        else
+            BM_CUDA(cudaMemcpy2DAsync(b, wb, a, pitch_a, wb, (size_t)c.W, cudaMemcpyDeviceToDevice, st));
+        off += (c1 - c0) * c.W;
+    }
+    return BATMAP_OK;
+}
+
+// Complete a sharded build: the other parts' columns into the arena, then F, f, Fail(i) and A_b
+// from every part's failure records exactly as after a whole build.
+batmap_status shard_import(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
+                           const uint32_t* words_all, int64_t stride_words, const uint64_t* fails_all,
+                           const int64_t* n_fails, int64_t stride_fails, cudaStream_t st) {
+    const int N = h->shard_n_parts;
+    for (int p = 0; p < N; ++p) {
+        if (p == h->shard_part) continue;
+        BM_TRY(shard_copy(h, p, N, const_cast<uint32_t*>(words_all) + (int64_t)p * stride_words, true, st));
+    }
+    int64_t F = 0;
+    for (int p = 0; p < N; ++p) F += n_fails[p];
+    uint64_t* fails = nullptr;
+    BM_TRY(dalloc_t(&fails, std::max<int64_t>(F, 1), st));
+    int64_t at = 0;
+    for (int p = 0; p < N; ++p) {
+        if (n_fails[p] == 0) continue;
+        BM_CUDA(cudaMemcpyAsync(fails + at, fails_all + (int64_t)p * stride_fails, n_fails[p] * sizeof(uint64_t),
+                                cudaMemcpyDeviceToDevice, st));
+        at += n_fails[p];
+    }
+    BM_TRY(post_failures(h, offsets, tids, fails, F, st));
+    dfree(fails, st);
+    dfree(h->shard_fails_d, st);
+    h->shard_fails_d = nullptr;
+    h->shard_pending = false;
+    BM_CUDA(cudaGetLastError());
     return BATMAP_OK;
 }
 

@@ -27,7 +27,7 @@ void free_all(batmap_collection* h) {
     void* ptrs[] = {h->pos2orig_d, h->orig2pos_d, h->arena_d,   h->f_d,      h->fail_off_d, h->fail_tid_d,
                     h->fidx_of_tid_d, h->ab_off_d, h->ab_pos_d, h->cand_d,   h->ctr_d,      h->key_d,
                     h->val_d,     h->cub_tmp,    h->sel_arena_d, h->sel_idx_d, h->res_d,
-                    h->cnt_d};
+                    h->cnt_d, h->shard_fails_d};
     for (void* p : ptrs) dfree(p, st);
     if (h->k2prep) destroy_k2(h->k2prep, st);
     h->k2prep = nullptr;
@@ -53,6 +53,16 @@ const char* batmap_version(void) { return "batmap-b200 0.1 (sm_100a)"; }
 
 batmap_status batmap_build(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t n_transactions,
                            const batmap_build_opts* opts, batmap_stream_t stream, batmap_handle* out) {
+    return batmap_build_shard(offsets, tids, n_items, n_transactions, opts, 0, 1, stream, out);
+}
+
+batmap_status batmap_build_shard(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                                 int64_t n_transactions, const batmap_build_opts* opts, int32_t part,
+                                 int32_t n_parts, batmap_stream_t stream, batmap_handle* out) {
+    if (n_parts < 1 || part < 0 || part >= n_parts) {
+        set_error("need 0 <= part < n_parts (got %d of %d)", part, n_parts);
+        return BATMAP_E_INVALID;
+    }
     if (!out) {
         set_error("out is NULL");
         return BATMAP_E_INVALID;
@@ -95,7 +105,7 @@ batmap_status batmap_build(const int64_t* offsets, const int32_t* tids, int64_t 
     h->seed = opts ? opts->seed : 0;
     h->r_min = r_min;
     h->max_loop_opt = opts ? opts->max_loop : 0;
-    batmap_status rc = build_collection(h, offsets, tids, opts, st);
+    batmap_status rc = build_collection(h, offsets, tids, opts, part, n_parts, st);
     if (rc != BATMAP_OK) {
         free_all(h);
         delete h;
@@ -105,9 +115,69 @@ batmap_status batmap_build(const int64_t* offsets, const int32_t* tids, int64_t 
     return BATMAP_OK;
 }
 
+batmap_status batmap_shard_sizes(batmap_handle h, int32_t part, int64_t* words, int64_t* n_fail) {
+    if (!h || !words || part < 0 || part >= h->shard_n_parts) {
+        set_error("bad handle / part / words");
+        return BATMAP_E_INVALID;
+    }
+    *words = shard_words(h, part, h->shard_n_parts);
+    if (n_fail) *n_fail = part == h->shard_part ? h->shard_n_fail : -1;
+    return BATMAP_OK;
+}
+
+batmap_status batmap_shard_export(batmap_handle h, uint32_t* words_out, int64_t words_capacity, uint64_t* fails_out,
+                                  int64_t fails_capacity, batmap_stream_t stream) {
+    if (!h || !h->shard_pending) {
+        set_error("not a pending sharded build");
+        return BATMAP_E_INVALID;
+    }
+    const int64_t need = shard_words(h, h->shard_part, h->shard_n_parts);
+    if ((need && !words_out) || words_capacity < need || fails_capacity < h->shard_n_fail ||
+        (h->shard_n_fail && !fails_out)) {
+        set_error("export buffers too small: need %lld words and %lld failure records", (long long)need,
+                  (long long)h->shard_n_fail);
+        return BATMAP_E_CAPACITY;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    BM_TRY(shard_copy(h, h->shard_part, h->shard_n_parts, words_out, false, st));
+    if (h->shard_n_fail)
+        BM_CUDA(cudaMemcpyAsync(fails_out, h->shard_fails_d, h->shard_n_fail * sizeof(uint64_t),
+                                cudaMemcpyDeviceToDevice, st));
+    return BATMAP_OK;
+}
+
+batmap_status batmap_shard_import(batmap_handle h, const int64_t* offsets, const int32_t* tids,
+                                  const uint32_t* words_all, int64_t stride_words, const uint64_t* fails_all,
+                                  const int64_t* n_fails, int64_t stride_fails, batmap_stream_t stream) {
+    if (!h || !h->shard_pending || !offsets || !n_fails) {
+        set_error("not a pending sharded build, or NULL arguments");
+        return BATMAP_E_INVALID;
+    }
+    const int N = h->shard_n_parts;
+    for (int p = 0; p < N; ++p) {
+        if (shard_words(h, p, N) > stride_words || n_fails[p] < 0 || n_fails[p] > stride_fails ||
+            (p == h->shard_part && n_fails[p] != h->shard_n_fail)) {
+            set_error("part %d: words/failure counts do not fit the strides or disagree with this part", p);
+            return BATMAP_E_INVALID;
+        }
+        if ((p != h->shard_part && shard_words(h, p, N) && !words_all) || (n_fails[p] && !fails_all)) {
+            set_error("NULL exchange buffer");
+            return BATMAP_E_INVALID;
+        }
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    BM_TRY(shard_import(h, offsets, tids, words_all, stride_words, fails_all, n_fails, stride_fails, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    return BATMAP_OK;
+}
+
 batmap_status batmap_pair_supports_ex(batmap_handle h, const int32_t* items, int64_t n_sel, uint32_t threshold,
                                       int32_t part, int32_t n_parts, uint32_t flags, batmap_triple* out,
                                       int64_t capacity, int64_t* n_out, batmap_stream_t stream) {
+    if (h && h->shard_pending) {
+        set_error("sharded build not complete: call batmap_shard_import first");
+        return BATMAP_E_INVALID;
+    }
     if (!h || !n_out || (!out && capacity > 0) || capacity < 0) {
         set_error("null handle / n_out / out");
         return BATMAP_E_INVALID;

@@ -160,6 +160,11 @@ struct batmap_collection {
     size_t cub_tmp_bytes = 0;
     // K2: plan of the full selection prepared during the build; counters of accumulated rectangles
     bm::K2Prepared* k2prep = nullptr;
+    // sharded build (batmap_build_shard): this part's failure records until batmap_shard_import
+    bool shard_pending = false;
+    int shard_part = 0, shard_n_parts = 1;
+    uint64_t* shard_fails_d = nullptr;
+    int64_t shard_n_fail = 0;
     uint32_t* cnt_d = nullptr;
     int64_t cnt_cap = 0;
     // selection scratch
@@ -217,7 +222,12 @@ batmap_status ensure(T** p, int64_t* cap, int64_t need, cudaStream_t s) {
 
 // build.cu
 batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
-                               const batmap_build_opts* o, cudaStream_t st);
+                               const batmap_build_opts* o, int part, int n_parts, cudaStream_t st);
+int64_t shard_words(const batmap_collection* h, int p, int n_parts);
+batmap_status shard_copy(batmap_collection* h, int p, int n_parts, uint32_t* packed, bool to_arena, cudaStream_t st);
+batmap_status shard_import(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
+                           const uint32_t* words_all, int64_t stride_words, const uint64_t* fails_all,
+                           const int64_t* n_fails, int64_t stride_fails, cudaStream_t st);
 // intersect.cu
 struct TileList {
     std::vector<int4> tiles;  // (a, b, ti, tj)

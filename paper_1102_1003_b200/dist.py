@@ -34,6 +34,41 @@ def gather_triples(local: torch.Tensor, dst: int = 0, group=None):
     return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
 
 
+def _all_gather_flat(t, group=None):
+    """Concatenation of every rank's equal-sized 1-D tensor `t` (rank order)."""
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=group)
+        return out
+    src = t.cpu()  # gloo (tests): host staging
+    parts = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(parts, src, group=group)
+    return torch.cat(parts).to(t.device)
+
+
+def build_distributed(offsets, tids, n_transactions: int, group=None, **kw):
+    """Sharded build: every rank builds the BatMaps of its share of each width
+    class (batmap_build_shard), the shares and failure records are all-gathered over the process
+    group (NCCL over NVLink on a B200 box), and batmap_shard_import completes every rank's handle.
+    Returns a Collection equivalent to a whole build on every rank."""
+    from .batmap import Collection
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    c = Collection(offsets, tids, n_transactions, part=rank, n_parts=world, **kw)
+    stride_w = max(c.shard_sizes(p)[0] for p in range(world))
+    nf = torch.tensor([c.shard_sizes(rank)[1]], dtype=torch.int64, device=offsets.device)
+    counts = _all_gather_flat(nf, group)
+    n_fails = [int(x) for x in counts.tolist()]
+    stride_f = max(max(n_fails), 1)
+    words = torch.empty(max(stride_w, 1), dtype=torch.int32, device=offsets.device)
+    fails = torch.empty(stride_f, dtype=torch.int64, device=offsets.device)
+    c.shard_export(words, fails)
+    c.shard_import(_all_gather_flat(words, group), words.numel(), _all_gather_flat(fails, group), n_fails, stride_f)
+    return c
+
+
 def pair_supports_distributed(coll, items=None, threshold: int = 1, dst: int = 0, group=None):
     """This rank's share of the pairs (batmap_pair_supports_part), gathered and sorted on `dst`."""
     from .batmap import sort_triples

@@ -1,5 +1,6 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): the tile partition and the gather of
-compacted triples that the N-GPU path uses.  The GPU parts (per-rank pair
+"""Multi-rank host logic on CPU (gloo, world_size 2): the tile partition, the flat all_gather of
+the sharded build's exchange and the gather of compacted triples that the N-GPU path uses
+(SURVEY §8(e)).  The GPU parts (per-rank pair
 supports, device merge-sort) are covered by tests/test_gpu_parity.py::test_items_subset_and_parts."""
 import os
 import socket
@@ -43,6 +44,13 @@ def _worker(rank, world, port, q):
         mine = full[full[:, 0] % world == rank]
         got = gather_triples(torch.as_tensor(mine))
         empty = gather_triples(torch.zeros((0, 3), dtype=torch.int32))  # empty parts are legal
+        # 3) the flat all_gather of the sharded build's exchange (dist.build_distributed)
+        from paper_1102_1003_b200.dist import _all_gather_flat
+
+        flat = _all_gather_flat(torch.arange(5, dtype=torch.int64) + 10 * rank)
+        flat_ok = flat.tolist() == [10 * r + k for r in range(world) for k in range(5)]
+        if not flat_ok:
+            raise AssertionError(f"all_gather_flat: {flat.tolist()}")
         if rank == 0:
             g = got.numpy()
             g = g[np.lexsort((g[:, 1], g[:, 0]))]

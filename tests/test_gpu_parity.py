@@ -191,6 +191,53 @@ def test_cluster_and_global_tiers(max_loop):
     np.testing.assert_array_equal(_np(c.pair_supports(threshold=0)), oracle.pairs_merge(off, tids, threshold=0))
 
 
+def _sharded(off, tids, m, n_parts, **kw):
+    """Build every part of a sharded build in this process and exchange as build_distributed
+    does (the all_gather is a concatenation here)."""
+    from paper_1102_1003_b200 import BatMapError
+
+    parts = [_coll(off, tids, m, part=p, n_parts=n_parts, **kw) for p in range(n_parts)]
+    with pytest.raises(BatMapError):
+        parts[0].pair_supports(threshold=1)  # incomplete until shard_import
+    sw = max(parts[0].shard_sizes(p)[0] for p in range(n_parts))
+    assert all(parts[q].shard_sizes(p)[0] == parts[0].shard_sizes(p)[0] for p in range(n_parts) for q in range(n_parts))
+    nf = [c.shard_sizes(c.part)[1] for c in parts]
+    sf = max(max(nf), 1)
+    words = torch.zeros(n_parts * sw, dtype=torch.int32, device="cuda")
+    fails = torch.zeros(n_parts * sf, dtype=torch.int64, device="cuda")
+    for p, c in enumerate(parts):
+        c.shard_export(words[p * sw:(p + 1) * sw], fails[p * sf:(p + 1) * sf])
+    for c in parts:
+        c.shard_import(words, sw, fails, nf, sf)
+    return parts
+
+
+@pytest.mark.parametrize("n_parts,serial,max_loop", [(2, False, 0), (3, True, 1), (4, False, 1), (5, True, 0)])
+def test_sharded_build_exchange(n_parts, serial, max_loop):
+    off, tids, m = _mixed(7, n=45)
+    parts = _sharded(off, tids, m, n_parts, seed=3, serial=serial, max_loop=max_loop)
+    ref = oracle.pairs_merge(off, tids, threshold=1)
+    whole = _coll(off, tids, m, seed=3, serial=serial, max_loop=max_loop)
+    for c in parts:
+        np.testing.assert_array_equal(_np(c.pair_supports(threshold=1)), ref)
+        if serial:  # the serial build is deterministic per item: shards reassemble the same bytes
+            assert c.info()["n_failures"] == whole.info()["n_failures"]
+            for i in range(len(off) - 1):
+                np.testing.assert_array_equal(c.export_entries(i), whole.export_entries(i))
+    if max_loop:
+        assert whole.info()["n_failures"] > 0
+
+
+def test_sharded_build_tiers_and_parts():
+    """Cluster and global tiers split across parts; each rank's share of the pairs after the exchange."""
+    off, tids, m = _tiers(5)
+    parts = _sharded(off, tids, m, 3, seed=2)
+    ref = oracle.pairs_merge(off, tids, threshold=1)
+    got = np.concatenate([_np(c.pair_supports(threshold=1, part=c.part, n_parts=3)) for c in parts])
+    got = got[np.lexsort((got[:, 1], got[:, 0]))]
+    np.testing.assert_array_equal(got, ref)
+
+
 # ----------------------------------------------------------------------------- end to end
 def _check_exact(off, tids, m, thr, items=None, **kw):
     c = _coll(off, tids, m, **kw)
