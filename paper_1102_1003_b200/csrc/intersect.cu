@@ -76,7 +76,8 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 //   v = ~p & (xm | ym)                  LOP3 (xm = x & M, ym = y & M from the mask plane; an
 //                                             explicit lop3, else ptxas recomputes (x|y)&M per pair)
 //   acc = dp4a(v, 0x01010101, acc)      IDP4A: every byte of v is 0x80 or 0
-// (tools/swar_ubench.cu measured this mix at 0.96 of R_int = 32 compares/clk/SM without LDS.)
+// (tools/swar_ubench.cu: this mix runs at 0.84 of R_int = 32 compares/clk/SM, with or without the
+// shared-memory operand loads -- the practical ceiling of the inner loop on B200.)
 __device__ __forceinline__ uint32_t swar_step(uint32_t x, uint32_t y, uint32_t xm, uint32_t ym, uint32_t acc) {
     const uint32_t u = (x ^ y) | 0x80808080u;
     const uint32_t p = u - 0x01010101u;
