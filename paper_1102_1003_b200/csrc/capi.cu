@@ -27,7 +27,7 @@ void free_all(batmap_collection* h) {
     void* ptrs[] = {h->pos2orig_d, h->orig2pos_d, h->arena_d,   h->f_d,      h->fail_off_d, h->fail_tid_d,
                     h->fidx_of_tid_d, h->ab_off_d, h->ab_pos_d, h->cand_d,   h->ctr_d,      h->key_d,
                     h->val_d,     h->cub_tmp,    h->sel_arena_d, h->sel_idx_d, h->res_d,
-                    h->cnt_d, h->shard_fails_d};
+                    h->cnt_d, h->tail_d, h->shard_fails_d};
     for (void* p : ptrs) dfree(p, st);
     if (h->k2prep) destroy_k2(h->k2prep, st);
     h->k2prep = nullptr;

@@ -167,6 +167,8 @@ struct batmap_collection {
     int64_t shard_n_fail = 0;
     uint32_t* cnt_d = nullptr;
     int64_t cnt_cap = 0;
+    uint32_t* tail_d = nullptr;  // partial counts of the cut tail tiles (k2_tiled -> k2_tail_threshold)
+    int64_t tail_cap = 0;
     // selection scratch
     uint32_t* sel_arena_d = nullptr;
     int64_t sel_arena_cap = 0;

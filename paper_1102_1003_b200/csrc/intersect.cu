@@ -278,8 +278,9 @@ __device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int
 // finished the previous chunk, so that buffer is refilled with the chunk kStages-1 ahead.
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     k2_tiled(const __grid_constant__ K2Maps prm, const Rect* __restrict__ rects, const Work* __restrict__ work,
-             int n_work, int* work_ctr, uint32_t* __restrict__ cnt, const int32_t* __restrict__ f, uint32_t thr,
-             uint32_t use_f, Cand* __restrict__ out, unsigned long long* __restrict__ ctr, int64_t cap) {
+             int n_work, int* work_ctr, uint32_t* __restrict__ cnt, uint32_t* __restrict__ tail_buf,
+             const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f, Cand* __restrict__ out,
+             unsigned long long* __restrict__ ctr, int64_t cap) {
     extern __shared__ __align__(1024) uint32_t smem_raw[];
     uint32_t* stages = smem_raw;  // keep the shared address space visible to the compiler (LDS, not LD)
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kStageSmem);
@@ -314,7 +315,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         const int2 mt = meta[buf];
         if (mt.y && cur >= 0) {  // a new work item (or the end) begins: finish the previous one
             const Work wk = work[cur];
-            work_epilogue(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, thr, use_f, out, ctr, cap);
+            if (wk.tail) {  // a piece of a cut tail tile: partial counts to its slice (thread-major)
+                uint4* dst = reinterpret_cast<uint4*>(tail_buf + (int64_t)(wk.tail - 1) * (kBM * kBN)) +
+                             threadIdx.x * 16;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    dst[2 * i] = make_uint4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+                    dst[2 * i + 1] = make_uint4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+                }
+            } else {
+                work_epilogue(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, thr, use_f, out, ctr, cap);
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -359,6 +370,42 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
             }
         }
     }
+}
+
+// Cut tail tiles: one CTA per tile sums its pieces' partial counts (same thread mapping as
+// k2_tiled) and runs the ordinary epilogue -- candidate test c + f_i + f_j >= s and append.
+__global__ void __launch_bounds__(kThreads) k2_tail_threshold(const TailTile* __restrict__ tails, int pieces,
+                                                              const Rect* __restrict__ rects,
+                                                              const uint32_t* __restrict__ tail_buf,
+                                                              const int32_t* __restrict__ f, uint32_t thr,
+                                                              uint32_t use_f, Cand* __restrict__ out,
+                                                              unsigned long long* __restrict__ ctr, int64_t cap) {
+    const TailTile t = tails[blockIdx.x];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tr = ((warp & 1) << 3) | (lane & 7);
+    const int tc = ((warp >> 1) << 2) | (lane >> 3);
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    for (int p = 0; p < pieces; ++p) {
+        const uint4* src = reinterpret_cast<const uint4*>(tail_buf + (int64_t)(blockIdx.x * pieces + p) * (kBM * kBN)) +
+                           threadIdx.x * 16;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint4 a = src[2 * i], b = src[2 * i + 1];
+            acc[i][0] += a.x;
+            acc[i][1] += a.y;
+            acc[i][2] += a.z;
+            acc[i][3] += a.w;
+            acc[i][4] += b.x;
+            acc[i][5] += b.y;
+            acc[i][6] += b.z;
+            acc[i][7] += b.w;
+        }
+    }
+    work_epilogue(rects[t.rect], t.ti, t.tj, tr, tc, lane, acc, nullptr, f, thr, use_f, out, ctr, cap);
 }
 
 // Accumulated rectangles: one CTA per owned tile row; candidate test on the summed counters.
@@ -578,6 +625,7 @@ struct K2Prepared {
     Rect* rects_d = nullptr;
     Work* work_d = nullptr;
     AccUnit* units_d = nullptr;
+    TailTile* tails_d = nullptr;
     uint32_t* virt_d = nullptr;
 };
 
@@ -588,7 +636,9 @@ void release_k2(K2Prepared* kp, cudaStream_t st) {
     dfree(kp->rects_d, st);
     dfree(kp->work_d, st);
     dfree(kp->units_d, st);
+    dfree(kp->tails_d, st);
     dfree(kp->virt_d, st);
+    kp->tails_d = nullptr;
     kp->rects_d = nullptr;
     kp->work_d = nullptr;
     kp->units_d = nullptr;
@@ -633,6 +683,11 @@ batmap_status prepare_k2(batmap_collection* h, const Selection& sel, int part, i
     if (!pl.units.empty())
         BM_CUDA(cudaMemcpyAsync(kp->units_d, pl.units.data(), pl.units.size() * sizeof(AccUnit),
                                 cudaMemcpyHostToDevice, st));
+    if (!pl.tails.empty()) {
+        BM_TRY(dalloc_t(&kp->tails_d, (int64_t)pl.tails.size(), st));
+        BM_CUDA(cudaMemcpyAsync(kp->tails_d, pl.tails.data(), pl.tails.size() * sizeof(TailTile),
+                                cudaMemcpyHostToDevice, st));
+    }
     return BATMAP_OK;
 }
 
@@ -706,6 +761,8 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         h->launches += 1;
     }
     if (pl.cnt_entries) BM_TRY(ensure(&h->cnt_d, &h->cnt_cap, pl.cnt_entries, st));
+    const int64_t tail_words = (int64_t)pl.tails.size() * pl.tail_pieces * kBM * kBN;
+    if (tail_words) BM_TRY(ensure(&h->tail_d, &h->tail_cap, tail_words, st));
     static bool attr_set = false;
     if (!attr_set) {
         BM_CUDA(cudaFuncSetAttribute(k2_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
@@ -722,10 +779,17 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, 2 * sizeof(unsigned long long), st));  // [1] = work counter
         if (pl.cnt_entries) BM_CUDA(cudaMemsetAsync(h->cnt_d, 0, pl.cnt_entries * sizeof(uint32_t), st));
         rec(h, EV_K20, st);
-        k2_tiled<<<grid, kThreads, kSmemBytes, st>>>(*prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, sel.f,
-                                                     threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
+        k2_tiled<<<grid, kThreads, kSmemBytes, st>>>(*prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d,
+                                                     h->tail_d, sel.f, threshold, use_f, h->cand_d, h->ctr_d,
+                                                     h->cand_cap);
         rec(h, EV_K21, st);
         h->launches += 1;
+        if (!pl.tails.empty()) {
+            k2_tail_threshold<<<(unsigned)pl.tails.size(), kThreads, 0, st>>>(
+                kp->tails_d, pl.tail_pieces, rects_d, h->tail_d, sel.f, threshold, use_f, h->cand_d, h->ctr_d,
+                h->cand_cap);
+            h->launches += 1;
+        }
         if (!pl.units.empty()) {
             k2_acc_threshold<<<(unsigned)pl.units.size(), 256, 0, st>>>(units_d, rects_d, h->cnt_d, sel.f, threshold,
                                                                         use_f, h->cand_d, h->ctr_d, h->cand_cap);

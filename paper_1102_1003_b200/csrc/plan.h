@@ -29,7 +29,12 @@ struct Rect {
 };
 
 struct Work {   // one work item: tile (ti, tj) of a rectangle over k-chunks [k0, k1)
-    int32_t rect, ti, tj, k0, k1, pad;
+    int32_t rect, ti, tj, k0, k1;
+    int32_t tail;  // 0, or 1 + the slice of the tail buffer this piece of a cut tail tile writes
+};
+
+struct TailTile {  // a whole tile of an ordinary rectangle, cut into pieces at the end of the schedule
+    int32_t rect, ti, tj, pad;
 };
 
 struct AccUnit {  // a tile row (rect, ti) of an accumulated rectangle owned by this part
@@ -46,6 +51,8 @@ struct Plan {
     std::vector<Work> work;       // this part's work items, longest first
     std::vector<AccUnit> units;   // this part's tile rows of accumulated rectangles
     std::vector<VirtCopy> virt;
+    std::vector<TailTile> tails;  // cut tail tiles; piece p of tail t writes slice t * tail_pieces + p
+    int32_t tail_pieces = 0;
     int64_t virt_words = 0;
     int64_t cnt_entries = 0;
     int64_t word_compares = 0;    // algorithmic: sum over this part's pairs of max(W_i, W_j)

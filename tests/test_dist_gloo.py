@@ -33,7 +33,9 @@ def _worker(rank, world, port, q):
         # 1) the planner's share of this rank: gather every rank's tiles and check exact cover
         class_n, class_w = [7800, 2200], [1536, 3072]
         items, wc, work = plan_work(class_n, class_w, rank, world)
-        t = torch.as_tensor(items[:, :3].copy())
+        # (tile key, tile column, k-chunks) per work item; tiles may be cut into k pieces
+        t = torch.as_tensor(np.stack([items[:, 0] * 100000 + items[:, 1] * 1000 + items[:, 2], items[:, 3],
+                                      items[:, 5] - items[:, 4]], 1).astype(np.int32))
         allt = gather_triples(t)
         w = torch.tensor([work], dtype=torch.int64)
         ws = [torch.zeros_like(w) for _ in range(world)]
@@ -54,7 +56,9 @@ def _worker(rank, world, port, q):
         if rank == 0:
             g = got.numpy()
             g = g[np.lexsort((g[:, 1], g[:, 0]))]
-            q.put(("ok", allt.shape[0], [int(x) for x in ws], bool(np.array_equal(g, full)), empty.shape[0]))
+            a = allt.numpy()
+            cover = (len({(int(x), int(y)) for x, y, _ in a}), int(a[:, 2].sum()))
+            q.put(("ok", cover, [int(x) for x in ws], bool(np.array_equal(g, full)), empty.shape[0]))
         else:
             q.put(("ok", None if got is None else -1, None, got is None, None if empty is None else -1))
     except Exception as e:  # pragma: no cover
@@ -78,8 +82,9 @@ def test_gather_and_partition_world2():
     r0 = [r for r in res if r[1] is not None and r[1] != -1][0]
     from paper_1102_1003_b200 import plan_work
 
-    n_all = len(plan_work([7800, 2200], [1536, 3072], 0, 1)[0])
-    assert r0[1] == n_all  # the ranks' tile lists cover the triangle exactly once
+    full = plan_work([7800, 2200], [1536, 3072], 0, 1)[0]
+    n_tiles = len({(int(a) * 100000 + int(b) * 1000 + int(ti), int(tj)) for a, b, ti, tj in full[:, :4]})
+    assert r0[1] == (n_tiles, int((full[:, 5] - full[:, 4]).sum()))  # the ranks cover every tile and chunk once
     assert abs(r0[2][0] - r0[2][1]) <= 128 * 128 * 3072  # balanced within one tile
     assert r0[3] is True  # gathered triples == the full result
     assert r0[4] == 0
