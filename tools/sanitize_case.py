@@ -1,4 +1,7 @@
-"""Small end-to-end case for compute-sanitizer (memcheck / racecheck / synccheck / initcheck)."""
+"""Small end-to-end case for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+every build tier (CTA, cluster of 1/2/4 CTAs over DSMEM), serial and concurrent builds with
+forced failures, item subsets, a sharded build exchanged in-process, the cut tail tiles of K2,
+and (not under initcheck, whose reads of cuBLASLt's output are false positives) the dense path."""
 import os
 import sys
 
@@ -10,18 +13,40 @@ import oracle  # noqa: E402
 from paper_1102_1003_b200 import Collection, dense_pair_supports  # noqa: E402
 from workloads import uniform  # noqa: E402
 
-off, tids = uniform(300, 20000, 0.02, 7)
 m = 20000
+off0, tids0 = uniform(300, m, 0.02, 7)
+rng = np.random.default_rng(8)
+rows = [tids0[off0[i]:off0[i + 1]] for i in range(len(off0) - 1)]
+for size in (3000, 3500, 9000, 17000):  # r = 8192 (cluster of 1), 32768 (2), 65536 (4)
+    rows.append(np.sort(rng.choice(m, size=size, replace=False)).astype(np.int32))
+off = np.zeros(len(rows) + 1, np.int64)
+off[1:] = np.cumsum([len(r) for r in rows])
+tids = np.concatenate(rows)
+n = len(rows)
 ref = oracle.pairs_horizontal(off, tids, m, threshold=2)
 o, t = torch.as_tensor(off).cuda(), torch.as_tensor(tids).cuda()
 for serial in (False, True):
     c = Collection(o, t, m, seed=3, max_loop=2, serial=serial)  # forced failures exercise K3
     got = c.pair_supports(threshold=2).cpu().numpy().astype(np.uint32)
     assert np.array_equal(got, ref)
-    sub = np.arange(0, 300, 3, dtype=np.int32)
-    got = c.pair_supports(sub, threshold=2).cpu().numpy().astype(np.uint32)
+    sub = np.arange(0, n, 3, dtype=np.int32)
+    got = c.pair_supports(torch.as_tensor(sub).cuda(), threshold=2).cpu().numpy().astype(np.uint32)
     assert np.array_equal(got, oracle.pairs_horizontal(off, tids, m, items=sub, threshold=2))
     c.close()
-d, _ = dense_pair_supports(o, t, m, threshold=2)
-assert np.array_equal(d.cpu().numpy().astype(np.uint32), ref)
+# sharded build, two parts exchanged in this process
+parts = [Collection(o, t, m, seed=4, max_loop=2, part=p, n_parts=2) for p in range(2)]
+sw = max(parts[0].shard_sizes(p)[0] for p in range(2))
+nf = [c.shard_sizes(c.part)[1] for c in parts]
+sf = max(max(nf), 1)
+words = torch.zeros(2 * sw, dtype=torch.int32, device="cuda")
+fails = torch.zeros(2 * sf, dtype=torch.int64, device="cuda")
+for p, c in enumerate(parts):
+    c.shard_export(words[p * sw:(p + 1) * sw], fails[p * sf:(p + 1) * sf])
+for c in parts:
+    c.shard_import(words, sw, fails, nf, sf)
+    assert np.array_equal(c.pair_supports(threshold=2).cpu().numpy().astype(np.uint32), ref)
+    c.close()
+if os.environ.get("SANITIZE_TOOL") != "initcheck":
+    d, _ = dense_pair_supports(o, t, m, threshold=2)
+    assert np.array_equal(d.cpu().numpy().astype(np.uint32), ref)
 print("sanitize case ok", len(ref))
