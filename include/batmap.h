@@ -260,6 +260,19 @@ batmap_status batmap_dense_pair_supports(const int64_t* offsets, const int32_t* 
                                          uint32_t threshold, batmap_triple* out, int64_t capacity,
                                          int64_t* n_out, double* gemm_ms, batmap_stream_t stream);
 
+/*
+ * batmap_merge_pair_supports -- NEXT-2 comparison path, NOT the BatMap method: the same triples
+ * by sorted-list merging (a + b steps per pair of lengths a, b), the
+ * intersection the paper compares BatMaps with.  Arguments as batmap_dense_pair_supports;
+ * kernel_ms [host] or NULL: device time of the merge kernel; merge_steps [host] or NULL: the
+ * algorithmic step count sum over pairs of (a + b).  Tidlists must be strictly increasing.
+ */
+batmap_status batmap_merge_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                                         int64_t n_transactions, const int32_t* items, int64_t n_sel,
+                                         uint32_t threshold, batmap_triple* out, int64_t capacity,
+                                         int64_t* n_out, double* kernel_ms, int64_t* merge_steps,
+                                         batmap_stream_t stream);
+
 /* ---------------------------------------------------------------- inspection / test hooks */
 
 /*

@@ -8,6 +8,7 @@ from .batmap import (  # noqa: F401
     Collection,
     dense_pair_supports,
     load_library,
+    merge_pair_supports,
     mine_host,
     plan_work,
     sort_triples,

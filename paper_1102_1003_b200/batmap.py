@@ -90,6 +90,8 @@ def load_library():
         "batmap_sort_triples": ([P, I64, P], ctypes.c_int),
         "batmap_dense_pair_supports": ([P, P, I64, I64, P, I64, U32, P, I64, PI64, ctypes.POINTER(ctypes.c_double), P],
                                        ctypes.c_int),
+        "batmap_merge_pair_supports": ([P, P, I64, I64, P, I64, U32, P, I64, PI64, ctypes.POINTER(ctypes.c_double),
+                                        PI64, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -313,6 +315,34 @@ def dense_pair_supports(offsets, tids, n_transactions: int, items=None, threshol
         cap = int(n_out.value)
     _check(rc)
     return out[: n_out.value], float(ms.value)
+
+
+def merge_pair_supports(offsets, tids, n_transactions: int, items=None, threshold: int = 1, *, stream=None,
+                        capacity: int | None = None):
+    """NEXT-2 comparison path (batmap_merge_pair_supports): sorted-list merging.
+    Returns (int32 tensor [K, 3] sorted by (i, j), kernel_ms, merge_steps)."""
+    import torch
+
+    lib = load_library()
+    offsets = offsets.contiguous().to(torch.int64)
+    tids = tids.contiguous().to(torch.int32)
+    it = None if items is None else torch.as_tensor(np.asarray(items) if not hasattr(items, "is_cuda") else items) \
+        .to(device="cuda", dtype=torch.int32).contiguous()
+    n_sel = 0 if it is None else it.numel()
+    cap = capacity if capacity is not None else 1 << 16
+    n_out = ctypes.c_int64(0)
+    ms = ctypes.c_double(0)
+    steps = ctypes.c_int64(0)
+    for _ in range(2):
+        out = torch.empty((max(cap, 1), 3), dtype=torch.int32, device="cuda")
+        rc = lib.batmap_merge_pair_supports(_dptr(offsets), _dptr(tids), offsets.numel() - 1, int(n_transactions),
+                                            _dptr(it), n_sel, int(threshold), _dptr(out), cap, ctypes.byref(n_out),
+                                            ctypes.byref(ms), ctypes.byref(steps), _stream_ptr(stream))
+        if rc != BATMAP_E_CAPACITY:
+            break
+        cap = int(n_out.value)
+    _check(rc)
+    return out[: n_out.value], float(ms.value), int(steps.value)
 
 
 def sort_triples(t, stream=None):

@@ -330,6 +330,35 @@ batmap_status batmap_dense_pair_supports(const int64_t* offsets, const int32_t* 
                                gemm_ms, st);
 }
 
+batmap_status batmap_merge_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                                         int64_t n_transactions, const int32_t* items, int64_t n_sel,
+                                         uint32_t threshold, batmap_triple* out, int64_t capacity, int64_t* n_out,
+                                         double* kernel_ms, int64_t* merge_steps, batmap_stream_t stream) {
+    if (!offsets || (!tids && n_items > 0) || !n_out || (!out && capacity > 0) || n_items < 0 ||
+        n_transactions < 1 || (items && n_sel < 0)) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    if (n_items >= (1ll << 31) || n_transactions >= (1ll << 31)) {
+        set_error("n_items and n_transactions must be < 2^31");
+        return BATMAP_E_OVERFLOW;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (items && n_sel) {  // validate the selection on the host
+        std::vector<int32_t> it(n_sel);
+        BM_CUDA(cudaMemcpyAsync(it.data(), items, n_sel * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        std::sort(it.begin(), it.end());
+        for (int64_t k = 0; k < n_sel; ++k)
+            if (it[k] < 0 || it[k] >= n_items || (k && it[k] == it[k - 1])) {
+                set_error("items must be distinct ids in [0, n_items)");
+                return BATMAP_E_INVALID;
+            }
+    }
+    return merge_pair_supports(offsets, tids, n_items, items, n_sel, threshold, out, capacity, n_out, kernel_ms,
+                               merge_steps, st);
+}
+
 batmap_status batmap_sort_triples(batmap_triple* triples, int64_t n, batmap_stream_t stream) {
     if (!triples && n > 0) {
         set_error("null triples");

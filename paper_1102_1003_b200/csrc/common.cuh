@@ -226,6 +226,11 @@ batmap_status ensure(T** p, int64_t* cap, int64_t need, cudaStream_t s) {
 batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
                                const batmap_build_opts* o, int part, int n_parts, cudaStream_t st);
 int64_t shard_words(const batmap_collection* h, int p, int n_parts);
+batmap_status emit_sorted_keys(uint64_t* keys, uint32_t* vals, int64_t K, int64_t cap, batmap_triple* out,
+                               cudaStream_t st);
+batmap_status merge_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items, const int32_t* items,
+                                  int64_t n_sel, uint32_t threshold, batmap_triple* out, int64_t capacity,
+                                  int64_t* n_out, double* kernel_ms, int64_t* merge_steps, cudaStream_t st);
 batmap_status shard_copy(batmap_collection* h, int p, int n_parts, uint32_t* packed, bool to_arena, cudaStream_t st);
 batmap_status shard_import(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
                            const uint32_t* words_all, int64_t stride_words, const uint64_t* fails_all,

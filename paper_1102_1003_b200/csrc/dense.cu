@@ -166,6 +166,30 @@ static batmap_status gemm_int8(const int8_t* A, const int8_t* B, int32_t* C, int
     return rc;
 }
 
+// (key = i << 32 | j, value = support) pairs in keys[0, K) / vals[0, K) (each buffer 2 cap long:
+// the radix sort's double buffer) -> out[0, K) sorted by (i, j); synchronises st.
+batmap_status emit_sorted_keys(uint64_t* keys, uint32_t* vals, int64_t K, int64_t cap, batmap_triple* out,
+                               cudaStream_t st) {
+    if (K > 1) {
+        cub::DoubleBuffer<uint64_t> dk(keys, keys + cap);
+        cub::DoubleBuffer<uint32_t> dv(vals, vals + cap);
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)K, 0, 64, st);
+        void* tmp = nullptr;
+        BM_TRY(dalloc(&tmp, tb + 16, st));
+        cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)K, 0, 64, st);
+        k_dense_emit<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(dk.Current(), dv.Current(), K, out);
+        dfree(tmp, st);
+    } else if (K == 1) {
+        k_dense_emit<<<1, 32, 0, st>>>(keys, vals, 1, out);
+    }
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        set_error("sort/emit of the result: %s", cudaGetErrorString(cudaGetLastError()));
+        return BATMAP_E_CUDA;
+    }
+    return BATMAP_OK;
+}
+
 batmap_status dense_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t m,
                                   const int32_t* items, int64_t n_sel, uint32_t threshold, batmap_triple* out,
                                   int64_t capacity, int64_t* n_out, double* gemm_ms, cudaStream_t st) {
@@ -261,23 +285,7 @@ batmap_status dense_pair_supports(const int64_t* offsets, const int32_t* tids, i
             rc = BATMAP_E_CAPACITY;
             break;
         }
-        if (K > 1) {
-            cub::DoubleBuffer<uint64_t> dk(keys, keys + cap);
-            cub::DoubleBuffer<uint32_t> dv(vals, vals + cap);
-            size_t tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)K, 0, 64, st);
-            void* tmp = nullptr;
-            if ((rc = dalloc(&tmp, tb + 16, st)) != BATMAP_OK) break;
-            cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)K, 0, 64, st);
-            k_dense_emit<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(dk.Current(), dv.Current(), (int64_t)K, out);
-            dfree(tmp, st);
-        } else if (K == 1) {
-            k_dense_emit<<<1, 32, 0, st>>>(keys, vals, 1, out);
-        }
-        if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
-            set_error("dense path: %s", cudaGetErrorString(cudaGetLastError()));
-            rc = BATMAP_E_CUDA;
-        }
+        rc = emit_sorted_keys(keys, vals, (int64_t)K, cap, out, st);
         break;
     }
     cleanup();

@@ -400,3 +400,54 @@ def test_dense_xtx_c2_equals_batmap():
     got, ms = _dense(w.offsets, w.tids, w.m, w.threshold)
     np.testing.assert_array_equal(got, oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=w.threshold))
     assert ms > 0
+
+
+# ----------------------------------------------------------------------------- NEXT-2 sorted merge
+def _merge(off, tids, m, thr, items=None):
+    from paper_1102_1003_b200 import merge_pair_supports
+
+    t, ms, steps = merge_pair_supports(torch.as_tensor(off).cuda(), torch.as_tensor(tids).cuda(), m, items=items,
+                                       threshold=thr)
+    return _np(t), ms, steps
+
+
+def test_merge_exact_small_subset_and_edges():
+    w = make_config("C1", scale_items=0.3)
+    got, _, steps = _merge(w.offsets, w.tids, w.m, 0)  # every pair, zeros included
+    np.testing.assert_array_equal(got, oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=0))
+    lens = np.diff(w.offsets)
+    assert steps == (len(lens) - 1) * int(lens.sum())  # sum over pairs of (a + b)
+    w = make_config("C1")
+    items = np.random.default_rng(6).choice(w.n, size=600, replace=False).astype(np.int32)
+    got, _, _ = _merge(w.offsets, w.tids, w.m, 2, items=items)
+    np.testing.assert_array_equal(got, oracle.pairs_horizontal(w.offsets, w.tids, w.m, items=items, threshold=2))
+    # empty lists, a single long list against short ones, identical lists, windows refilled many times
+    rows = [np.array([], np.int32), np.arange(0, 5000, 1, dtype=np.int32), np.arange(0, 5000, 7, dtype=np.int32),
+            np.arange(3, 5000, 7, dtype=np.int32), np.arange(0, 5000, 1, dtype=np.int32), np.array([4999], np.int32)]
+    off = np.zeros(len(rows) + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    tids = np.concatenate(rows)
+    got, _, _ = _merge(off, tids, 5000, 0)
+    np.testing.assert_array_equal(got, oracle.pairs_merge(off, tids, threshold=0))
+
+
+def test_merge_c2_equals_batmap_and_oracle():
+    w = make_config("C2")
+    got, ms, _ = _merge(w.offsets, w.tids, w.m, w.threshold)
+    np.testing.assert_array_equal(got, oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=w.threshold))
+    assert ms > 0
+
+
+@pytest.mark.parametrize("long_len", [9000, 60000])
+def test_merge_long_rows_from_global(long_len):
+    """Lists too long to stage in shared memory (one S_i + 8 S_j per CTA) take the global-memory
+    variant."""
+    rng = np.random.default_rng(9)
+    m = 200000
+    rows = [np.sort(rng.choice(m, size=long_len, replace=False)).astype(np.int32)]
+    rows += [np.sort(rng.choice(m, size=int(k), replace=False)).astype(np.int32) for k in rng.integers(10, 3000, 40)]
+    off = np.zeros(len(rows) + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    tids = np.concatenate(rows)
+    got, _, _ = _merge(off, tids, m, 1)
+    np.testing.assert_array_equal(got, oracle.pairs_merge(off, tids, threshold=1))

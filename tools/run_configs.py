@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
-from paper_1102_1003_b200 import Collection, dense_pair_supports  # noqa: E402
+from paper_1102_1003_b200 import Collection, dense_pair_supports, merge_pair_supports  # noqa: E402
 from workloads import CONFIGS, make_config, to_horizontal  # noqa: E402
 
 
@@ -72,6 +72,16 @@ def run(name, reps=3):
         ops = 2.0 * w.n * w.n / 2 * w.m
         dense = dict(total_ms=best_d[0], gemm_ms=best_d[1], equal_to_batmap=bool(np.array_equal(dgot, got)),
                      int8_tops=ops / (best_d[1] / 1e3) / 1e12)
+    merge = None
+    lens = np.diff(w.offsets)
+    if (w.n - 1) * float(lens.sum()) <= 2e12:  # NEXT-2 comparison: sorted-list merging on the GPU
+        best_m = None
+        for _ in range(2):
+            mt, mms, msteps = merge_pair_supports(off_d, tids_d, w.m, threshold=w.threshold, capacity=int(got.shape[0]) + 16)
+            if best_m is None or mms < best_m[0]:
+                best_m = (mms, msteps, mt)
+        merge = dict(kernel_ms=best_m[0], merge_steps=best_m[1], steps_per_s=best_m[1] / (best_m[0] / 1e3),
+                     equal_to_batmap=bool(np.array_equal(best_m[2].cpu().numpy().astype(np.uint32), got)))
     n = w.n
     pairs = n * (n - 1) // 2
     peak = 32 * torch.cuda.get_device_properties(0).multi_processor_count * 1.965e9
@@ -82,7 +92,8 @@ def run(name, reps=3):
                 word_compares=st["word_compares"], tile_compares=st["tile_compares"],
                 pairs_per_s=pairs / (tot / 1e3), freq_pairs_per_s=got.shape[0] / (tot / 1e3),
                 k2_frac_R_int=(st["word_compares"] / (st["k2_ms"] / 1e3) / peak) if st["k2_ms"] > 0 else None,
-                exact=exact, parity=how, oracle_s=round(oracle_s, 1), gen_s=round(gen_s, 1), dense_xtx=dense)
+                exact=exact, parity=how, oracle_s=round(oracle_s, 1), gen_s=round(gen_s, 1), dense_xtx=dense,
+                merge=merge)
     print(json.dumps(line), flush=True)
     return exact
 
