@@ -187,7 +187,11 @@ def test_cluster_and_global_tiers(max_loop):
     assert {2 ** 14, 2 ** 15, 2 ** 16, 2 ** 17, 2 ** 18} <= set(rs)
     _check_layout_invariants(c, off, tids, m, 6)
     if max_loop:
-        assert c.info()["n_failures"] > 2000  # per-CTA failure lists overflow: the rescan path runs
+        # some item's failure list overflows its 512-entry shared-memory list (kConcFailCap in
+        # build.cu), so the global rescan path runs (the total count varies run to run: the
+        # concurrent build is nondeterministic, reading #9b)
+        per_item = np.bincount(c.failures()[:, 0], minlength=len(off) - 1)
+        assert per_item.max() > 512, per_item
     np.testing.assert_array_equal(_np(c.pair_supports(threshold=0)), oracle.pairs_merge(off, tids, threshold=0))
 
 
