@@ -303,7 +303,8 @@ batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n
  * batmap_plan_work -- host-only view of the intersection planner (no device needed).  For width
  * classes a = 0..n_classes-1 with class_n[a] items of class_w[a] words (class_w ascending, each a
  * multiple of 16), lists the work items of `part` of `n_parts` in execution order.  A work item is
- * the 128 x 128 tile (ti, tj) of the class rectangle (a, b), a <= b (tj >= ti when a == b), over
+ * the 128 x 128 tile (ti, tj) of the class rectangle (a, b) of PLANNED classes (see
+ * batmap_plan_groups; equal to the input classes when nothing is promoted), a <= b (tj >= ti when a == b), over
  * k-chunks [k0, k1) of 16 words; R > 1 marks a virtualised rectangle (each class-b BatMap viewed as
  * R columns of class_w[a] words); acc = 1 marks rectangles whose partial counts are summed in
  * global counters (virtualised or split along k).
@@ -316,6 +317,22 @@ batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const 
                                int32_t part, int32_t n_parts, int32_t grid_cap, int32_t* items,
                                int64_t capacity, int64_t* n_items, int64_t* word_compares,
                                int64_t* tile_compares);
+
+/*
+ * batmap_plan_groups -- host-only view of the planner's class promotion (no device needed).  The
+ * planner may merge a run of adjacent width classes (typically small, narrow ones whose own
+ * 128 x 128 tiles would be mostly padding) into ONE planned class of the widest member's width W:
+ * each narrower BatMap is replicated along k, B'[w] = B[w mod W_i] (valid because every width is
+ * 3r/4 with r a power of two, so W_i | W).  A pair of planned widths then compares K words, which
+ * is K / max(W_i, W_j) times the wrap-around count of P:218-219; the epilogue divides
+ * exactly.  Same input conventions as batmap_plan_work.  Set the environment variable
+ * BATMAP_K2_PROMOTE=0 to disable promotion (both here and in batmap_pair_supports*).
+ *   group_of  [host] n_classes int32: planned class of each input class (non-decreasing; the
+ *             `a`, `b` of batmap_plan_work's items index these planned classes).
+ * Errors: E_INVALID on bad arguments.
+ */
+batmap_status batmap_plan_groups(int32_t n_classes, const int64_t* class_n, const int64_t* class_w,
+                                 int32_t* group_of);
 
 #ifdef __cplusplus
 }

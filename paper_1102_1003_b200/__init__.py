@@ -10,6 +10,7 @@ from .batmap import (  # noqa: F401
     load_library,
     merge_pair_supports,
     mine_host,
+    plan_groups,
     plan_work,
     sort_triples,
     swar_device,

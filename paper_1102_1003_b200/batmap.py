@@ -86,6 +86,7 @@ def load_library():
         "batmap_export_failures": ([P, P, P, I64, PI64], ctypes.c_int),
         "batmap_swar_device": ([P, P, I64, P, P], ctypes.c_int),
         "batmap_plan_work": ([I32, P, P, I32, I32, I32, P, I64, PI64, PI64, PI64], ctypes.c_int),
+        "batmap_plan_groups": ([I32, P, P, P], ctypes.c_int),
         "batmap_stats": ([P, ctypes.POINTER(Stats)], ctypes.c_int),
         "batmap_sort_triples": ([P, I64, P], ctypes.c_int),
         "batmap_dense_pair_supports": ([P, P, I64, I64, P, I64, U32, P, I64, PI64, ctypes.POINTER(ctypes.c_double), P],
@@ -362,6 +363,17 @@ def swar_device(x, y, stream=None):
     out = torch.empty(2 * max(n, 1), dtype=torch.int32, device="cuda")
     _check(load_library().batmap_swar_device(_dptr(x), _dptr(y), n, _dptr(out), _stream_ptr(stream)))
     return out[:n], out[n:2 * n]
+
+
+def plan_groups(class_n, class_w):
+    """Host-only planner view (batmap_plan_groups): int32 [C] planned class of each input class."""
+    lib = load_library()
+    cn = np.ascontiguousarray(class_n, dtype=np.int64)
+    cw = np.ascontiguousarray(class_w, dtype=np.int64)
+    out = np.empty(max(cn.shape[0], 1), dtype=np.int32)
+    _check(lib.batmap_plan_groups(cn.shape[0], cn.ctypes.data_as(ctypes.c_void_p), cw.ctypes.data_as(ctypes.c_void_p),
+                                  out.ctypes.data_as(ctypes.c_void_p)))
+    return out[: cn.shape[0]]
 
 
 def plan_work(class_n, class_w, part: int = 0, n_parts: int = 1, grid_cap: int = 0):

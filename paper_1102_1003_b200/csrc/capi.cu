@@ -475,18 +475,18 @@ batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n
     return swar_device(x, y, n, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
-batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const int64_t* class_w, int32_t part,
-                               int32_t n_parts, int32_t grid_cap, int32_t* items, int64_t capacity, int64_t* n_items,
-                               int64_t* word_compares, int64_t* tile_compares) {
-    if (n_classes < 0 || (n_classes && (!class_n || !class_w)) || !n_items || !word_compares || !tile_compares ||
-        n_parts < 1 || part < 0 || part >= n_parts || grid_cap < 0) {
-        set_error("bad arguments");
-        return BATMAP_E_INVALID;
-    }
-    std::vector<ClassInfo> cls(n_classes);
+static bool promote_enabled() {
+    const char* e = getenv("BATMAP_K2_PROMOTE");
+    return !(e && e[0] == '0');
+}
+
+static batmap_status plan_classes(int32_t n_classes, const int64_t* class_n, const int64_t* class_w,
+                                  std::vector<ClassInfo>* out) {
+    std::vector<ClassInfo>& cls = *out;
+    cls.assign(n_classes, ClassInfo{});
     int64_t first = 0;
     for (int a = 0; a < n_classes; ++a) {
-        if (class_w[a] <= 0 || class_w[a] % kChunk || (a && class_w[a] < class_w[a - 1])) {
+        if (class_w[a] <= 0 || class_w[a] % kChunk || (a && class_w[a] < class_w[a - 1]) || class_n[a] < 0) {
             set_error("class_w must be ascending multiples of %d", kChunk);
             return BATMAP_E_INVALID;
         }
@@ -496,8 +496,35 @@ batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const 
         cls[a].n_pad = (int32_t)((class_n[a] + kPadItems - 1) / kPadItems * kPadItems);
         first += class_n[a];
     }
+    return BATMAP_OK;
+}
+
+batmap_status batmap_plan_groups(int32_t n_classes, const int64_t* class_n, const int64_t* class_w,
+                                 int32_t* group_of) {
+    if (n_classes < 0 || (n_classes && (!class_n || !class_w || !group_of))) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    std::vector<ClassInfo> cls;
+    BM_TRY(plan_classes(n_classes, class_n, class_w, &cls));
     Plan pl;
-    plan_work(cls, part, n_parts, grid_cap ? grid_cap : 2 * 148, true, true, &pl);
+    plan_work(cls, 0, 1, 2 * 148, true, true, promote_enabled(), &pl);
+    for (int a = 0; a < n_classes; ++a) group_of[a] = pl.eff_of[a];
+    return BATMAP_OK;
+}
+
+batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const int64_t* class_w, int32_t part,
+                               int32_t n_parts, int32_t grid_cap, int32_t* items, int64_t capacity, int64_t* n_items,
+                               int64_t* word_compares, int64_t* tile_compares) {
+    if (n_classes < 0 || (n_classes && (!class_n || !class_w)) || !n_items || !word_compares || !tile_compares ||
+        n_parts < 1 || part < 0 || part >= n_parts || grid_cap < 0) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    std::vector<ClassInfo> cls;
+    BM_TRY(plan_classes(n_classes, class_n, class_w, &cls));
+    Plan pl;
+    plan_work(cls, part, n_parts, grid_cap ? grid_cap : 2 * 148, true, true, promote_enabled(), &pl);
     *n_items = (int64_t)pl.work.size();
     *word_compares = pl.word_compares;
     *tile_compares = pl.tile_compares;

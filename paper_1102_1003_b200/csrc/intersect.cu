@@ -216,17 +216,18 @@ __device__ __forceinline__ void append_candidates(uint64_t mask, int cnt, int la
 // End of a work item: ordinary rectangles test c + f_i + f_j >= thr and append; accumulated ones
 // add the partial counts to their counters (4 adjacent virtual columns of one item pre-summed).
 __device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int tr, int tc, int lane,
-                                              const uint32_t (&acc)[8][8], uint32_t* __restrict__ cnt,
-                                              const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f,
-                                              Cand* __restrict__ out, unsigned long long* __restrict__ ctr,
-                                              int64_t cap) {
+                                              const uint32_t (&acc_in)[8][8], uint32_t* __restrict__ cnt,
+                                              const int32_t* __restrict__ f, const uint8_t* __restrict__ lw,
+                                              uint32_t thr, uint32_t use_f, Cand* __restrict__ out,
+                                              unsigned long long* __restrict__ ctr, int64_t cap) {
     int rows[8], cols[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         rows[i] = ti * kBM + (i < 4 ? 4 * tr + i : 64 + 4 * tr + (i - 4));
         cols[i] = tj * kBN + (i < 4 ? 4 * tc + i : 64 + 4 * tc + (i - 4));
     }
-    if (r.acc) {
+    if (r.acc) {  // scaled partial counts; k2_acc_threshold divides promoted pairs
+        const uint32_t (&acc)[8][8] = acc_in;
         uint32_t* base = cnt + r.cnt_off;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -250,6 +251,23 @@ __device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int
             }
         }
         return;
+    }
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = acc_in[i][j];
+    if (r.promo) {  // promoted pairs compared K = 2^lgK W_min words: K / max(W_i, W_j) times the count
+        int lr[8], lc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            lr[i] = rows[i] < r.n_rows ? (int)__ldg(lw + r.row_first + rows[i]) : 0;
+            lc[i] = cols[i] < r.n_cols ? (int)__ldg(lw + r.col_first + cols[i]) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = ((acc[i][j] >> 7) >> (r.lgK - max(lr[i], lc[j]))) << 7;
     }
     uint32_t fr[8], fc[8];
 #pragma unroll
@@ -279,8 +297,8 @@ __device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     k2_tiled(const __grid_constant__ K2Maps prm, const Rect* __restrict__ rects, const Work* __restrict__ work,
              int n_work, int* work_ctr, uint32_t* __restrict__ cnt, uint32_t* __restrict__ tail_buf,
-             const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f, Cand* __restrict__ out,
-             unsigned long long* __restrict__ ctr, int64_t cap) {
+             const int32_t* __restrict__ f, const uint8_t* __restrict__ lw, uint32_t thr, uint32_t use_f,
+             Cand* __restrict__ out, unsigned long long* __restrict__ ctr, int64_t cap) {
     extern __shared__ __align__(1024) uint32_t smem_raw[];
     uint32_t* stages = smem_raw;  // keep the shared address space visible to the compiler (LDS, not LD)
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kStageSmem);
@@ -324,7 +342,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
                     dst[2 * i + 1] = make_uint4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
                 }
             } else {
-                work_epilogue(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, thr, use_f, out, ctr, cap);
+                work_epilogue(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, lw, thr, use_f, out, ctr,
+                              cap);
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
@@ -377,7 +396,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 __global__ void __launch_bounds__(kThreads) k2_tail_threshold(const TailTile* __restrict__ tails, int pieces,
                                                               const Rect* __restrict__ rects,
                                                               const uint32_t* __restrict__ tail_buf,
-                                                              const int32_t* __restrict__ f, uint32_t thr,
+                                                              const int32_t* __restrict__ f,
+                                                              const uint8_t* __restrict__ lw, uint32_t thr,
                                                               uint32_t use_f, Cand* __restrict__ out,
                                                               unsigned long long* __restrict__ ctr, int64_t cap) {
     const TailTile t = tails[blockIdx.x];
@@ -405,14 +425,15 @@ __global__ void __launch_bounds__(kThreads) k2_tail_threshold(const TailTile* __
             acc[i][7] += b.w;
         }
     }
-    work_epilogue(rects[t.rect], t.ti, t.tj, tr, tc, lane, acc, nullptr, f, thr, use_f, out, ctr, cap);
+    work_epilogue(rects[t.rect], t.ti, t.tj, tr, tc, lane, acc, nullptr, f, lw, thr, use_f, out, ctr, cap);
 }
 
 // Accumulated rectangles: one CTA per owned tile row; candidate test on the summed counters.
 __global__ void __launch_bounds__(256) k2_acc_threshold(const AccUnit* __restrict__ units,
                                                         const Rect* __restrict__ rects,
                                                         const uint32_t* __restrict__ cnt,
-                                                        const int32_t* __restrict__ f, uint32_t thr, uint32_t use_f,
+                                                        const int32_t* __restrict__ f,
+                                                        const uint8_t* __restrict__ lw, uint32_t thr, uint32_t use_f,
                                                         Cand* __restrict__ out, unsigned long long* __restrict__ ctr,
                                                         int64_t cap) {
     const AccUnit u = units[blockIdx.x];
@@ -424,7 +445,8 @@ __global__ void __launch_bounds__(256) k2_acc_threshold(const AccUnit* __restric
         const int row = r0 + (int)(e / r.n_cols_real);
         const int col = (int)(e % r.n_cols_real);
         if (r.diag && col <= row) continue;
-        const uint32_t c = cnt[r.cnt_off + (int64_t)row * r.n_cols_real + col];
+        uint32_t c = cnt[r.cnt_off + (int64_t)row * r.n_cols_real + col];
+        if (r.promo) c >>= r.lgK - max((int)lw[r.row_first + row], (int)lw[r.col_first + col]);
         uint64_t t = c;
         if (use_f) t += (uint32_t)f[r.row_first + row] + (uint32_t)f[r.col_first + col];
         if (t >= thr) {
@@ -454,6 +476,32 @@ __global__ void k_virtualize(const uint32_t* __restrict__ src, int32_t src_npad,
         word = src[((int64_t)rep * W_a + k) * src_npad + j];
     }
     dst[idx] = word;
+}
+
+// Promoted group: dst[w * n_pad + c] = word (w mod W_k) of item c, taken from its own class k's
+// block (B'[w] = B[w mod W_k], W_k | W); padding columns are ⊥ words.
+constexpr int kMaxPromoMembers = 32;
+struct PromoSrc {
+    int32_t n_members, W, n, n_pad;
+    int64_t word_off[kMaxPromoMembers];
+    int32_t c0[kMaxPromoMembers + 1], W_k[kMaxPromoMembers], npad_k[kMaxPromoMembers];
+};
+
+__global__ void k_promote(const uint32_t* __restrict__ arena, const __grid_constant__ PromoSrc ps,
+                          uint32_t* __restrict__ dst) {
+    const int64_t total = (int64_t)ps.W * ps.n_pad;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int w = (int)(idx / ps.n_pad);
+        const int c = (int)(idx - (int64_t)w * ps.n_pad);
+        uint32_t word = kNullWord;
+        if (c < ps.n) {
+            int k = 0;
+            while (c >= ps.c0[k + 1]) ++k;
+            word = arena[ps.word_off[k] + (int64_t)(w % ps.W_k[k]) * ps.npad_k[k] + (c - ps.c0[k])];
+        }
+        dst[idx] = word;
+    }
 }
 
 // ------------------------------------------------------------------ simple kernel (one thread per pair)
@@ -620,6 +668,7 @@ static batmap_status run_simple(batmap_collection* h, const Selection& sel, uint
 
 struct K2Prepared {
     int part = -1, n_parts = -1;
+    bool promote = true;  // planned with class promotion (BATMAP_K2_PROMOTE)
     Plan pl;
     K2Maps* prm = nullptr;
     Rect* rects_d = nullptr;
@@ -627,6 +676,8 @@ struct K2Prepared {
     AccUnit* units_d = nullptr;
     TailTile* tails_d = nullptr;
     uint32_t* virt_d = nullptr;
+    uint32_t* promo_d = nullptr;  // promoted class blocks
+    uint8_t* lw_d = nullptr;      // per selection position: log2(W_i / W_min), if any promotion
 };
 
 void release_k2(K2Prepared* kp, cudaStream_t st) {
@@ -638,6 +689,10 @@ void release_k2(K2Prepared* kp, cudaStream_t st) {
     dfree(kp->units_d, st);
     dfree(kp->tails_d, st);
     dfree(kp->virt_d, st);
+    dfree(kp->promo_d, st);
+    dfree(kp->lw_d, st);
+    kp->promo_d = nullptr;
+    kp->lw_d = nullptr;
     kp->tails_d = nullptr;
     kp->rects_d = nullptr;
     kp->work_d = nullptr;
@@ -658,20 +713,38 @@ batmap_status prepare_k2(batmap_collection* h, const Selection& sel, int part, i
         set_error("cuTensorMapEncodeTiled unavailable");
         return BATMAP_E_CUDA;
     }
-    const int C = (int)sel.classes.size();
     kp->part = part;
     kp->n_parts = n_parts;
     const int grid_cap = kMinBlocks * h->num_sms;
+    const bool promote = !env_off("BATMAP_K2_PROMOTE");
+    kp->promote = promote;
     plan_work(sel.classes, part, n_parts, grid_cap, !env_off("BATMAP_K2_VIRTUAL"), !env_off("BATMAP_K2_SPLIT"),
-              &kp->pl);
-    if (C + (int)kp->pl.virt.size() > kMaxMaps) plan_work(sel.classes, part, n_parts, grid_cap, false, true, &kp->pl);
+              promote, &kp->pl);
+    if ((int)kp->pl.eff.size() + (int)kp->pl.virt.size() > kMaxMaps)
+        plan_work(sel.classes, part, n_parts, grid_cap, false, true, promote, &kp->pl);
     const Plan& pl = kp->pl;
+    const int C = (int)pl.eff.size();
     if (pl.work.empty()) return BATMAP_OK;
     if (pl.virt_words) BM_TRY(dalloc_t(&kp->virt_d, pl.virt_words, st));
+    if (pl.promo_words) {
+        for (const PromoCopy& pc : pl.promo)
+            if (pc.cls_hi - pc.cls_lo + 1 > kMaxPromoMembers) {
+                set_error("promoted group of %d classes", pc.cls_hi - pc.cls_lo + 1);
+                return BATMAP_E_INVALID;
+            }
+        BM_TRY(dalloc_t(&kp->promo_d, pl.promo_words, st));
+        std::vector<uint8_t> lw((size_t)sel.n_sel, 0);
+        for (const ClassInfo& c : sel.classes)
+            for (int64_t q = 0; q < c.n; ++q) lw[(size_t)(c.first + q)] = (uint8_t)lg_ratio(c.W, sel.classes[0].W);
+        BM_TRY(dalloc_t(&kp->lw_d, sel.n_sel, st));
+        BM_CUDA(cudaMemcpyAsync(kp->lw_d, lw.data(), lw.size(), cudaMemcpyHostToDevice, st));
+        BM_CUDA(cudaStreamSynchronize(st));  // lw is a host temporary
+    }
     kp->prm = new K2Maps();
-    for (int a = 0; a < C; ++a)
-        BM_TRY(encode_map(enc, &kp->prm->maps[a], sel.arena + sel.classes[a].word_off, sel.classes[a].n_pad,
-                          sel.classes[a].W));
+    for (int a = 0; a < C; ++a) {
+        const uint32_t* base = pl.eff_promo[a] >= 0 ? kp->promo_d : sel.arena;
+        BM_TRY(encode_map(enc, &kp->prm->maps[a], base + pl.eff[a].word_off, pl.eff[a].n_pad, pl.eff[a].W));
+    }
     for (size_t k = 0; k < pl.virt.size(); ++k)
         BM_TRY(encode_map(enc, &kp->prm->maps[C + k], kp->virt_d + pl.virt[k].dst_word_off, pl.virt[k].vpad,
                           pl.virt[k].W_a));
@@ -731,7 +804,8 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
     // kernels run, and reused; item subsets are planned here
     K2Prepared* kp = nullptr;
     K2Prepared local;
-    if (!sel.sel2pos && h->k2prep && h->k2prep->part == part && h->k2prep->n_parts == n_parts) {
+    if (!sel.sel2pos && h->k2prep && h->k2prep->part == part && h->k2prep->n_parts == n_parts &&
+        h->k2prep->promote == !env_off("BATMAP_K2_PROMOTE")) {
         kp = h->k2prep;
     } else {
         const batmap_status prc = prepare_k2(h, sel, part, n_parts, st, &local);
@@ -752,11 +826,34 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         if (kp == &local) release_k2(&local, st);
         return BATMAP_OK;
     }
-    // virtual copies of the wide classes of skinny rectangles (after the build kernels wrote the arena)
+    // promoted groups, then virtual copies of the wide classes of skinny rectangles (after the build
+    // kernels wrote the arena; a virtual copy may read a promoted block)
+    for (const PromoCopy& pc : pl.promo) {
+        PromoSrc ps{};
+        ps.n_members = pc.cls_hi - pc.cls_lo + 1;
+        ps.W = pc.W;
+        ps.n = pc.n;
+        ps.n_pad = pc.n_pad;
+        int32_t c0 = 0;
+        for (int k = 0; k < ps.n_members; ++k) {
+            const ClassInfo& A = sel.classes[pc.cls_lo + k];
+            ps.word_off[k] = A.word_off;
+            ps.c0[k] = c0;
+            ps.W_k[k] = A.W;
+            ps.npad_k[k] = A.n_pad;
+            c0 += A.n;
+        }
+        ps.c0[ps.n_members] = c0;
+        const int64_t cnt = (int64_t)pc.W * pc.n_pad;
+        const unsigned blocks = (unsigned)std::min<int64_t>((cnt + 255) / 256, 8 * h->num_sms);
+        k_promote<<<blocks, 256, 0, st>>>(sel.arena, ps, kp->promo_d + pc.dst_word_off);
+        h->launches += 1;
+    }
     for (const VirtCopy& v : pl.virt) {
-        const ClassInfo& B = sel.classes[v.cls_b];
+        const ClassInfo& B = pl.eff[v.cls_b];
+        const uint32_t* base = pl.eff_promo[v.cls_b] >= 0 ? kp->promo_d : sel.arena;
         const int64_t cnt = (int64_t)v.W_a * v.vpad;
-        k_virtualize<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(sel.arena + B.word_off, B.n_pad, B.n, v.W_a, v.R,
+        k_virtualize<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(base + B.word_off, B.n_pad, B.n, v.W_a, v.R,
                                                                     v.vpad, kp->virt_d + v.dst_word_off);
         h->launches += 1;
     }
@@ -780,19 +877,20 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         if (pl.cnt_entries) BM_CUDA(cudaMemsetAsync(h->cnt_d, 0, pl.cnt_entries * sizeof(uint32_t), st));
         rec(h, EV_K20, st);
         k2_tiled<<<grid, kThreads, kSmemBytes, st>>>(*prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d,
-                                                     h->tail_d, sel.f, threshold, use_f, h->cand_d, h->ctr_d,
-                                                     h->cand_cap);
+                                                     h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
+                                                     h->ctr_d, h->cand_cap);
         rec(h, EV_K21, st);
         h->launches += 1;
         if (!pl.tails.empty()) {
             k2_tail_threshold<<<(unsigned)pl.tails.size(), kThreads, 0, st>>>(
-                kp->tails_d, pl.tail_pieces, rects_d, h->tail_d, sel.f, threshold, use_f, h->cand_d, h->ctr_d,
-                h->cand_cap);
+                kp->tails_d, pl.tail_pieces, rects_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
+                h->ctr_d, h->cand_cap);
             h->launches += 1;
         }
         if (!pl.units.empty()) {
-            k2_acc_threshold<<<(unsigned)pl.units.size(), 256, 0, st>>>(units_d, rects_d, h->cnt_d, sel.f, threshold,
-                                                                        use_f, h->cand_d, h->ctr_d, h->cand_cap);
+            k2_acc_threshold<<<(unsigned)pl.units.size(), 256, 0, st>>>(units_d, rects_d, h->cnt_d, sel.f, kp->lw_d,
+                                                                        threshold, use_f, h->cand_d, h->ctr_d,
+                                                                        h->cand_cap);
             h->launches += 1;
         }
         cudaError_t le = cudaGetLastError();

@@ -1,6 +1,6 @@
 // plan.cu -- host-side planner of ★K2: width-class rectangles, 128 x 128 tiles with the
 // symmetry cut p <= q, virtualised skinny rectangles, split-K for long tiles, and
-// the deal of work to the parts of a multi-GPU run.
+// the deal of work to the parts of a multi-GPU run, and promotion of small narrow classes.
 #include <algorithm>
 
 #include "plan.h"
@@ -9,11 +9,146 @@ namespace bm {
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-void plan_work(const std::vector<ClassInfo>& cls, int part, int n_parts, int grid_cap, bool allow_virtual,
-               bool allow_split, Plan* out) {
+int lg_ratio(int64_t W, int64_t W_min) {
+    if (W_min <= 0 || W < W_min || W % W_min) return -1;
+    const int64_t q = W / W_min;
+    int l = 0;
+    while ((int64_t(1) << l) < q) ++l;
+    return (int64_t(1) << l) == q ? l : -1;
+}
+
+// Estimated executed compares of tiling classes (n[a], W[a]) the way plan_work does (skinny
+// rectangles virtualised when that saves > 30 %), plus the copy traffic of promoted groups
+// (a written word ~ 12 compare-equivalents: 4 B at ~1/3 of R_int's compare rate per byte).
+static int64_t est_cost(const std::vector<int64_t>& n, const std::vector<int64_t>& W,
+                        const std::vector<int64_t>& copy_words, bool allow_virtual) {
+    const int C = (int)n.size();
+    const int64_t T2 = (int64_t)kTile * kTile;
+    int64_t tot = 0;
+    for (int a = 0; a < C; ++a) {
+        tot += 12 * copy_words[a];
+        if (n[a] == 0) continue;
+        const int64_t ta = ceil_div(n[a], kTile);
+        for (int b = a; b < C; ++b) {
+            if (n[b] == 0) continue;
+            if (a == b) {
+                if (n[a] >= 2) tot += ta * (ta + 1) / 2 * T2 * W[a];
+                continue;
+            }
+            int64_t c = ta * ceil_div(n[b], kTile) * T2 * W[b];
+            const int64_t R = W[b] / W[a];
+            if (allow_virtual && R > 1) {
+                const int64_t v = ta * ceil_div(n[b] * R, kTile) * T2 * W[a];
+                if (v * 10 < c * 7) c = v;
+            }
+            tot += c;
+        }
+    }
+    return tot;
+}
+
+// Greedy promotion: repeatedly merge the adjacent pair of class groups whose merge lowers the
+// estimated cost most, while that gains > 1 %.  Groups are runs [lo, hi] of the width-sorted
+// classes; a group is planned at its widest member's width.
+static std::vector<std::pair<int, int>> choose_groups(const std::vector<ClassInfo>& cls, bool allow_virtual) {
+    const int C = (int)cls.size();
+    std::vector<std::pair<int, int>> g;
+    for (int a = 0; a < C; ++a) g.push_back({a, a});
+    if (C < 2) return g;
+    for (int a = 0; a < C; ++a)
+        if (lg_ratio(cls[a].W, cls[0].W) < 0) return g;  // widths must be W_0 times powers of two
+    auto cost = [&](const std::vector<std::pair<int, int>>& gs) {
+        std::vector<int64_t> n, W, cw;
+        for (const auto& p : gs) {
+            int64_t s = 0;
+            for (int a = p.first; a <= p.second; ++a) s += cls[a].n;
+            n.push_back(s);
+            W.push_back(cls[p.second].W);
+            cw.push_back(p.first == p.second ? 0 : ceil_div(s, kPadItems) * kPadItems * cls[p.second].W);
+        }
+        return est_cost(n, W, cw, allow_virtual);
+    };
+    constexpr int64_t kMaxPromoWords = int64_t(1) << 27;  // 512 MB per promoted block
+    int64_t best = cost(g);
+    for (;;) {
+        int pick = -1;
+        int64_t pick_cost = 0;
+        for (size_t k = 0; k + 1 < g.size(); ++k) {
+            int64_t s = 0;
+            for (int a = g[k].first; a <= g[k + 1].second; ++a) s += cls[a].n;
+            if (ceil_div(s, kPadItems) * kPadItems * cls[g[k + 1].second].W > kMaxPromoWords) continue;
+            std::vector<std::pair<int, int>> t = g;
+            t[k].second = t[k + 1].second;
+            t.erase(t.begin() + (long)k + 1);
+            const int64_t c = cost(t);
+            if (pick < 0 || c < pick_cost) {
+                pick = (int)k;
+                pick_cost = c;
+            }
+        }
+        if (pick < 0 || pick_cost * 100 >= best * 99) break;
+        g[pick].second = g[pick + 1].second;
+        g.erase(g.begin() + pick + 1);
+        best = pick_cost;
+    }
+    return g;
+}
+
+void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int grid_cap, bool allow_virtual,
+               bool allow_split, bool allow_promote, Plan* out) {
     Plan& P = *out;
     P = Plan();
+    // ---- planned classes: original classes, or promoted groups of adjacent ones
+    const std::vector<std::pair<int, int>> groups =
+        allow_promote ? choose_groups(orig, allow_virtual) : [&] {
+            std::vector<std::pair<int, int>> g;
+            for (int a = 0; a < (int)orig.size(); ++a) g.push_back({a, a});
+            return g;
+        }();
+    P.eff_of.assign(orig.size(), -1);
+    for (const auto& gr : groups) {
+        const int e = (int)P.eff.size();
+        for (int a = gr.first; a <= gr.second; ++a) P.eff_of[a] = e;
+        if (gr.first == gr.second) {
+            P.eff.push_back(orig[gr.first]);
+            P.eff_promo.push_back(-1);
+            continue;
+        }
+        ClassInfo c = orig[gr.second];
+        c.first = orig[gr.first].first;
+        int64_t n = 0;
+        for (int a = gr.first; a <= gr.second; ++a) n += orig[a].n;
+        c.n = (int32_t)n;
+        c.n_pad = (int32_t)(ceil_div(n, kPadItems) * kPadItems);
+        c.word_off = P.promo_words;
+        PromoCopy pc{};
+        pc.cls_lo = gr.first;
+        pc.cls_hi = gr.second;
+        pc.W = c.W;
+        pc.n = c.n;
+        pc.n_pad = c.n_pad;
+        pc.dst_word_off = P.promo_words;
+        P.promo_words += (int64_t)c.n_pad * c.W;
+        P.eff_promo.push_back((int32_t)P.promo.size());
+        P.promo.push_back(pc);
+        P.eff.push_back(c);
+    }
+    const std::vector<ClassInfo>& cls = P.eff;
     const int C = (int)cls.size();
+    const int64_t W_min = orig.empty() ? 1 : orig[0].W;
+    // sum of the original widths of planned-class items [q0, q1) (local indices)
+    auto sumW = [&](int c, int64_t q0, int64_t q1) -> int64_t {
+        if (q1 <= q0) return 0;
+        if (P.eff_promo[c] < 0) return (q1 - q0) * cls[c].W;
+        const PromoCopy& pc = P.promo[P.eff_promo[c]];
+        int64_t s = 0, base = 0;
+        for (int a = pc.cls_lo; a <= pc.cls_hi; ++a) {
+            const int64_t lo = std::max(q0, base), hi = std::min(q1, base + orig[a].n);
+            if (hi > lo) s += (hi - lo) * orig[a].W;
+            base += orig[a].n;
+        }
+        return s;
+    };
     // ---- rectangles
     for (int a = 0; a < C; ++a)
         for (int b = a; b < C; ++b) {
@@ -36,6 +171,8 @@ void plan_work(const std::vector<ClassInfo>& cls, int part, int n_parts, int gri
             r.col_first = (int32_t)B.first;
             r.diag = (a == b);
             r.n_cols_real = B.n;
+            r.promo = P.eff_promo[b] >= 0;
+            r.lgK = lg_ratio(B.W, W_min);
             if (virt) {
                 VirtCopy vc{};
                 vc.cls_b = b;
@@ -78,7 +215,8 @@ void plan_work(const std::vector<ClassInfo>& cls, int part, int n_parts, int gri
             P.cnt_entries += (int64_t)r.n_rows * r.n_cols_real;
         }
     if (P.cnt_entries > (int64_t(1) << 29) && (allow_virtual || allow_split)) {  // > 2 GB of counters
-        plan_work(cls, part, n_parts, grid_cap, false, false, out);
+        const std::vector<ClassInfo> o = orig;
+        plan_work(o, part, n_parts, grid_cap, false, false, false, out);
         return;
     }
     // ---- units dealt to the parts: a tile row of an accumulated rectangle (all contributions
@@ -114,20 +252,30 @@ void plan_work(const std::vector<ClassInfo>& cls, int part, int n_parts, int gri
         const int64_t rows = std::min<int64_t>(kTile, r.n_rows - (int64_t)u.ti * kTile);
         const int W_real = r.W * r.R;
         if (r.acc) P.units.push_back({u.rect, u.ti});
-        // algorithmic compares of the pairs this unit owns
+        // algorithmic compares of the pairs this unit owns: sum of max(W_i, W_j) = W_j (columns are
+        // never narrower than rows: width-sorted positions)
+        const int64_t r0 = (int64_t)u.ti * kTile;
         if (r.acc && r.diag) {
-            const int64_t r0 = (int64_t)u.ti * kTile;
-            for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += (int64_t)(r.n_rows - 1 - q) * W_real;
+            if (P.eff_promo[r.cls_b] < 0)
+                for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += (int64_t)(r.n_rows - 1 - q) * W_real;
+            else
+                for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += sumW(r.cls_b, q + 1, r.n_rows);
         } else if (r.acc) {
-            P.word_compares += rows * r.n_cols_real * (int64_t)W_real;
+            P.word_compares += rows * sumW(r.cls_b, 0, r.n_cols_real);
         }
         const int jb = u.tj >= 0 ? u.tj : (r.diag ? u.ti : 0);
         const int je = u.tj >= 0 ? u.tj + 1 : tb;
         for (int j = jb; j < je; ++j) {
             if (!r.acc) {
-                const int64_t cols = std::min<int64_t>(kTile, r.n_cols - (int64_t)j * kTile);
-                const int64_t pairs = (r.diag && j == u.ti) ? rows * (rows - 1) / 2 : rows * cols;
-                P.word_compares += pairs * (int64_t)W_real;
+                const int64_t c0 = (int64_t)j * kTile, c1 = std::min<int64_t>(r.n_cols, c0 + kTile);
+                if (r.diag && j == u.ti) {
+                    if (P.eff_promo[r.cls_b] < 0)
+                        P.word_compares += rows * (rows - 1) / 2 * (int64_t)W_real;
+                    else
+                        for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += sumW(r.cls_b, q + 1, c1);
+                } else {
+                    P.word_compares += rows * sumW(r.cls_b, c0, c1);
+                }
             }
             const int nk = r.W / kChunk;
             int pieces = 1;

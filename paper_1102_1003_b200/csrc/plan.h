@@ -26,6 +26,8 @@ struct Rect {
     int32_t diag, R;              // diag: a == b (pairs i < j only)
     int32_t acc, n_cols_real;     // acc: partial counts accumulate into cnt[] (virtual or split-K)
     int64_t cnt_off;              // offset of this rectangle's n_rows x n_cols_real counters
+    int32_t promo;                // rows or columns include promoted (replicated) items
+    int32_t lgK;                  // log2 of the rectangle's real width in units of the smallest W
 };
 
 struct Work {   // one work item: tile (ti, tj) of a rectangle over k-chunks [k0, k1)
@@ -46,7 +48,26 @@ struct VirtCopy {  // materialise class b's BatMaps as R virtual columns of peri
     int64_t dst_word_off;  // into the virtual-copy scratch arena
 };
 
+// Promotion: a run of adjacent (narrow, small) width classes [cls_lo, cls_hi] is planned as ONE
+// class of the widest member's width W.  Each narrower BatMap is replicated along k,
+// B'[w] = B[w mod W_i] (W_i | W), into a word-major scratch block, so the members share tiles
+// instead of each padding its own.  A pair then compares K = the rectangle's real width words,
+// K / max(W_i, W_j) times the wrap-around count of P:273-274 (all widths are 3 r / 4 with r a
+// power of two), and the epilogue divides exactly: c = c' >> (lgK - max(lw_i, lw_j)).
+struct PromoCopy {
+    int32_t cls_lo, cls_hi;  // original classes merged (ascending width)
+    int32_t W, n, n_pad;     // promoted class: width, items, padded items
+    int32_t pad;
+    int64_t dst_word_off;    // into the promotion scratch arena
+};
+
 struct Plan {
+    std::vector<ClassInfo> eff;   // the planned classes (original, or promoted groups)
+    std::vector<int32_t> eff_of;  // original class -> planned class
+    std::vector<PromoCopy> promo; // planned class -> copy, for promoted groups (eff[k].word_off is
+                                  // then an offset into the promotion arena)
+    std::vector<int32_t> eff_promo;  // planned class -> index into promo, or -1
+    int64_t promo_words = 0;
     std::vector<Rect> rects;
     std::vector<Work> work;       // this part's work items, longest first
     std::vector<AccUnit> units;   // this part's tile rows of accumulated rectangles
@@ -60,7 +81,11 @@ struct Plan {
 };
 
 // grid_cap: CTAs the kernel keeps resident (the split-K target is ~4 work items per CTA).
+// Rectangles, work items and units refer to the planned classes out->eff.
 void plan_work(const std::vector<ClassInfo>& cls, int part, int n_parts, int grid_cap, bool allow_virtual,
-               bool allow_split, Plan* out);
+               bool allow_split, bool allow_promote, Plan* out);
+
+// log2 of W / W_min for a width that is W_min times a power of two (else -1)
+int lg_ratio(int64_t W, int64_t W_min);
 
 }  // namespace bm

@@ -75,16 +75,29 @@ def _collect(class_n, class_w, n_parts, grid_cap=0):
     return parts
 
 
+def _planned(class_n, class_w):
+    """Planned classes (promotion merges runs of adjacent classes): (n, W, group_of)."""
+    from paper_1102_1003_b200 import plan_groups
+
+    g = plan_groups(class_n, class_w).tolist()
+    assert g == sorted(g) and g[0] == 0 and all(b - a in (0, 1) for a, b in zip(g, g[1:]))
+    pn = [sum(n for n, gg in zip(class_n, g) if gg == e) for e in range(g[-1] + 1)]
+    pw = [max(w for w, gg in zip(class_w, g) if gg == e) for e in range(g[-1] + 1)]
+    return pn, pw, g
+
+
 @pytest.mark.parametrize("class_n,class_w", [([1000], [96]), ([780, 220], [192, 384]),
                                              ([2000, 40, 30, 20, 10, 5, 3, 1], [96 * 2 ** k for k in range(8)]),
                                              ([300, 200, 120, 90, 50, 12], [96 * 2 ** k for k in range(6)]),
+                                             ([1, 7, 100, 454, 427, 11], [768 * 2 ** k for k in range(6)]),
                                              ([5], [96])])
 @pytest.mark.parametrize("n_parts", [1, 2, 3, 8])
 def test_plan_work_partition_exact(class_n, class_w, n_parts):
-    """Union over parts = every k-chunk of every tile of the pair triangle exactly once (P:464-467);
-    tile rows of accumulated rectangles stay on one part; algorithmic work adds up to
-    sum_{i<j} max(W_i, W_j)."""
+    """Union over parts = every k-chunk of every tile of the (planned-class) pair triangle exactly
+    once; tile rows of accumulated rectangles stay on one part; algorithmic work adds
+    up to sum_{i<j} max(W_i, W_j) over the ORIGINAL widths."""
     parts = _collect(class_n, class_w, n_parts)
+    pn, pw, _ = _planned(class_n, class_w)
     chunks = {}
     rect_R = {}
     row_part = {}
@@ -101,24 +114,42 @@ def test_plan_work_partition_exact(class_n, class_w, n_parts):
             if acc:
                 assert row_part.setdefault((a, b, ti), p) == p
     expect = set()
-    C = len(class_n)
+    C = len(pn)
     for a in range(C):
         for b in range(a, C):
-            if class_n[a] == 0 or class_n[b] == 0 or (a == b and class_n[a] < 2):
+            if pn[a] == 0 or pn[b] == 0 or (a == b and pn[a] < 2):
                 continue
             R, _ = rect_R[(a, b)]
-            W = class_w[b] // R
-            ta = -(-class_n[a] // 128)
-            tb = -(-(class_n[b] * R) // 128)
+            W = pw[b] // R
+            ta = -(-pn[a] // 128)
+            tb = -(-(pn[b] * R) // 128)
             for i in range(ta):
                 for j in range(i if a == b else 0, tb):
                     for k in range(W // 16):
                         expect.add((a, b, i, j, k))
     assert set(chunks) == expect
     wc_total = sum(wc for _, wc, _ in parts)
+    C = len(class_n)
     closed = sum(class_n[a] * class_n[b] * class_w[b] for a in range(C) for b in range(a + 1, C))
     closed += sum(n * (n - 1) // 2 * w for n, w in zip(class_n, class_w))
     assert wc_total == closed
+
+
+def test_plan_groups_promotion(monkeypatch):
+    """Small narrow classes are merged into a planned class of their widest member's width (the
+    T40I10D100K-shaped C3 classes: 1, 7 and 100 items of 768 ... 3072 words); large classes stay
+    apart; BATMAP_K2_PROMOTE=0 disables it; executed work drops."""
+    from paper_1102_1003_b200 import plan_groups
+
+    cn, cw = [1, 7, 100, 454, 427, 11], [768 * 2 ** k for k in range(6)]
+    g = plan_groups(cn, cw).tolist()
+    assert g[0] == g[1] == g[2] and len(set(g)) >= 3
+    assert plan_groups([7822, 2178], [1536, 3072]).tolist() == [0, 1]  # C2: nothing to gain
+    _, wc1, tc1 = _collect(cn, cw, 1)[0]
+    monkeypatch.setenv("BATMAP_K2_PROMOTE", "0")
+    assert plan_groups(cn, cw).tolist() == list(range(6))
+    _, wc0, tc0 = _collect(cn, cw, 1)[0]
+    assert wc0 == wc1 and tc1 < 0.85 * tc0
 
 
 def test_plan_work_virtual_and_split():
@@ -132,33 +163,42 @@ def test_plan_work_virtual_and_split():
 
 
 def test_plan_work_covers_every_pair_once():
-    """Expanding the work items (virtual columns, k-chunks) covers every word compare of every pair
-    i < j exactly once: c_ij = sum_{w < W_j} SWAR(B_j[w], B_i[w mod W_i])."""
-    class_n, class_w = [130, 7, 3], [16, 64, 256]
-    first = np.cumsum([0] + class_n)
-    items = _collect(class_n, class_w, 1)[0][0]
-    cover = {}
-    for a, b, ti, tj, k0, k1, R, acc in items.tolist():
-        Wv = class_w[b] // R
-        for r in range(ti * 128, min(class_n[a], ti * 128 + 128)):
-            for v in range(tj * 128, min(class_n[b] * R, tj * 128 + 128)):
-                j, rep = divmod(v, R)
-                if a == b and r >= j:
-                    continue
-                key = (first[a] + r, first[b] + j)
-                for k in range(k0 * 16, k1 * 16):
-                    w = rep * Wv + k  # word of B_j
-                    cover[(key, w)] = cover.get((key, w), 0) + 1
-    n = sum(class_n)
-    pairs = {(i, j) for i in range(n) for j in range(i + 1, n)}
-    assert {k for k, _ in cover} == pairs
-    assert set(cover.values()) == {1}
-    width = {}
-    for a in range(3):
-        for r in range(class_n[a]):
-            width[first[a] + r] = class_w[a]
-    per_pair = {}
-    for (key, w) in cover:
-        per_pair[key] = per_pair.get(key, 0) + 1
-    for (i, j), cnt in per_pair.items():
-        assert cnt == max(width[i], width[j])
+    """Expanding the work items (virtual columns, k-chunks, promoted classes) covers, for every pair
+    i < j, each of the K words of its planned column item exactly once, with K a power-of-two
+    multiple of max(W_i, W_j): c_ij = sum_{w < W_j} SWAR(B_j[w], B_i[w mod W_i]),
+    counted K / max(W_i, W_j) times and divided exactly."""
+    for class_n, class_w in (([130, 7, 3], [16, 64, 256]), ([3, 5, 140, 2], [16, 32, 64, 128])):
+        pn, pw, g = _planned(class_n, class_w)
+        first = np.cumsum([0] + pn)
+        items = _collect(class_n, class_w, 1)[0][0]
+        cover = {}
+        for a, b, ti, tj, k0, k1, R, acc in items.tolist():
+            Wv = pw[b] // R
+            for r in range(ti * 128, min(pn[a], ti * 128 + 128)):
+                for v in range(tj * 128, min(pn[b] * R, tj * 128 + 128)):
+                    j, rep = divmod(v, R)
+                    if a == b and r >= j:
+                        continue
+                    key = (first[a] + r, first[b] + j)
+                    for k in range(k0 * 16, k1 * 16):
+                        w = rep * Wv + k  # word of (planned) B_j
+                        cover[(key, w)] = cover.get((key, w), 0) + 1
+        n = sum(class_n)
+        pairs = {(i, j) for i in range(n) for j in range(i + 1, n)}
+        assert {k for k, _ in cover} == pairs
+        assert set(cover.values()) == {1}
+        width, pwidth = {}, {}
+        pos = 0
+        for a in range(len(class_n)):
+            for r in range(class_n[a]):
+                width[pos] = class_w[a]
+                pwidth[pos] = pw[g[a]]
+                pos += 1
+        per_pair = {}
+        for (key, w) in cover:
+            per_pair[key] = per_pair.get(key, 0) + 1
+        for (i, j), cnt in per_pair.items():
+            K = pwidth[j]
+            assert cnt == K and K % max(width[i], width[j]) == 0
+            q = K // max(width[i], width[j])
+            assert q & (q - 1) == 0

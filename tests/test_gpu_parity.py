@@ -285,6 +285,51 @@ def test_colliding_pi_forces_failures_exact():
     assert c.info()["n_failures"] > 0
 
 
+def _quest_widths(seed, m=100_000):
+    """Width classes shaped like C3's (1, 7, ~40, ~300, ~50, 3 items of r = 2^10 .. 2^15 at
+    m = 10^5): small narrow classes that the planner promotes, with shared elements."""
+    rng = np.random.default_rng(seed)
+    plan = [(1, 300), (7, 700), (40, 1500), (300, 3000), (50, 6000), (3, 12000)]
+    pool = np.sort(rng.choice(m, size=20000, replace=False))
+    rows = []
+    for cnt, size in plan:
+        for _ in range(cnt):
+            k = int(size * rng.uniform(0.6, 1.0))
+            own = rng.choice(m, size=k - k // 4, replace=False)
+            shared = rng.choice(pool, size=k // 4, replace=False)
+            rows.append(np.unique(np.concatenate([own, shared])).astype(np.int32))
+    order = rng.permutation(len(rows))  # ids not in width order
+    rows = [rows[k] for k in order]
+    off = np.zeros(len(rows) + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    return off, np.concatenate(rows), m
+
+
+@pytest.mark.parametrize("max_loop", [0, 1])
+def test_promoted_classes_exact(max_loop, monkeypatch):
+    """Class promotion (small narrow width classes planned as one class of the widest member's
+    width, counts divided by K / max(W_i, W_j)): bit-exact against the oracle at thresholds 0, 1
+    and 40, on the full selection and on a subset, with and without forced failures; raw counts
+    and executed work compared with promotion disabled."""
+    off, tids, m = _quest_widths(5)
+    c = _coll(off, tids, m, seed=3, max_loop=max_loop)
+    if max_loop:
+        assert c.info()["n_failures"] > 0
+    for thr in (0, 1, 40):
+        np.testing.assert_array_equal(_np(c.pair_supports(threshold=thr)), oracle.pairs_merge(off, tids, threshold=thr))
+    tc_on = c.stats()["tile_compares"]
+    raw_on = _np(c.pair_supports(threshold=0, raw=True))
+    sub = np.sort(np.random.default_rng(2).choice(len(off) - 1, size=150, replace=False)).astype(np.int32)
+    sub_on = _np(c.pair_supports(items=torch.as_tensor(sub).cuda(), threshold=1))
+    np.testing.assert_array_equal(sub_on, oracle.pairs_merge(off, tids, items=sub, threshold=1))
+    monkeypatch.setenv("BATMAP_K2_PROMOTE", "0")
+    raw_off = _np(c.pair_supports(threshold=0, raw=True))
+    tc_off = c.stats()["tile_compares"]
+    np.testing.assert_array_equal(raw_on, raw_off)
+    assert tc_on < 0.9 * tc_off, (tc_on, tc_off)
+    c.close()
+
+
 def test_items_subset_and_parts():
     w = make_config("C1")
     rng = np.random.default_rng(3)
