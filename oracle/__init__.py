@@ -12,6 +12,8 @@ Contents
                  horizontal pair counting; C + OpenMP for speed.
   batmap_ref.py  step-by-step BatMap method in the paper's notation, for
                  byte-level parity of the build and raw-count parity of the intersection.
+  fimi.py        NEXT-3: FIMI-repository text -> vertical tidlists (P:56-58, P:556-558,
+                 SPEC S:504-512) and the frequent-item pre-filter.
 
 Parity pins (tests/test_oracle_*.py) tie both to things other than themselves: brute
 force on tiny inputs, the Gram matrix X^T X (numpy int64 matmul), the invariant

@@ -8,6 +8,7 @@ imported here.
 """
 from .gen import (  # noqa: F401
     CONFIGS,
+    fimi_text,
     Workload,
     make_config,
     quest,

@@ -22,7 +22,7 @@ import math
 
 import numpy as np
 
-__all__ = ["Workload", "uniform", "zipf", "quest", "to_horizontal", "make_config", "CONFIGS"]
+__all__ = ["Workload", "uniform", "zipf", "quest", "to_horizontal", "make_config", "CONFIGS", "fimi_text"]
 
 
 @dataclasses.dataclass
@@ -232,3 +232,33 @@ def make_config(name: str, scale_items: float = 1.0, seed: int | None = None) ->
         raise ValueError(cfg["kind"])
     return Workload(name=name, offsets=off, tids=tids, m=m, threshold=cfg["threshold"],
                     meta=dict(cfg, n=n))
+
+
+def fimi_text(offsets: np.ndarray, tids: np.ndarray, m: int, *, labels: np.ndarray | None = None, seed: int = 0,
+              messy: bool = False, final_newline: bool = True) -> bytes:
+    """Write a vertical CSR as FIMI-repository text (one transaction per line, item labels
+    separated by whitespace).  ``labels[i]`` is item i's label (default: i).
+    ``messy`` varies the formatting the way real files do (tabs, runs of spaces, CRLF line
+    ends, leading/trailing blanks, items repeated within a line, unsorted lines); every
+    transaction -- empty ones too -- is one line."""
+    toff, items = to_horizontal(offsets, tids, m)
+    lab = np.arange(offsets.shape[0] - 1, dtype=np.int64) if labels is None else np.asarray(labels, np.int64)
+    rng = np.random.default_rng(seed)
+    if not messy:
+        lines = [" ".join(map(str, lab[items[toff[t]:toff[t + 1]]].tolist())) for t in range(m)]
+        body = "\n".join(lines)
+        return (body + ("\n" if final_newline and m else "")).encode()
+    seps = [" ", "  ", "\t", " \t ", "   "]
+    out = []
+    for t in range(m):
+        row = lab[items[toff[t]:toff[t + 1]]].tolist()
+        if row and rng.random() < 0.3:
+            row = row + [row[int(rng.integers(len(row)))]]  # a repeated item
+        rng.shuffle(row)
+        s = (" " if rng.random() < 0.2 else "")
+        s += "".join(str(v) + seps[int(rng.integers(len(seps)))] if k + 1 < len(row) else str(v)
+                     for k, v in enumerate(row))
+        s += (" " if rng.random() < 0.2 else "") + ("\r" if rng.random() < 0.3 else "")
+        out.append(s)
+    body = "\n".join(out)
+    return (body + ("\n" if final_newline and m else "")).encode()
