@@ -318,6 +318,69 @@ batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const 
                                int64_t capacity, int64_t* n_items, int64_t* word_compares,
                                int64_t* tile_compares);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT-3: FIMI-repository text -> vertical tidlists, and the frequent-item filter.
+ *
+ * The paper's real-data experiment reads a file "taken from the Frequent Itemset Mining Dataset
+ * Repository" -- one transaction per line, whitespace-separated item labels -- and
+ * the method starts from the vertical layout.  It also assumes the data "preprocessed
+ * ... to remove items with support below the threshold".  Semantics (
+ * readings #21-#25 in DESIGN.md):
+ *   - transaction id = 0-based line index; the text after the last '
+' is a transaction iff it
+ *     is non-empty; blank lines are empty transactions;
+ *   - a label is a run of decimal digits, 0 <= label <= 2^32 - 1; separators are ' ', '	', '';
+ *     any other byte, or a longer number, is an error;
+ *   - duplicate labels within a line collapse (set semantics);
+ *   - items are re-densified: dense id k is the k-th smallest label present; labels[k] maps back.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct batmap_fimi* batmap_fimi_handle; /* library-owned; free with batmap_fimi_destroy */
+
+/*
+ * batmap_fimi_parse -- parse FIMI text into a library-owned vertical database.
+ *   text      [device] n_bytes bytes (any alignment; 16-byte aligned is read with 128-bit loads).
+ *             Read-only; may be freed once the call returns.
+ *   out       [host] receives the handle (NULL on error).
+ *   bad_line  [host] 1-based line of the first offending byte / oversized label on E_INVALID,
+ *             else -1.
+ * Synchronises `stream` (three times: token count, errors, item count).
+ * Errors: E_INVALID (null pointer, n_bytes < 0, malformed text), E_OVERFLOW (>= 2^31
+ * transactions), E_NOMEM, E_CUDA.
+ */
+batmap_status batmap_fimi_parse(const uint8_t* text, int64_t n_bytes, batmap_stream_t stream,
+                                batmap_fimi_handle* out, int64_t* bad_line);
+
+/* Sizes of the parsed (and possibly filtered) database: items, (item, tid) pairs, transactions. */
+batmap_status batmap_fimi_info(batmap_fimi_handle h, int64_t* n_items, int64_t* nnz,
+                               int64_t* n_transactions);
+
+/*
+ * batmap_fimi_filter -- keep only the items with support |S_i| >= min_support, in
+ * ascending dense-id (= label) order; labels follow; n_transactions unchanged.  min_support 0
+ * keeps everything.  Synchronises `stream`.
+ */
+batmap_status batmap_fimi_filter(batmap_fimi_handle h, uint32_t min_support, batmap_stream_t stream);
+
+/*
+ * batmap_fimi_export -- copy the database into caller-owned device buffers (any may be NULL):
+ *   offsets [device] n_items + 1 int64; tids [device] nnz int32 (each list strictly increasing);
+ *   labels [device] n_items uint32.  The CSR is exactly what batmap_build takes.  Asynchronous.
+ */
+batmap_status batmap_fimi_export(batmap_fimi_handle h, int64_t* offsets, int32_t* tids, uint32_t* labels,
+                                 batmap_stream_t stream);
+
+void batmap_fimi_destroy(batmap_fimi_handle h);
+
+/*
+ * batmap_frequent_items -- the frequent-item pre-filter on any vertical CSR: the ids
+ * i with offsets[i+1] - offsets[i] >= min_support, ascending, written to items_out (a selection
+ * for batmap_pair_supports: a pair with support >= s has both items frequent).
+ *   offsets    [device] n_items + 1;  items_out [device] capacity n_items;  n_out [host].
+ * Synchronises `stream`.  Errors: E_INVALID (null pointers, n_items < 0), E_OVERFLOW (n_items >= 2^31).
+ */
+batmap_status batmap_frequent_items(const int64_t* offsets, int64_t n_items, uint32_t min_support,
+                                    int32_t* items_out, int64_t* n_out, batmap_stream_t stream);
+
 /*
  * batmap_plan_groups -- host-only view of the planner's class promotion (no device needed).  The
  * planner may merge a run of adjacent width classes (typically small, narrow ones whose own

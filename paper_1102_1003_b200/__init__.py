@@ -8,7 +8,11 @@ from .batmap import (  # noqa: F401
     Collection,
     dense_pair_supports,
     load_library,
+    FimiDB,
+    frequent_items,
     merge_pair_supports,
+    mine_fimi,
+    parse_fimi,
     mine_host,
     plan_groups,
     plan_work,

@@ -87,6 +87,12 @@ def load_library():
         "batmap_swar_device": ([P, P, I64, P, P], ctypes.c_int),
         "batmap_plan_work": ([I32, P, P, I32, I32, I32, P, I64, PI64, PI64, PI64], ctypes.c_int),
         "batmap_plan_groups": ([I32, P, P, P], ctypes.c_int),
+        "batmap_fimi_parse": ([P, I64, P, ctypes.POINTER(P), PI64], ctypes.c_int),
+        "batmap_fimi_info": ([P, PI64, PI64, PI64], ctypes.c_int),
+        "batmap_fimi_filter": ([P, U32, P], ctypes.c_int),
+        "batmap_fimi_export": ([P, P, P, P, P], ctypes.c_int),
+        "batmap_fimi_destroy": ([P], None),
+        "batmap_frequent_items": ([P, I64, U32, P, PI64, P], ctypes.c_int),
         "batmap_stats": ([P, ctypes.POINTER(Stats)], ctypes.c_int),
         "batmap_sort_triples": ([P, I64, P], ctypes.c_int),
         "batmap_dense_pair_supports": ([P, P, I64, I64, P, I64, U32, P, I64, PI64, ctypes.POINTER(ctypes.c_double), P],
@@ -363,6 +369,81 @@ def swar_device(x, y, stream=None):
     out = torch.empty(2 * max(n, 1), dtype=torch.int32, device="cuda")
     _check(load_library().batmap_swar_device(_dptr(x), _dptr(y), n, _dptr(out), _stream_ptr(stream)))
     return out[:n], out[n:2 * n]
+
+
+class FimiDB:
+    """A FIMI-repository file parsed on the device (batmap_fimi_parse, optionally filtered by
+    batmap_fimi_filter): the vertical CSR ``offsets`` (int64) / ``tids`` (int32) that
+    ``Collection`` takes, ``labels`` (int64: dense id -> the file's item label) and ``m``."""
+
+    def __init__(self, offsets, tids, labels, m: int):
+        self.offsets, self.tids, self.labels, self.m = offsets, tids, labels, m
+
+    @property
+    def n_items(self) -> int:
+        return self.offsets.numel() - 1
+
+
+def parse_fimi(text, min_support: int = 0, *, stream=None) -> FimiDB:
+    """FIMI text (bytes, or a uint8 CUDA tensor) -> FimiDB on the device; items with support
+    below ``min_support`` dropped.  Raises BatMapError (status E_INVALID, message with
+    the line number) on malformed text."""
+    import torch
+
+    lib = load_library()
+    if isinstance(text, (bytes, bytearray, memoryview)):
+        buf = torch.frombuffer(bytearray(text), dtype=torch.uint8) if len(text) else torch.empty(0, dtype=torch.uint8)
+        t = buf.pin_memory().to("cuda", non_blocking=True) if len(text) else buf.cuda()
+    else:
+        t = text.to(device="cuda", dtype=torch.uint8).contiguous()
+    h = ctypes.c_void_p()
+    bad = ctypes.c_int64(-1)
+    _check(lib.batmap_fimi_parse(_dptr(t), t.numel(), _stream_ptr(stream), ctypes.byref(h), ctypes.byref(bad)))
+    try:
+        if min_support:
+            _check(lib.batmap_fimi_filter(h, int(min_support), _stream_ptr(stream)))
+        n, nnz, m = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.batmap_fimi_info(h, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(m)))
+        off = torch.empty(n.value + 1, dtype=torch.int64, device="cuda")
+        tids = torch.empty(max(nnz.value, 1), dtype=torch.int32, device="cuda")
+        lab = torch.empty(max(n.value, 1), dtype=torch.int32, device="cuda")
+        _check(lib.batmap_fimi_export(h, _dptr(off), _dptr(tids), _dptr(lab), _stream_ptr(stream)))
+        (torch.cuda.current_stream() if stream is None else stream).synchronize()
+    finally:
+        lib.batmap_fimi_destroy(h)
+    labels = lab[: n.value].to(torch.int64) & 0xFFFFFFFF
+    return FimiDB(off, tids[: nnz.value], labels, int(m.value))
+
+
+def frequent_items(offsets, min_support: int, *, stream=None):
+    """batmap_frequent_items: int32 CUDA tensor of the ids with |S_i| >= min_support."""
+    import torch
+
+    lib = load_library()
+    offsets = offsets.to(device="cuda", dtype=torch.int64).contiguous()
+    n = offsets.numel() - 1
+    out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    k = ctypes.c_int64(0)
+    _check(lib.batmap_frequent_items(_dptr(offsets), n, int(min_support), _dptr(out), ctypes.byref(k),
+                                     _stream_ptr(stream)))
+    return out[: k.value]
+
+
+def mine_fimi(text, threshold: int, **build_kw) -> np.ndarray:
+    """End to end from a FIMI file: parse + frequent-item filter on the device, build the BatMaps
+    of the frequent items, emit every pair with support >= threshold.  Returns int64 [K, 3] of
+    (label_i, label_j, support), label_i < label_j, sorted."""
+    db = parse_fimi(text, min_support=threshold)
+    if db.n_items < 2:
+        return np.zeros((0, 3), np.int64)
+    with Collection(db.offsets, db.tids, max(db.m, 1), **build_kw) as c:
+        t = c.pair_supports(threshold=threshold)
+    if not t.numel():
+        return np.zeros((0, 3), np.int64)
+    import torch
+
+    t = t.to(torch.int64)
+    return torch.stack([db.labels[t[:, 0]], db.labels[t[:, 1]], t[:, 2]], dim=1).cpu().numpy()
 
 
 def plan_groups(class_n, class_w):

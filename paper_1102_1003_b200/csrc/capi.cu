@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fimi.h"
 #include "plan.h"
 
 using namespace bm;
@@ -473,6 +474,89 @@ batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n
         return BATMAP_E_INVALID;
     }
     return swar_device(x, y, n, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ------------------------------------------------------------------ NEXT-3: FIMI ingestion
+batmap_status batmap_fimi_parse(const uint8_t* text, int64_t n_bytes, batmap_stream_t stream, batmap_fimi_handle* out,
+                                int64_t* bad_line) {
+    if (!out || !bad_line || n_bytes < 0 || (!text && n_bytes > 0)) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    *out = nullptr;
+    *bad_line = -1;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) set_pool_threshold(dev);
+    batmap_fimi* h = new (std::nothrow) batmap_fimi();
+    if (!h) {
+        set_error("host allocation");
+        return BATMAP_E_NOMEM;
+    }
+    const batmap_status rc = fimi_parse(text, n_bytes, st, h, bad_line);
+    if (rc != BATMAP_OK) {
+        batmap_fimi_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return BATMAP_OK;
+}
+
+batmap_status batmap_fimi_info(batmap_fimi_handle h, int64_t* n_items, int64_t* nnz, int64_t* n_transactions) {
+    if (!h || !n_items || !nnz || !n_transactions) {
+        set_error("null argument");
+        return BATMAP_E_INVALID;
+    }
+    *n_items = h->n_items;
+    *nnz = h->nnz;
+    *n_transactions = h->m;
+    return BATMAP_OK;
+}
+
+batmap_status batmap_fimi_filter(batmap_fimi_handle h, uint32_t min_support, batmap_stream_t stream) {
+    if (!h) {
+        set_error("null handle");
+        return BATMAP_E_INVALID;
+    }
+    return fimi_filter(h, min_support, reinterpret_cast<cudaStream_t>(stream));
+}
+
+batmap_status batmap_fimi_export(batmap_fimi_handle h, int64_t* offsets, int32_t* tids, uint32_t* labels,
+                                 batmap_stream_t stream) {
+    if (!h) {
+        set_error("null handle");
+        return BATMAP_E_INVALID;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (offsets)
+        BM_CUDA(cudaMemcpyAsync(offsets, h->off_d, (h->n_items + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    if (tids && h->nnz) BM_CUDA(cudaMemcpyAsync(tids, h->tids_d, h->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    if (labels && h->n_items)
+        BM_CUDA(cudaMemcpyAsync(labels, h->labels_d, h->n_items * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    return BATMAP_OK;
+}
+
+void batmap_fimi_destroy(batmap_fimi_handle h) {
+    if (!h) return;
+    dfree(h->off_d, nullptr);
+    dfree(h->tids_d, nullptr);
+    dfree(h->labels_d, nullptr);
+    delete h;
+}
+
+batmap_status batmap_frequent_items(const int64_t* offsets, int64_t n_items, uint32_t min_support, int32_t* items_out,
+                                    int64_t* n_out, batmap_stream_t stream) {
+    if (!n_out || n_items < 0 || (n_items > 0 && (!offsets || !items_out))) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    if (n_items >= (1ll << 31)) {
+        set_error("n_items must be < 2^31");
+        return BATMAP_E_OVERFLOW;
+    }
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) set_pool_threshold(dev);
+    return frequent_items(offsets, n_items, min_support, items_out, n_out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 static bool promote_enabled() {

@@ -254,6 +254,11 @@ batmap_status run_finalize(batmap_collection* h, const Selection& sel, int64_t n
 batmap_status gather_selection(batmap_collection* h, const int32_t* items_d, int64_t n_sel,
                                cudaStream_t st, Selection* sel);
 batmap_status sort_triples(batmap_triple* t, int64_t n, cudaStream_t st);
+// ingest.cu
+batmap_status fimi_parse(const uint8_t* text, int64_t n, cudaStream_t st, batmap_fimi* h, int64_t* bad_line);
+batmap_status fimi_filter(batmap_fimi* h, uint32_t min_support, cudaStream_t st);
+batmap_status frequent_items(const int64_t* off, int64_t n_items, uint32_t min_support, int32_t* items_out,
+                             int64_t* n_out, cudaStream_t st);
 // dense.cu
 batmap_status dense_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t m,
                                   const int32_t* items, int64_t n_sel, uint32_t threshold, batmap_triple* out,

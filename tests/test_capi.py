@@ -66,6 +66,16 @@ def test_argument_errors_without_device():
     inf = batmap.Info()
     assert lib.batmap_info(None, ctypes.byref(inf)) == batmap.BATMAP_E_INVALID
     lib.batmap_destroy(None)
+    fh, bad = ctypes.c_void_p(), ctypes.c_int64()
+    assert lib.batmap_fimi_parse(None, 5, None, ctypes.byref(fh), ctypes.byref(bad)) == batmap.BATMAP_E_INVALID
+    assert lib.batmap_fimi_parse(ctypes.c_void_p(8), -1, None, ctypes.byref(fh), ctypes.byref(bad)) == \
+        batmap.BATMAP_E_INVALID
+    assert lib.batmap_fimi_filter(None, 3, None) == batmap.BATMAP_E_INVALID
+    assert lib.batmap_fimi_info(None, ctypes.byref(n), ctypes.byref(n), ctypes.byref(n)) == batmap.BATMAP_E_INVALID
+    assert lib.batmap_frequent_items(None, 5, 1, None, ctypes.byref(n), None) == batmap.BATMAP_E_INVALID
+    assert lib.batmap_frequent_items(ctypes.c_void_p(8), -1, 1, ctypes.c_void_p(8), ctypes.byref(n), None) == \
+        batmap.BATMAP_E_INVALID
+    lib.batmap_fimi_destroy(None)
 
 
 def _collect(class_n, class_w, n_parts, grid_cap=0):
