@@ -234,6 +234,9 @@ typedef struct {
     int32_t k2_grid;        /* CTAs launched for K2                                        */
     int64_t launches_build;
     int64_t launches_pairs;
+    double build_pre_ms;    /* batmap_build up to the insertion kernel (offsets read-back, host
+                               planning, uploads, padding fill) as seen on the stream          */
+    double build_post_ms;   /* batmap_build after the encode (failure list F, Fail(i), A_b)     */
 } batmap_stats_t;
 
 batmap_status batmap_stats(batmap_handle h, batmap_stats_t* out);
@@ -329,7 +332,8 @@ batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const 
  *   - transaction id = 0-based line index; the text after the last '
 ' is a transaction iff it
  *     is non-empty; blank lines are empty transactions;
- *   - a label is a run of decimal digits, 0 <= label <= 2^32 - 1; separators are ' ', '	', '';
+ *   - a label is a run of decimal digits, 0 <= label <= 2^32 - 1; separators are ' ', '	', '
+';
  *     any other byte, or a longer number, is an error;
  *   - duplicate labels within a line collapse (set semantics);
  *   - items are re-densified: dense id k is the k-th smallest label present; labels[k] maps back.

@@ -44,7 +44,8 @@ class Stats(ctypes.Structure):
                 ("pairs_ms", ctypes.c_double), ("k2_ms", ctypes.c_double), ("k3_ms", ctypes.c_double),
                 ("word_compares", ctypes.c_int64), ("tile_compares", ctypes.c_int64),
                 ("n_candidates", ctypes.c_int64), ("n_results", ctypes.c_int64), ("k2_kind", ctypes.c_int32),
-                ("k2_grid", ctypes.c_int32), ("launches_build", ctypes.c_int64), ("launches_pairs", ctypes.c_int64)]
+                ("k2_grid", ctypes.c_int32), ("launches_build", ctypes.c_int64), ("launches_pairs", ctypes.c_int64),
+                ("build_pre_ms", ctypes.c_double), ("build_post_ms", ctypes.c_double)]
 
 
 class Info(ctypes.Structure):

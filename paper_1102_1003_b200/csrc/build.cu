@@ -585,23 +585,26 @@ __global__ void k_fidx(const int32_t* __restrict__ mark, const int32_t* __restri
     if (i < m) fidx[i] = mark[i] ? rank[i] : -1;
 }
 
-// warp per item: count / emit (fidx << 32 | pos) for entries whose tid failed somewhere
+// Flat over the CSR entries (bandwidth-bound, no per-item serial loop): an entry whose tid failed
+// somewhere (fidx >= 0, rare) finds its item by binary search in offsets, then counts / emits
+// (fidx << 32 | pos).
 template <bool kEmit>
 __global__ void k_ab_scan(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
-                          const int32_t* __restrict__ orig2pos, int64_t n,
+                          const int32_t* __restrict__ orig2pos, int64_t n, int64_t nnz,
                           const int32_t* __restrict__ fidx, unsigned long long* __restrict__ cnt,
                           uint64_t* __restrict__ keys, unsigned long long* __restrict__ cursor) {
-    int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-    int lane = threadIdx.x & 31;
-    if (item >= n) return;
-    int64_t b = offsets[item], e = offsets[item + 1];
-    uint32_t pos = (uint32_t)orig2pos[item];
-    for (int64_t k = b + lane; k < e; k += 32) {
-        int32_t f = fidx[tids[k]];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = __ldg(fidx + __ldg(tids + k));
         if (f < 0) continue;
         if (kEmit) {
-            unsigned long long at = atomicAdd(cursor, 1ull);
-            keys[at] = ((uint64_t)(uint32_t)f << 32) | pos;
+            int64_t lo = 0, hi = n - 1;  // last item with offsets[item] <= k
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (__ldg(offsets + mid) <= k) lo = mid;
+                else hi = mid - 1;
+            }
+            const unsigned long long at = atomicAdd(cursor, 1ull);
+            keys[at] = ((uint64_t)(uint32_t)f << 32) | (uint32_t)orig2pos[lo];
         } else {
             atomicAdd(cnt + f, 1ull);
         }
@@ -632,7 +635,7 @@ static int ilog2_u64(uint64_t v) {
 }
 
 // Failure list F sorted by (pos, tid), per-item offsets and A_b of failed tids.
-static batmap_status post_failures(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
+static batmap_status post_failures(batmap_collection* h, const int64_t* offsets, const int32_t* tids, int64_t nnz,
                                    uint64_t* fails, int64_t F, cudaStream_t st) {
     const int64_t n = h->n, m = h->m;
     BM_TRY(dalloc_t(&h->fail_off_d, n + 1, st));
@@ -703,8 +706,9 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     unsigned long long* cnt = nullptr;
     BM_TRY(dalloc_t(&cnt, nft + 1, st));
     BM_CUDA(cudaMemsetAsync(cnt, 0, (nft + 1) * sizeof(unsigned long long), st));
-    k_ab_scan<false><<<grid_for(n * 32, 256), 256, 0, st>>>(offsets, tids, h->orig2pos_d, n,
-                                                             h->fidx_of_tid_d, cnt, nullptr, nullptr);
+    const unsigned scan_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(nnz, 256), 148 * 8));
+    k_ab_scan<false><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, cnt, nullptr,
+                                                nullptr);
     h->launches += 1;
     BM_TRY(dalloc_t(&h->ab_off_d, nft + 1, st));
     {
@@ -724,8 +728,8 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     BM_TRY(dalloc_t(&keys2, total, st));
     BM_TRY(dalloc_t(&cursor, 1, st));
     BM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
-    k_ab_scan<true><<<grid_for(n * 32, 256), 256, 0, st>>>(offsets, tids, h->orig2pos_d, n,
-                                                            h->fidx_of_tid_d, nullptr, keys, cursor);
+    k_ab_scan<true><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, nullptr, keys,
+                                               cursor);
     h->launches += 1;
     {
         int eb = 32 + std::max(1, ilog2_u64((uint64_t)nft + 1));
@@ -830,6 +834,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         lr_item[i] = (uint8_t)std::max(l, lmin);
     }
     const int64_t nnz = off_h[n];
+    h->nnz = nnz;
     // ---- sort by width, stable by id (reading #16): counting sort over log2 r
     h->pos2orig_h.resize(n);
     h->orig2pos_h.resize(n);
@@ -1046,7 +1051,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     rec(h, EV_E1, st);
     BM_CUDA(cudaGetLastError());
     if (n_parts == 1) {
-        BM_TRY(post_failures(h, offsets, tids, fails, F, st));
+        BM_TRY(post_failures(h, offsets, tids, nnz, fails, F, st));
     } else {  // sharded: keep this part's failure records for the exchange (batmap_shard_import)
         BM_TRY(dalloc_t(&h->shard_fails_d, std::max<int64_t>(F, 1), st));
         if (F) BM_CUDA(cudaMemcpyAsync(h->shard_fails_d, fails, F * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
@@ -1117,7 +1122,7 @@ batmap_status shard_import(batmap_collection* h, const int64_t* offsets, const i
                                 cudaMemcpyDeviceToDevice, st));
         at += n_fails[p];
     }
-    BM_TRY(post_failures(h, offsets, tids, fails, F, st));
+    BM_TRY(post_failures(h, offsets, tids, h->nnz, fails, F, st));
     dfree(fails, st);
     dfree(h->shard_fails_d, st);
     h->shard_fails_d = nullptr;

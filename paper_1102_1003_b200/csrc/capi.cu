@@ -23,6 +23,11 @@ void set_pool_threshold(int dev) {
     done[dev] = true;
 }
 
+void init_pool() {  // keep freed blocks in the stream-ordered pool (no re-mapping per call)
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) set_pool_threshold(dev);
+}
+
 void free_all(batmap_collection* h) {
     cudaStream_t st = h->stream;
     void* ptrs[] = {h->pos2orig_d, h->orig2pos_d, h->arena_d,   h->f_d,      h->fail_off_d, h->fail_tid_d,
@@ -292,6 +297,8 @@ batmap_status batmap_stats(batmap_handle h, batmap_stats_t* out) {
         h->stats.build_ms = ev_ms(h, EV_B0, EV_B1);
         h->stats.k1_insert_ms = ev_ms(h, EV_I0, EV_I1);
         h->stats.k1_encode_ms = ev_ms(h, EV_E0, EV_E1);
+        h->stats.build_pre_ms = ev_ms(h, EV_B0, EV_I0);
+        h->stats.build_post_ms = ev_ms(h, EV_E1, EV_B1);
     }
     if (h->ev_ok && h->pairs_timed) {
         h->stats.pairs_ms = ev_ms(h, EV_P0, EV_P1);
@@ -316,6 +323,7 @@ batmap_status batmap_dense_pair_supports(const int64_t* offsets, const int32_t* 
         return BATMAP_E_OVERFLOW;
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    init_pool();
     if (items && n_sel) {  // validate the selection on the host
         std::vector<int32_t> it(n_sel);
         BM_CUDA(cudaMemcpyAsync(it.data(), items, n_sel * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -345,6 +353,7 @@ batmap_status batmap_merge_pair_supports(const int64_t* offsets, const int32_t* 
         return BATMAP_E_OVERFLOW;
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    init_pool();
     if (items && n_sel) {  // validate the selection on the host
         std::vector<int32_t> it(n_sel);
         BM_CUDA(cudaMemcpyAsync(it.data(), items, n_sel * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -486,8 +495,7 @@ batmap_status batmap_fimi_parse(const uint8_t* text, int64_t n_bytes, batmap_str
     *out = nullptr;
     *bad_line = -1;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) set_pool_threshold(dev);
+    init_pool();
     batmap_fimi* h = new (std::nothrow) batmap_fimi();
     if (!h) {
         set_error("host allocation");
@@ -554,8 +562,7 @@ batmap_status batmap_frequent_items(const int64_t* offsets, int64_t n_items, uin
         set_error("n_items must be < 2^31");
         return BATMAP_E_OVERFLOW;
     }
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) set_pool_threshold(dev);
+    init_pool();
     return frequent_items(offsets, n_items, min_support, items_out, n_out, reinterpret_cast<cudaStream_t>(stream));
 }
 

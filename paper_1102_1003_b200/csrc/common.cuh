@@ -121,6 +121,7 @@ struct batmap_collection {
     cudaStream_t stream = nullptr;
 
     int64_t n = 0, m = 0;
+    int64_t nnz = 0;  // entries of the input CSR (set by the build)
     int s = 0;
     int64_t U = 0;
     int64_t r0 = 0;

@@ -87,7 +87,8 @@ def run(name, reps=3):
     peak = 32 * torch.cuda.get_device_properties(0).multi_processor_count * 1.965e9
     line = dict(config=name, n=n, m=w.m, nnz=w.nnz, threshold=w.threshold, classes=inf["n_classes"],
                 arena_MB=inf["arena_bytes"] / 1e6, failures=inf["n_failures"], K=int(got.shape[0]),
-                step_ms=tot, build_ms=st["build_ms"], k1_ms=st["k1_insert_ms"], k1_encode_ms=st["k1_encode_ms"], pairs_ms=st["pairs_ms"],
+                step_ms=tot, build_ms=st["build_ms"], k1_ms=st["k1_insert_ms"], k1_encode_ms=st["k1_encode_ms"], build_pre_ms=st["build_pre_ms"],
+                build_post_ms=st["build_post_ms"], pairs_ms=st["pairs_ms"],
                 k2_ms=st["k2_ms"], k3_ms=st["k3_ms"], k2_kind=st["k2_kind"],
                 word_compares=st["word_compares"], tile_compares=st["tile_compares"],
                 pairs_per_s=pairs / (tot / 1e3), freq_pairs_per_s=got.shape[0] / (tot / 1e3),
