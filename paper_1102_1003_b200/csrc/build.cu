@@ -429,63 +429,6 @@ __global__ void __launch_bounds__(NT) k1_conc_cluster(
     if (CS > 1) cl.sync();  // no CTA may exit while another still reads its slice
 }
 
-// Concurrent tier for large tables (r > kClusterMaxR): the working table lives in global memory
-// (raw tids, atomics in L2); π is recomputed on every swap.  One CTA per item.
-__global__ void __launch_bounds__(256) k1_conc_global(
-    const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
-    const int64_t* __restrict__ work_off, int64_t pos_begin, PiParams P, uint32_t r, int log2r, uint32_t r0,
-    int log2r0, uint32_t max_loop_opt, uint32_t* __restrict__ work, int32_t* __restrict__ fcount,
-    uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr, int64_t fail_cap) {
-    __shared__ uint32_t fl[kConcFailCap];
-    __shared__ int nfl, overflow;
-    const int64_t pos = pos_begin + blockIdx.x;
-    const int orig = pos2orig[pos];
-    const int64_t b = offsets[orig];
-    const int n = (int)(offsets[orig + 1] - b);
-    const int32_t* S = tids + b;
-    uint32_t* A = work + work_off[blockIdx.x];
-    if (threadIdx.x == 0) {
-        nfl = 0;
-        overflow = 0;
-    }
-    __syncthreads();
-    const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)log2r;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const uint32_t x = (uint32_t)__ldg(S + e);
-        for (int copy = 0; copy < 2; ++copy) {
-            uint32_t tau = x;
-            for (uint32_t l = 0; l < max_loop && tau != kEmpty; ++l)
-#pragma unroll
-                for (int t = 0; t < 3 && tau != kEmpty; ++t)
-                    tau = atomicExch(&A[slot_of(t, pi_eval(P, t, tau), r, r0, log2r0)], tau);
-            if (tau != kEmpty) record_failure(fl, &nfl, fails, fail_ctr, fail_cap, pos, tau, tau, &overflow);
-        }
-    }
-    __syncthreads();
-    const int nf = nfl;
-    if (!overflow) {
-        for (int k = threadIdx.x; k < nf; k += blockDim.x) {
-            const uint32_t x = fl[k];
-#pragma unroll
-            for (int t = 0; t < 3; ++t) atomicCAS(&A[slot_of(t, pi_eval(P, t, x), r, r0, log2r0)], x, kEmpty);
-        }
-    } else {
-        for (int e = threadIdx.x; e < n; e += blockDim.x) {
-            const uint32_t x = (uint32_t)S[e];
-            uint32_t q[3];
-            int cnt = 0;
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-                q[t] = slot_of(t, pi_eval(P, t, x), r, r0, log2r0);
-                cnt += (A[q[t]] == x);
-            }
-            if (cnt == 1)
-#pragma unroll
-                for (int t = 0; t < 3; ++t) atomicCAS(&A[q[t]], x, kEmpty);
-        }
-    }
-    if (threadIdx.x == 0) fcount[pos] = nf;
-}
 
 // Encode columns [0, n) of one class block: thread per (word w, column c); writes
 // arena_cls[w * n_pad + c] (padding columns are filled by k_fill_padding).
@@ -583,6 +526,68 @@ __global__ void k_fidx(const int32_t* __restrict__ mark, const int32_t* __restri
                        int32_t* __restrict__ fidx) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) fidx[i] = mark[i] ? rank[i] : -1;
+}
+
+// Global tier split over CTAs (reading #9b): the giant tables (C4: one item of r = 2^21 holds 1.2e6
+// elements) are cut into chunks of kGChunk elements, each chunk a CTA, all inserting concurrently
+// into the item's table in L2/HBM with atomic swaps; a chain exceeding MaxLoop records its
+// nestless element in F directly.  Copies are conserved by every swap, so once all chunks are done
+// an element with exactly one copy left is exactly a recorded failure: k1_gchunk_cleanup deletes
+// that copy (F itself is deduplicated and counted per item by post_failures).
+constexpr int kGChunk = 2048;
+struct GChunk {
+    int64_t pos;     // width-sorted position of the item
+    int32_t e0, e1;  // element range of the chunk
+    int32_t log2r, pad;
+};
+
+__global__ void __launch_bounds__(256) k1_gchunk_insert(
+    const GChunk* __restrict__ chunks, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
+    const int32_t* __restrict__ pos2orig, const int64_t* __restrict__ work_off, int64_t big_begin, PiParams P,
+    uint32_t r0, int log2r0, uint32_t max_loop_opt, uint32_t* __restrict__ work, uint64_t* __restrict__ fails,
+    unsigned long long* __restrict__ fail_ctr, int64_t fail_cap) {
+    const GChunk ch = chunks[blockIdx.x];
+    const uint32_t r = 1u << ch.log2r;
+    const int32_t* S = tids + offsets[pos2orig[ch.pos]];
+    uint32_t* A = work + work_off[ch.pos - big_begin];
+    const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)ch.log2r;
+    for (int e = ch.e0 + threadIdx.x; e < ch.e1; e += blockDim.x) {
+        const uint32_t x = (uint32_t)__ldg(S + e);
+        for (int copy = 0; copy < 2; ++copy) {
+            uint32_t tau = x;
+            for (uint32_t l = 0; l < max_loop && tau != kEmpty; ++l)
+#pragma unroll
+                for (int t = 0; t < 3 && tau != kEmpty; ++t)
+                    tau = atomicExch(&A[slot_of(t, pi_eval(P, t, tau), r, r0, log2r0)], tau);
+            if (tau != kEmpty) {
+                const unsigned long long idx = atomicAdd(fail_ctr, 1ull);
+                if ((int64_t)idx < fail_cap) fails[idx] = ((uint64_t)ch.pos << 32) | tau;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k1_gchunk_cleanup(
+    const GChunk* __restrict__ chunks, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
+    const int32_t* __restrict__ pos2orig, const int64_t* __restrict__ work_off, int64_t big_begin, PiParams P,
+    uint32_t r0, int log2r0, uint32_t* __restrict__ work) {
+    const GChunk ch = chunks[blockIdx.x];
+    const uint32_t r = 1u << ch.log2r;
+    const int32_t* S = tids + offsets[pos2orig[ch.pos]];
+    uint32_t* A = work + work_off[ch.pos - big_begin];
+    for (int e = ch.e0 + threadIdx.x; e < ch.e1; e += blockDim.x) {
+        const uint32_t x = (uint32_t)__ldg(S + e);
+        uint32_t q[3];
+        int cnt = 0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            q[t] = slot_of(t, pi_eval(P, t, x), r, r0, log2r0);
+            cnt += (A[q[t]] == x);
+        }
+        if (cnt == 1)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) atomicCAS(&A[q[t]], x, kEmpty);
+    }
 }
 
 // Flat over the CSR entries (bandwidth-bound, no per-item serial loop): an entry whose tid failed
@@ -911,6 +916,19 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         v.word_off = c.word_off + c0;
         return v;
     };
+    // ---- chunks of the global tier's items (this part's share of each class)
+    std::vector<GChunk> gchunks;
+    if (!serial)
+        for (const ClassInfo& cl : h->classes) {
+            const ClassInfo c = view(cl);
+            if (c.r <= kClusterMaxR) continue;
+            for (int64_t p = c.first; p < c.first + c.n; ++p) {
+                const int32_t o2 = h->pos2orig_h[p];
+                const int32_t len = (int32_t)(off_h[o2 + 1] - off_h[o2]);
+                for (int32_t e0 = 0; e0 < std::max(len, 1); e0 += kGChunk)
+                    gchunks.push_back({p, e0, std::min(len, e0 + kGChunk), ilog2_u64((uint64_t)c.r), 0});
+            }
+        }
     // ---- device state
     BM_TRY(dalloc_t(&h->pos2orig_d, n, st));
     BM_TRY(dalloc_t(&h->orig2pos_d, n, st));
@@ -922,6 +940,10 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     BM_TRY(dalloc_t(&work_off_d, n_big + 1, st));
     BM_TRY(dalloc_t(&lr_d, n, st));
     BM_TRY(dalloc_t(&work, work_entries, st));
+    GChunk* gchunks_d = nullptr;
+    BM_TRY(dalloc_t(&gchunks_d, (int64_t)gchunks.size(), st));
+    if (!gchunks.empty())
+        BM_CUDA(cudaMemcpyAsync(gchunks_d, gchunks.data(), gchunks.size() * sizeof(GChunk), cudaMemcpyHostToDevice, st));
     if (n) {
         BM_CUDA(cudaMemcpyAsync(h->pos2orig_d, h->pos2orig_h.data(), n * 4, cudaMemcpyHostToDevice, st));
         BM_CUDA(cudaMemcpyAsync(h->orig2pos_d, h->orig2pos_h.data(), n * 4, cudaMemcpyHostToDevice, st));
@@ -942,6 +964,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
             dfree(work_off_d, st);
             dfree(lr_d, st);
             dfree(work, st);
+            dfree(gchunks_d, st);
             set_error("invalid tidlists: every tidlist must be strictly increasing in [0, n_transactions)");
             return BATMAP_E_INVALID;
         }
@@ -991,13 +1014,10 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
                 h->launches += 1;
             }
         } else {
-            for (size_t a = 0; a < h->classes.size(); ++a) {  // big classes first (longest items)
-                const ClassInfo c = view(h->classes[a]);
-                if (c.r <= kClusterMaxR || c.n == 0) continue;
-                k1_conc_global<<<c.n, 256, 0, st>>>(offsets, tids, h->pos2orig_d, work_off_d + (c.first - big_begin),
-                                                    c.first, h->pi, (uint32_t)c.r, ilog2_u64((uint64_t)c.r),
-                                                    (uint32_t)h->r0, h->log2r0, h->max_loop_opt, work, h->f_d, fails,
-                                                    fail_ctr, fail_cap);
+            if (!gchunks.empty()) {  // big classes first (longest items), split over CTAs
+                k1_gchunk_insert<<<(unsigned)gchunks.size(), 256, 0, st>>>(
+                    gchunks_d, offsets, tids, h->pos2orig_d, work_off_d, big_begin, h->pi, (uint32_t)h->r0,
+                    h->log2r0, h->max_loop_opt, work, fails, fail_ctr, fail_cap);
                 h->launches += 1;
             }
             // r <= cl_min_r: the slot-caching CTA kernel (faster for narrow tables, measured on C2);
@@ -1024,6 +1044,12 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
                     fail_ctr, fail_cap);
                 h->launches += 1;
             }
+        }
+        if (!serial && !gchunks.empty()) {
+            k1_gchunk_cleanup<<<(unsigned)gchunks.size(), 256, 0, st>>>(gchunks_d, offsets, tids, h->pos2orig_d,
+                                                                        work_off_d, big_begin, h->pi,
+                                                                        (uint32_t)h->r0, h->log2r0, work);
+            h->launches += 1;
         }
         rec(h, EV_I1, st);
         BM_CUDA(cudaGetLastError());
@@ -1066,6 +1092,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     dfree(work, st);
     dfree(work_off_d, st);
     dfree(lr_d, st);
+    dfree(gchunks_d, st);
     rec(h, EV_B1, st);
     h->build_timed = true;
     h->stats.launches_build = h->launches - l0;

@@ -2,12 +2,46 @@
 // symmetry cut p <= q, virtualised skinny rectangles, split-K for long tiles, and
 // the deal of work to the parts of a multi-GPU run, and promotion of small narrow classes.
 #include <algorithm>
+#include <functional>
+#include <unordered_map>
 
 #include "plan.h"
 
 namespace bm {
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Stable sort by descending cost.  Work lists have few distinct costs (one per rectangle, per
+// accumulated tile row or per k-piece length), so this buckets in O(T) instead of comparing
+// (C4: 3e5 tiles; the plan is built on the host while the build kernels run).
+template <typename T, typename Cost>
+static void stable_sort_desc(std::vector<T>& v, Cost cost) {
+    std::unordered_map<int64_t, int32_t> first_seen;  // cost -> id in order of first appearance
+    std::vector<int64_t> keys;
+    std::vector<int32_t> bucket(v.size());
+    int64_t last = -1;
+    int32_t last_id = -1;
+    for (size_t e = 0; e < v.size(); ++e) {
+        const int64_t c = cost(v[e]);
+        if (c != last) {  // runs of equal cost are the common case
+            auto it = first_seen.emplace(c, (int32_t)keys.size());
+            if (it.second) keys.push_back(c);
+            last = c;
+            last_id = it.first->second;
+        }
+        bucket[e] = last_id;
+    }
+    std::vector<int32_t> order(keys.size()), rank(keys.size());
+    for (size_t k = 0; k < keys.size(); ++k) order[k] = (int32_t)k;
+    std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return keys[a] > keys[b]; });
+    for (size_t k = 0; k < order.size(); ++k) rank[order[k]] = (int32_t)k;
+    std::vector<int64_t> at(keys.size() + 1, 0);
+    for (size_t e = 0; e < v.size(); ++e) ++at[rank[bucket[e]] + 1];
+    for (size_t k = 1; k < at.size(); ++k) at[k] += at[k - 1];
+    std::vector<T> out(v.size());
+    for (size_t e = 0; e < v.size(); ++e) out[at[rank[bucket[e]]]++] = v[e];
+    v.swap(out);
+}
 
 int lg_ratio(int64_t W, int64_t W_min) {
     if (W_min <= 0 || W < W_min || W % W_min) return -1;
@@ -226,6 +260,14 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         int64_t cost;
     };
     std::vector<Unit> units;
+    {
+        int64_t nu = 0;
+        for (const Rect& r : P.rects) {
+            const int64_t ta = ceil_div(r.n_rows, kTile), tb = ceil_div(r.n_cols, kTile);
+            nu += r.acc ? ta : (r.diag ? ta * (ta + 1) / 2 : ta * tb);
+        }
+        units.reserve((size_t)nu);
+    }
     for (int ri = 0; ri < (int)P.rects.size(); ++ri) {
         const Rect& r = P.rects[ri];
         const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, kTile);
@@ -238,12 +280,13 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             }
         }
     }
-    std::stable_sort(units.begin(), units.end(), [](const Unit& x, const Unit& y) { return x.cost > y.cost; });
+    stable_sort_desc(units, [](const Unit& x) { return x.cost; });
     struct WorkC {
         Work w;
         int64_t cost;
     };
     std::vector<WorkC> work;
+    work.reserve(units.size() / (size_t)n_parts + 16);
     for (size_t k = 0; k < units.size(); ++k) {
         if ((int)(k % (size_t)n_parts) != part) continue;
         const Unit& u = units[k];
@@ -293,7 +336,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             }
         }
     }
-    std::stable_sort(work.begin(), work.end(), [](const WorkC& x, const WorkC& y) { return x.cost > y.cost; });
+    stable_sort_desc(work, [](const WorkC& x) { return x.cost; });
     // ---- the tail of the schedule: the last grid_cap items (the shortest, claimed last) are whole
     // tiles of ordinary rectangles; cut each into pieces along k so that the CTAs finish within a
     // piece of each other (C2: makespan/mean 1.046 -> 1.005 in the planner's cost model).  The
@@ -324,8 +367,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         if (!P.tails.empty()) {
             P.tail_pieces = pcs;
             work.insert(work.end(), pieces.begin(), pieces.end());
-            std::stable_sort(work.begin(), work.end(),
-                             [](const WorkC& x, const WorkC& y) { return x.cost > y.cost; });
+            stable_sort_desc(work, [](const WorkC& x) { return x.cost; });
         }
     }
     P.work.reserve(work.size());
