@@ -20,6 +20,18 @@ from paper_1102_1003_b200 import Collection, dense_pair_supports, merge_pair_sup
 from workloads import CONFIGS, make_config, to_horizontal  # noqa: E402
 
 
+def _hbm_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        for k in ("hbm_gbs", "hbm_copy_gbs", "hbm_GBps"):
+            if k in d:
+                return float(d[k])
+    except Exception:
+        pass
+    return 6650.0  # B200_PROFILING.md fallback
+
+
 def run(name, reps=3):
     t0 = time.time()
     w = make_config(name)
@@ -85,6 +97,12 @@ def run(name, reps=3):
     n = w.n
     pairs = n * (n - 1) // 2
     peak = 32 * torch.cuda.get_device_properties(0).multi_processor_count * 1.965e9
+    # ★K1: 2 nnz insertions; compulsory bytes = the tids read + the arena written
+    hbm = _hbm_peak_gbs() * 1e9
+    k1_s = (st["k1_insert_ms"] + st["k1_encode_ms"]) / 1e3
+    k1 = dict(insertions_per_s=2 * w.nnz / k1_s if k1_s > 0 else None,
+              compulsory_bytes=4 * w.nnz + inf["arena_bytes"],
+              hbm_frac=(4 * w.nnz + inf["arena_bytes"]) / k1_s / hbm if k1_s > 0 else None)
     line = dict(config=name, n=n, m=w.m, nnz=w.nnz, threshold=w.threshold, classes=inf["n_classes"],
                 arena_MB=inf["arena_bytes"] / 1e6, failures=inf["n_failures"], K=int(got.shape[0]),
                 step_ms=tot, build_ms=st["build_ms"], k1_ms=st["k1_insert_ms"], k1_encode_ms=st["k1_encode_ms"], build_pre_ms=st["build_pre_ms"],
@@ -93,7 +111,7 @@ def run(name, reps=3):
                 word_compares=st["word_compares"], tile_compares=st["tile_compares"],
                 pairs_per_s=pairs / (tot / 1e3), freq_pairs_per_s=got.shape[0] / (tot / 1e3),
                 k2_frac_R_int=(st["word_compares"] / (st["k2_ms"] / 1e3) / peak) if st["k2_ms"] > 0 else None,
-                exact=exact, parity=how, oracle_s=round(oracle_s, 1), gen_s=round(gen_s, 1), dense_xtx=dense,
+                k1=k1, exact=exact, parity=how, oracle_s=round(oracle_s, 1), gen_s=round(gen_s, 1), dense_xtx=dense,
                 merge=merge)
     print(json.dumps(line), flush=True)
     return exact
