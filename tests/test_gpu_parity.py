@@ -371,6 +371,27 @@ def test_edge_cases():
     np.testing.assert_array_equal(res, oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=2))
 
 
+@pytest.mark.parametrize("m", [1, 2, 126, 127, 128, 254, 255, 1016, 1017])
+def test_universe_boundaries(m):
+    """Around the code-width boundaries 127 * 2^s (reading #2: s = min{s : 127 * 2^s >= m}; at
+    s = 0 every code 0..126 is live and ⊥ = 0x7F must never match): full tidlists (|S| = m),
+    identical ones, singletons and random sets, all pairs at threshold 0 and 1, both build modes."""
+    rng = np.random.default_rng(m)
+    rows = [np.arange(m), np.arange(m), np.array([m - 1]), np.array([0])]
+    for _ in range(14):
+        k = int(rng.integers(0, m + 1))
+        rows.append(np.sort(rng.choice(m, size=k, replace=False)))
+    rows.append(rows[-1].copy())
+    off = np.zeros(len(rows) + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    tids = np.concatenate(rows).astype(np.int32)
+    for serial in (False, True):
+        c = _coll(off, tids, m, seed=m, serial=serial)
+        for thr in (0, 1):
+            np.testing.assert_array_equal(_np(c.pair_supports(threshold=thr)), oracle.pairs_merge(off, tids, threshold=thr))
+        c.close()
+
+
 def test_determinism_and_seed_independence():
     w = make_config("C1")
     a = _coll(w.offsets, w.tids, w.m, seed=1, serial=True)
