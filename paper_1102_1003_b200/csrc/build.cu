@@ -514,12 +514,13 @@ __global__ void k_fail_offsets(const uint64_t* __restrict__ keys, int64_t F, int
 }
 
 __global__ void k_fail_split(const uint64_t* __restrict__ keys, int64_t F, int32_t* __restrict__ tid,
-                             int32_t* __restrict__ mark) {
+                             int32_t* __restrict__ mark, uint32_t* __restrict__ fbits) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= F) return;
     uint32_t t = (uint32_t)keys[i];
     tid[i] = (int32_t)t;
     mark[t] = 1;
+    atomicOr(fbits + (t >> 5), 1u << (t & 31));
 }
 
 __global__ void k_fidx(const int32_t* __restrict__ mark, const int32_t* __restrict__ rank, int64_t m,
@@ -590,28 +591,53 @@ __global__ void __launch_bounds__(256) k1_gchunk_cleanup(
     }
 }
 
-// Flat over the CSR entries (bandwidth-bound, no per-item serial loop): an entry whose tid failed
-// somewhere (fidx >= 0, rare) finds its item by binary search in offsets, then counts / emits
-// (fidx << 32 | pos).
+// Flat over the CSR entries, 4 per thread per step so that the fidx gathers of a thread are
+// independent (the pass is latency-bound otherwise).  An entry whose tid failed somewhere
+// (fidx >= 0, rare) finds its item by binary search in offsets, then counts / emits
+// (fidx << 32 | pos); emits take one cursor atomic per warp.
 template <bool kEmit>
-__global__ void k_ab_scan(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
-                          const int32_t* __restrict__ orig2pos, int64_t n, int64_t nnz,
-                          const int32_t* __restrict__ fidx, unsigned long long* __restrict__ cnt,
-                          uint64_t* __restrict__ keys, unsigned long long* __restrict__ cursor) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t f = __ldg(fidx + __ldg(tids + k));
-        if (f < 0) continue;
-        if (kEmit) {
-            int64_t lo = 0, hi = n - 1;  // last item with offsets[item] <= k
-            while (lo < hi) {
-                const int64_t mid = (lo + hi + 1) >> 1;
-                if (__ldg(offsets + mid) <= k) lo = mid;
-                else hi = mid - 1;
+__global__ void __launch_bounds__(256) k_ab_scan(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
+                                                 const int32_t* __restrict__ orig2pos, int64_t n, int64_t nnz,
+                                                 const int32_t* __restrict__ fidx, const uint32_t* __restrict__ fbits,
+                                                 unsigned long long* __restrict__ cnt,
+                                                 uint64_t* __restrict__ keys, unsigned long long* __restrict__ cursor) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4 - lane * 4 + lane;
+         base - lane < nnz; base += stride) {
+        // the warp covers 128 consecutive entries; lane l takes entries base + 32 q (coalesced)
+        int32_t f[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t k = base + 32 * q;
+            f[q] = -1;
+            if (k < nnz) {  // the m-bit set of failed tids is L1-resident; fidx is read for hits only
+                const uint32_t t = (uint32_t)__ldg(tids + k);
+                if (__ldg(fbits + (t >> 5)) >> (t & 31) & 1u) f[q] = __ldg(fidx + t);
             }
-            const unsigned long long at = atomicAdd(cursor, 1ull);
-            keys[at] = ((uint64_t)(uint32_t)f << 32) | (uint32_t)orig2pos[lo];
-        } else {
-            atomicAdd(cnt + f, 1ull);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t k = base + 32 * q;
+            const bool hit = f[q] >= 0;
+            if (!kEmit) {
+                if (hit) atomicAdd(cnt + f[q], 1ull);
+                continue;
+            }
+            const unsigned mask = __ballot_sync(0xFFFFFFFFu, hit);
+            if (!mask) continue;
+            unsigned long long at = 0;
+            if (lane == __ffs(mask) - 1) at = atomicAdd(cursor, (unsigned long long)__popc(mask));
+            at = __shfl_sync(0xFFFFFFFFu, at, __ffs(mask) - 1) + __popc(mask & ((1u << lane) - 1));
+            if (hit) {
+                int64_t lo = 0, hi = n - 1;  // last item with offsets[item] <= k
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) >> 1;
+                    if (__ldg(offsets + mid) <= k) lo = mid;
+                    else hi = mid - 1;
+                }
+                keys[at] = ((uint64_t)(uint32_t)f[q] << 32) | (uint32_t)orig2pos[lo];
+            }
         }
     }
 }
@@ -689,10 +715,13 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     h->launches += 1;
     BM_TRY(dalloc_t(&h->fail_tid_d, F, st));
     int32_t *mark = nullptr, *rank = nullptr;
+    uint32_t* fbits = nullptr;
+    BM_TRY(dalloc_t(&fbits, (m + 31) / 32, st));
+    BM_CUDA(cudaMemsetAsync(fbits, 0, (m + 31) / 32 * sizeof(uint32_t), st));
     BM_TRY(dalloc_t(&mark, m + 1, st));
     BM_TRY(dalloc_t(&rank, m + 1, st));
     BM_CUDA(cudaMemsetAsync(mark, 0, (m + 1) * sizeof(int32_t), st));
-    k_fail_split<<<grid_for(F, 256), 256, 0, st>>>(sorted, F, h->fail_tid_d, mark);
+    k_fail_split<<<grid_for(F, 256), 256, 0, st>>>(sorted, F, h->fail_tid_d, mark, fbits);
     h->launches += 1;
     {
         size_t tb = 0;
@@ -711,8 +740,9 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     unsigned long long* cnt = nullptr;
     BM_TRY(dalloc_t(&cnt, nft + 1, st));
     BM_CUDA(cudaMemsetAsync(cnt, 0, (nft + 1) * sizeof(unsigned long long), st));
-    const unsigned scan_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(nnz, 256), 148 * 8));
-    k_ab_scan<false><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, cnt, nullptr,
+    // one 128-entry step per warp: every gather chain and hit's binary search runs in parallel
+    const unsigned scan_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(nnz, 1024), 1 << 30));
+    k_ab_scan<false><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, fbits, cnt, nullptr,
                                                 nullptr);
     h->launches += 1;
     BM_TRY(dalloc_t(&h->ab_off_d, nft + 1, st));
@@ -733,7 +763,7 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     BM_TRY(dalloc_t(&keys2, total, st));
     BM_TRY(dalloc_t(&cursor, 1, st));
     BM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
-    k_ab_scan<true><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, nullptr, keys,
+    k_ab_scan<true><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, fbits, nullptr, keys,
                                                cursor);
     h->launches += 1;
     {
@@ -752,6 +782,7 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     dfree(cursor, st);
     dfree(cnt, st);
     dfree(mark, st);
+    dfree(fbits, st);
     dfree(rank, st);
     dfree(sorted, st);
     dfree(uniq, st);
