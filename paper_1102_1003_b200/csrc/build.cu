@@ -794,13 +794,10 @@ template <int CS, int NT>
 static batmap_status launch_cluster(const ClassInfo& c, batmap_collection* h, const int64_t* offsets,
                                     const int32_t* tids, uint64_t* fails, unsigned long long* fail_ctr,
                                     int64_t fail_cap, cudaStream_t st) {
-    static bool attr = false;
     const size_t smem = (size_t)3 * c.r / CS * sizeof(uint32_t);
-    if (!attr) {
-        BM_CUDA(cudaFuncSetAttribute(k1_conc_cluster<CS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kClSliceBytesMax));
-        attr = true;
-    }
+    // set on every call: the attribute is per device, and the call is a cheap host-side update
+    BM_CUDA(cudaFuncSetAttribute(k1_conc_cluster<CS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kClSliceBytesMax));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)c.n * CS);
     cfg.blockDim = dim3(NT);
@@ -1006,12 +1003,9 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     unsigned long long* fail_ctr = nullptr;
     BM_TRY(dalloc_t(&fail_ctr, 1, st));
     int64_t F = 0;
-    static bool smem_attr = false;
-    if (!smem_attr) {
-        BM_CUDA(cudaFuncSetAttribute(k1_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        BM_CUDA(cudaFuncSetAttribute(k1_conc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        smem_attr = true;
-    }
+    // per device (no process-wide flag: a process may drive several GPUs)
+    BM_CUDA(cudaFuncSetAttribute(k1_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    BM_CUDA(cudaFuncSetAttribute(k1_conc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (int attempt = 0; attempt < 4; ++attempt) {
         BM_TRY(dalloc_t(&fails, fail_cap, st));
         for (const ClassInfo& c : h->classes) {  // ⊥ padding

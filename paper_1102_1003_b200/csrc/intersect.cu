@@ -860,11 +860,7 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
     if (pl.cnt_entries) BM_TRY(ensure(&h->cnt_d, &h->cnt_cap, pl.cnt_entries, st));
     const int64_t tail_words = (int64_t)pl.tails.size() * pl.tail_pieces * kBM * kBN;
     if (tail_words) BM_TRY(ensure(&h->tail_d, &h->tail_cap, tail_words, st));
-    static bool attr_set = false;
-    if (!attr_set) {
-        BM_CUDA(cudaFuncSetAttribute(k2_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
-        attr_set = true;
-    }
+    BM_CUDA(cudaFuncSetAttribute(k2_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));  // per device
     const K2Maps* prm = kp->prm;
     Rect* rects_d = kp->rects_d;
     Work* work_d = kp->work_d;

@@ -176,11 +176,7 @@ batmap_status merge_pair_supports(const int64_t* offsets, const int32_t* tids, i
     // lanes and from global memory in others issues both loads (measured 2x slower on C3)
     const bool stage_b = (size_t)(kMergeWarps + 1) * cap * 4 <= smem_max;
     const size_t smem = stage_b ? (size_t)(kMergeWarps + 1) * cap * 4 : 0;
-    static bool attr = false;
-    if (!attr) {
-        BM_CUDA(cudaFuncSetAttribute(k_merge<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
-        attr = true;
-    }
+    BM_CUDA(cudaFuncSetAttribute(k_merge<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
     int2* task_d = nullptr;
     int32_t* tids_pad = nullptr;
     uint64_t* keys = nullptr;
