@@ -237,6 +237,8 @@ typedef struct {
     double build_pre_ms;    /* batmap_build up to the insertion kernel (offsets read-back, host
                                planning, uploads, padding fill) as seen on the stream          */
     double build_post_ms;   /* batmap_build after the encode (failure list F, Fail(i), A_b)     */
+    int32_t k2_tile_cols;   /* tiled K2: tile width in items (128, or 64 for small/ragged plans)  */
+    int32_t reserved;
 } batmap_stats_t;
 
 batmap_status batmap_stats(batmap_handle h, batmap_stats_t* out);
@@ -311,7 +313,7 @@ batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n
  * k-chunks [k0, k1) of 16 words; R > 1 marks a virtualised rectangle (each class-b BatMap viewed as
  * R columns of class_w[a] words); acc = 1 marks rectangles whose partial counts are summed in
  * global counters (virtualised or split along k).
- *   grid_cap  resident CTAs assumed for the split-K target (0 => 2 x 148).
+ *   grid_cap  resident CTAs assumed for the split-K target (0 => 2 x 148, or 4 x 148 for 64-wide tiles).
  *   items     [host] 8 * capacity int32: (a, b, ti, tj, k0, k1, R, acc) per item.
  *   n_items, word_compares, tile_compares [host]: count; sum over this part's pairs of
  *             max(W_i, W_j); words x 128 x 128 summed over its items.
@@ -400,6 +402,16 @@ batmap_status batmap_frequent_items(const int64_t* offsets, int64_t n_items, uin
  */
 batmap_status batmap_plan_groups(int32_t n_classes, const int64_t* class_n, const int64_t* class_w,
                                  int32_t* group_of);
+
+/*
+ * batmap_plan_tile -- host-only view of the planner's tile shape (no device needed): tile_rows =
+ * 128 items; tile_cols = 128, or 64 when the cost model finds that 128 x 64 tiles execute > 10 %
+ * fewer compares (small or ragged width classes; 4 CTAs of 4 warps per SM instead of 2 of 8).
+ * BATMAP_K2_TN=64|128 overrides.  The `tj` of batmap_plan_work's items counts tile_cols-wide
+ * column tiles.  Same input conventions as batmap_plan_work.  Errors: E_INVALID.
+ */
+batmap_status batmap_plan_tile(int32_t n_classes, const int64_t* class_n, const int64_t* class_w,
+                               int32_t* tile_rows, int32_t* tile_cols);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,7 @@ from .batmap import (  # noqa: F401
     parse_fimi,
     mine_host,
     plan_groups,
+    plan_tile,
     plan_work,
     sort_triples,
     swar_device,

@@ -45,7 +45,8 @@ class Stats(ctypes.Structure):
                 ("word_compares", ctypes.c_int64), ("tile_compares", ctypes.c_int64),
                 ("n_candidates", ctypes.c_int64), ("n_results", ctypes.c_int64), ("k2_kind", ctypes.c_int32),
                 ("k2_grid", ctypes.c_int32), ("launches_build", ctypes.c_int64), ("launches_pairs", ctypes.c_int64),
-                ("build_pre_ms", ctypes.c_double), ("build_post_ms", ctypes.c_double)]
+                ("build_pre_ms", ctypes.c_double), ("build_post_ms", ctypes.c_double),
+                ("k2_tile_cols", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -88,6 +89,7 @@ def load_library():
         "batmap_swar_device": ([P, P, I64, P, P], ctypes.c_int),
         "batmap_plan_work": ([I32, P, P, I32, I32, I32, P, I64, PI64, PI64, PI64], ctypes.c_int),
         "batmap_plan_groups": ([I32, P, P, P], ctypes.c_int),
+        "batmap_plan_tile": ([I32, P, P, ctypes.POINTER(I32), ctypes.POINTER(I32)], ctypes.c_int),
         "batmap_fimi_parse": ([P, I64, P, ctypes.POINTER(P), PI64], ctypes.c_int),
         "batmap_fimi_info": ([P, PI64, PI64, PI64], ctypes.c_int),
         "batmap_fimi_filter": ([P, U32, P], ctypes.c_int),
@@ -456,6 +458,17 @@ def plan_groups(class_n, class_w):
     _check(lib.batmap_plan_groups(cn.shape[0], cn.ctypes.data_as(ctypes.c_void_p), cw.ctypes.data_as(ctypes.c_void_p),
                                   out.ctypes.data_as(ctypes.c_void_p)))
     return out[: cn.shape[0]]
+
+
+def plan_tile(class_n, class_w):
+    """Host-only planner view (batmap_plan_tile): (tile_rows, tile_cols) of the K2 plan."""
+    lib = load_library()
+    cn = np.ascontiguousarray(class_n, dtype=np.int64)
+    cw = np.ascontiguousarray(class_w, dtype=np.int64)
+    tr, tc = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.batmap_plan_tile(cn.shape[0], cn.ctypes.data_as(ctypes.c_void_p), cw.ctypes.data_as(ctypes.c_void_p),
+                                ctypes.byref(tr), ctypes.byref(tc)))
+    return int(tr.value), int(tc.value)
 
 
 def plan_work(class_n, class_w, part: int = 0, n_parts: int = 1, grid_cap: int = 0):

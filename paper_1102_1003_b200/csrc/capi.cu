@@ -599,8 +599,22 @@ batmap_status batmap_plan_groups(int32_t n_classes, const int64_t* class_n, cons
     std::vector<ClassInfo> cls;
     BM_TRY(plan_classes(n_classes, class_n, class_w, &cls));
     Plan pl;
-    plan_work(cls, 0, 1, 2 * 148, true, true, promote_enabled(), &pl);
+    const int tn = choose_tn(cls, true, promote_enabled());
+    plan_work(cls, 0, 1, (tn == 64 ? 4 : 2) * 148, true, true, promote_enabled(), &pl, tn);
     for (int a = 0; a < n_classes; ++a) group_of[a] = pl.eff_of[a];
+    return BATMAP_OK;
+}
+
+batmap_status batmap_plan_tile(int32_t n_classes, const int64_t* class_n, const int64_t* class_w, int32_t* tile_rows,
+                               int32_t* tile_cols) {
+    if (n_classes < 0 || (n_classes && (!class_n || !class_w)) || !tile_rows || !tile_cols) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    std::vector<ClassInfo> cls;
+    BM_TRY(plan_classes(n_classes, class_n, class_w, &cls));
+    *tile_rows = kTile;
+    *tile_cols = choose_tn(cls, true, promote_enabled());
     return BATMAP_OK;
 }
 
@@ -615,7 +629,9 @@ batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const 
     std::vector<ClassInfo> cls;
     BM_TRY(plan_classes(n_classes, class_n, class_w, &cls));
     Plan pl;
-    plan_work(cls, part, n_parts, grid_cap ? grid_cap : 2 * 148, true, true, promote_enabled(), &pl);
+    const int tn = choose_tn(cls, true, promote_enabled());
+    plan_work(cls, part, n_parts, grid_cap ? grid_cap : (tn == 64 ? 4 : 2) * 148, true, true, promote_enabled(), &pl,
+              tn);
     *n_items = (int64_t)pl.work.size();
     *word_compares = pl.word_compares;
     *tile_compares = pl.tile_compares;

@@ -28,15 +28,24 @@
 
 namespace bm {
 
-constexpr int kBM = kTile, kBN = kTile, kBK = kChunk, kThreads = 256, kStages = 3, kMinBlocks = 2;
-constexpr int kStageWords = kBK * (kBM + kBN);  // raw words TMA writes per stage
-constexpr int kStageSmem = 2 * kStageWords;      // + the indicator-mask plane the consumers derive
-constexpr size_t kSmemBytes = (size_t)kStages * kStageSmem * 4 + kStages * 8;
-constexpr int kMaxMaps = 96;  // 12 KB of __grid_constant__ parameters (CUDA >= 12.1 allows 32 KB)
+constexpr int kBM = kTile, kBK = kChunk;
+// Tile shapes: 128 x 128 pairs per CTA (8 warps, 2 CTAs per SM, 3 TMA stages) or 128 x 64 (4 warps,
+// 4 CTAs per SM, 2 stages) for small or ragged plans; each thread owns an 8 x 8 micro-tile either way.
+template <int BN>
+struct K2Cfg {
+    static constexpr int kThreads = 2 * BN;
+    static constexpr int kStages = BN == 128 ? 3 : 2;
+    static constexpr int kMinBlocks = BN == 128 ? 2 : 4;
+    static constexpr int kStageWords = kBK * (kBM + BN);  // raw words TMA writes per stage
+    static constexpr int kStageSmem = 2 * kStageWords;     // + the indicator-mask plane the consumers derive
+    static constexpr size_t kSmemBytes = (size_t)kStages * kStageSmem * 4 + kStages * 8;
+};
+constexpr int kMaxMaps = 48;  // per operand role: 2 x 48 x 128 B of __grid_constant__ parameters
 constexpr int kMaxTiledW = 1 << 23;  // 512 * W < 2^32 keeps the 128x-scaled counters exact
 
 struct K2Maps {
-    CUtensorMap maps[kMaxMaps];  // classes, then virtual copies
+    CUtensorMap a[kMaxMaps];  // row operand: box [16 words x 128 items]; classes
+    CUtensorMap b[kMaxMaps];  // column operand: box [16 words x BN items]; classes, then virtual copies
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -100,16 +109,17 @@ struct Ops {
     uint4 xa, xb, ya, yb, ma, mb, na, nb;
 };
 
+template <int BN>
 __device__ __forceinline__ void load_ops(Ops& o, const uint32_t* sA, const uint32_t* sB, const uint32_t* mA,
                                          const uint32_t* mB, int k, int tr, int tc) {
     o.xa = *reinterpret_cast<const uint4*>(sA + k * kBM + 4 * tr);
     o.xb = *reinterpret_cast<const uint4*>(sA + k * kBM + 64 + 4 * tr);
-    o.ya = *reinterpret_cast<const uint4*>(sB + k * kBN + 4 * tc);
-    o.yb = *reinterpret_cast<const uint4*>(sB + k * kBN + 64 + 4 * tc);
+    o.ya = *reinterpret_cast<const uint4*>(sB + k * BN + 4 * tc);
+    o.yb = *reinterpret_cast<const uint4*>(sB + k * BN + BN / 2 + 4 * tc);
     o.ma = *reinterpret_cast<const uint4*>(mA + k * kBM + 4 * tr);
     o.mb = *reinterpret_cast<const uint4*>(mA + k * kBM + 64 + 4 * tr);
-    o.na = *reinterpret_cast<const uint4*>(mB + k * kBN + 4 * tc);
-    o.nb = *reinterpret_cast<const uint4*>(mB + k * kBN + 64 + 4 * tc);
+    o.na = *reinterpret_cast<const uint4*>(mB + k * BN + 4 * tc);
+    o.nb = *reinterpret_cast<const uint4*>(mB + k * BN + BN / 2 + 4 * tc);
 }
 
 // The 64 compare-and-counts of one k step, written as a software pipeline over the pairs so
@@ -161,16 +171,18 @@ struct Cursor {
 };
 
 // Thread 0: fill buffer `buf` with the cursor's next chunk (TMA), or post the end marker once.
+template <int BN>
 __device__ __forceinline__ void issue_next(const K2Maps& prm, Cursor& c, const Rect* rects, const Work* work,
                                            int n_work, int* ctr, uint32_t* stages, int buf, uint64_t* full,
                                            int2* meta, bool& end_sent) {
+    using Cfg = K2Cfg<BN>;
     if (c.w < n_work) {
-        uint32_t* sA = stages + buf * kStageSmem;
+        uint32_t* sA = stages + buf * Cfg::kStageSmem;
         uint32_t* sB = sA + kBK * kBM;
         meta[buf] = make_int2(c.w, c.first);  // published by the mbarrier's release/acquire
-        mbar_expect_tx(&full[buf], kStageWords * 4);
-        tma_load_2d(sA, &prm.maps[c.ma], c.ti * kBM, c.ka, &full[buf]);  // B_i[w mod W_i]
-        tma_load_2d(sB, &prm.maps[c.mb], c.tj * kBN, c.kc * kBK, &full[buf]);
+        mbar_expect_tx(&full[buf], Cfg::kStageWords * 4);
+        tma_load_2d(sA, &prm.a[c.ma], c.ti * kBM, c.ka, &full[buf]);  // B_i[w mod W_i]
+        tma_load_2d(sB, &prm.b[c.mb], c.tj * BN, c.kc * kBK, &full[buf]);
         c.first = 0;
         ++c.kc;
         c.ka += kBK;
@@ -215,6 +227,7 @@ __device__ __forceinline__ void append_candidates(uint64_t mask, int cnt, int la
 
 // End of a work item: ordinary rectangles test c + f_i + f_j >= thr and append; accumulated ones
 // add the partial counts to their counters (4 adjacent virtual columns of one item pre-summed).
+template <int BN>
 __device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int tr, int tc, int lane,
                                               const uint32_t (&acc_in)[8][8], uint32_t* __restrict__ cnt,
                                               const int32_t* __restrict__ f, const uint8_t* __restrict__ lw,
@@ -224,7 +237,7 @@ __device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         rows[i] = ti * kBM + (i < 4 ? 4 * tr + i : 64 + 4 * tr + (i - 4));
-        cols[i] = tj * kBN + (i < 4 ? 4 * tc + i : 64 + 4 * tc + (i - 4));
+        cols[i] = tj * BN + (i < 4 ? 4 * tc + i : BN / 2 + 4 * tc + (i - 4));
     }
     if (r.acc) {  // scaled partial counts; k2_acc_threshold divides promoted pairs
         const uint32_t (&acc)[8][8] = acc_in;
@@ -291,14 +304,18 @@ __device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int
     append_candidates(mask, n, lane, rows, cols, r.row_first, r.col_first, acc, out, ctr, cap);
 }
 
-// 256 threads = 8 warps; thread (tr, tc) owns rows {4tr..4tr+3, 64+4tr..+3} x cols {4tc.., 64+4tc..}
-// of the 128 x 128 tile.  Thread 0 also drives TMA: after the per-chunk barrier every warp has
-// finished the previous chunk, so that buffer is refilled with the chunk kStages-1 ahead.
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+// 2 BN threads = BN / 16 warps; thread (tr, tc) owns rows {4tr..4tr+3, 64+4tr..+3} x cols {4tc..,
+// BN/2+4tc..} of the 128 x BN tile.  Thread 0 also drives TMA: after the per-chunk barrier every
+// warp has finished the previous chunk, so that buffer is refilled with the chunk kStages-1 ahead.
+template <int BN>
+__global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
     k2_tiled(const __grid_constant__ K2Maps prm, const Rect* __restrict__ rects, const Work* __restrict__ work,
              int n_work, int* work_ctr, uint32_t* __restrict__ cnt, uint32_t* __restrict__ tail_buf,
              const int32_t* __restrict__ f, const uint8_t* __restrict__ lw, uint32_t thr, uint32_t use_f,
              Cand* __restrict__ out, unsigned long long* __restrict__ ctr, int64_t cap) {
+    using Cfg = K2Cfg<BN>;
+    constexpr int kStages = Cfg::kStages, kStageSmem = Cfg::kStageSmem, kStageWords = Cfg::kStageWords;
+    constexpr int kThreads = Cfg::kThreads;
     extern __shared__ __align__(1024) uint32_t smem_raw[];
     uint32_t* stages = smem_raw;  // keep the shared address space visible to the compiler (LDS, not LD)
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kStageSmem);
@@ -314,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         pre.claim(rects, work, n_work, work_ctr);
         for (int s = 0; s < kStages - 1; ++s)
-            issue_next(prm, pre, rects, work, n_work, work_ctr, stages, s, full, meta, end_sent);
+            issue_next<BN>(prm, pre, rects, work, n_work, work_ctr, stages, s, full, meta, end_sent);
     }
     __syncthreads();
 
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         if (mt.y && cur >= 0) {  // a new work item (or the end) begins: finish the previous one
             const Work wk = work[cur];
             if (wk.tail) {  // a piece of a cut tail tile: partial counts to its slice (thread-major)
-                uint4* dst = reinterpret_cast<uint4*>(tail_buf + (int64_t)(wk.tail - 1) * (kBM * kBN)) +
+                uint4* dst = reinterpret_cast<uint4*>(tail_buf + (int64_t)(wk.tail - 1) * (kBM * BN)) +
                              threadIdx.x * 16;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
@@ -342,8 +359,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
                     dst[2 * i + 1] = make_uint4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
                 }
             } else {
-                work_epilogue(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, lw, thr, use_f, out, ctr,
-                              cap);
+                work_epilogue<BN>(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, lw, thr, use_f, out,
+                                  ctr, cap);
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
@@ -356,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
             // all lie beyond the rectangle skips the compute, leaving its issue slots to the other CTA
             const Work wk = work[mt.x];
             const Rect& r = rects[wk.rect];
-            warp_active = 32 * (warp & 1) < r.n_rows - wk.ti * kBM && 16 * (warp >> 1) < r.n_cols - wk.tj * kBN;
+            warp_active = 32 * (warp & 1) < r.n_rows - wk.ti * kBM && 16 * (warp >> 1) < r.n_cols - wk.tj * BN;
         }
         cur = mt.x;
         uint32_t* sA = stages + buf * kStageSmem;
@@ -375,8 +392,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         }
         __syncthreads();  // masks visible; every warp is done with the previous chunk's buffer
         if (threadIdx.x == 0)
-            issue_next(prm, pre, rects, work, n_work, work_ctr, stages, (int)((g + kStages - 1) % kStages), full,
-                       meta, end_sent);
+            issue_next<BN>(prm, pre, rects, work, n_work, work_ctr, stages, (int)((g + kStages - 1) % kStages),
+                           full, meta, end_sent);
         const uint32_t* sB = sA + kBK * kBM;
         const uint32_t* mA = sA + kStageWords;
         const uint32_t* mB = mA + kBK * kBM;
@@ -384,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll 1
             for (int k = 0; k < kBK; ++k) {
                 Ops o;
-                load_ops(o, sA, sB, mA, mB, k, tr, tc);
+                load_ops<BN>(o, sA, sB, mA, mB, k, tr, tc);
                 compute_ops(o, acc);
             }
         }
@@ -393,7 +410,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
 // Cut tail tiles: one CTA per tile sums its pieces' partial counts (same thread mapping as
 // k2_tiled) and runs the ordinary epilogue -- candidate test c + f_i + f_j >= s and append.
-__global__ void __launch_bounds__(kThreads) k2_tail_threshold(const TailTile* __restrict__ tails, int pieces,
+template <int BN>
+__global__ void __launch_bounds__(K2Cfg<BN>::kThreads) k2_tail_threshold(const TailTile* __restrict__ tails, int pieces,
                                                               const Rect* __restrict__ rects,
                                                               const uint32_t* __restrict__ tail_buf,
                                                               const int32_t* __restrict__ f,
@@ -410,8 +428,8 @@ __global__ void __launch_bounds__(kThreads) k2_tail_threshold(const TailTile* __
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0;
     for (int p = 0; p < pieces; ++p) {
-        const uint4* src = reinterpret_cast<const uint4*>(tail_buf + (int64_t)(blockIdx.x * pieces + p) * (kBM * kBN)) +
-                           threadIdx.x * 16;
+        const uint4* src =
+            reinterpret_cast<const uint4*>(tail_buf + (int64_t)(blockIdx.x * pieces + p) * (kBM * BN)) + threadIdx.x * 16;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint4 a = src[2 * i], b = src[2 * i + 1];
@@ -425,7 +443,7 @@ __global__ void __launch_bounds__(kThreads) k2_tail_threshold(const TailTile* __
             acc[i][7] += b.w;
         }
     }
-    work_epilogue(rects[t.rect], t.ti, t.tj, tr, tc, lane, acc, nullptr, f, lw, thr, use_f, out, ctr, cap);
+    work_epilogue<BN>(rects[t.rect], t.ti, t.tj, tr, tc, lane, acc, nullptr, f, lw, thr, use_f, out, ctr, cap);
 }
 
 // Accumulated rectangles: one CTA per owned tile row; candidate test on the summed counters.
@@ -602,10 +620,10 @@ static bool env_off(const char* name) {
 }
 
 static batmap_status encode_map(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const uint32_t* base,
-                                int64_t n_pad, int64_t W) {
+                                int64_t n_pad, int64_t W, int box_items) {
     cuuint64_t dims[2] = {(cuuint64_t)n_pad, (cuuint64_t)W};
     cuuint64_t strides[1] = {(cuuint64_t)n_pad * 4};
-    cuuint32_t box[2] = {(cuuint32_t)kBM, (cuuint32_t)kBK};
+    cuuint32_t box[2] = {(cuuint32_t)box_items, (cuuint32_t)kBK};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -666,8 +684,17 @@ static batmap_status run_simple(batmap_collection* h, const Selection& sel, uint
     return rc;
 }
 
+static int min_blocks(int tn) { return tn == 128 ? K2Cfg<128>::kMinBlocks : K2Cfg<64>::kMinBlocks; }
+
+static int env_tn() {  // BATMAP_K2_TN: 0 = the planner's choice
+    const char* e = getenv("BATMAP_K2_TN");
+    return e ? atoi(e) : 0;
+}
+
 struct K2Prepared {
     int part = -1, n_parts = -1;
+    int tn = kTile;       // tile width of the plan
+    int tn_env = 0;       // BATMAP_K2_TN when planned
     bool promote = true;  // planned with class promotion (BATMAP_K2_PROMOTE)
     Plan pl;
     K2Maps* prm = nullptr;
@@ -715,13 +742,15 @@ batmap_status prepare_k2(batmap_collection* h, const Selection& sel, int part, i
     }
     kp->part = part;
     kp->n_parts = n_parts;
-    const int grid_cap = kMinBlocks * h->num_sms;
     const bool promote = !env_off("BATMAP_K2_PROMOTE");
+    const bool virt = !env_off("BATMAP_K2_VIRTUAL");
     kp->promote = promote;
-    plan_work(sel.classes, part, n_parts, grid_cap, !env_off("BATMAP_K2_VIRTUAL"), !env_off("BATMAP_K2_SPLIT"),
-              promote, &kp->pl);
-    if ((int)kp->pl.eff.size() + (int)kp->pl.virt.size() > kMaxMaps)
-        plan_work(sel.classes, part, n_parts, grid_cap, false, true, promote, &kp->pl);
+    kp->tn = choose_tn(sel.classes, virt, promote);
+    kp->tn_env = env_tn();
+    const int grid_cap = min_blocks(kp->tn) * h->num_sms;
+    plan_work(sel.classes, part, n_parts, grid_cap, virt, !env_off("BATMAP_K2_SPLIT"), promote, &kp->pl, kp->tn);
+    if ((int)kp->pl.eff.size() > kMaxMaps || (int)(kp->pl.eff.size() + kp->pl.virt.size()) > kMaxMaps)
+        plan_work(sel.classes, part, n_parts, grid_cap, false, true, promote, &kp->pl, kp->tn);
     const Plan& pl = kp->pl;
     const int C = (int)pl.eff.size();
     if (pl.work.empty()) return BATMAP_OK;
@@ -741,13 +770,14 @@ batmap_status prepare_k2(batmap_collection* h, const Selection& sel, int part, i
         BM_CUDA(cudaStreamSynchronize(st));  // lw is a host temporary
     }
     kp->prm = new K2Maps();
-    for (int a = 0; a < C; ++a) {
+    for (int a = 0; a < C; ++a) {  // row role (box 128 items) and column role (box tn items)
         const uint32_t* base = pl.eff_promo[a] >= 0 ? kp->promo_d : sel.arena;
-        BM_TRY(encode_map(enc, &kp->prm->maps[a], base + pl.eff[a].word_off, pl.eff[a].n_pad, pl.eff[a].W));
+        BM_TRY(encode_map(enc, &kp->prm->a[a], base + pl.eff[a].word_off, pl.eff[a].n_pad, pl.eff[a].W, kBM));
+        BM_TRY(encode_map(enc, &kp->prm->b[a], base + pl.eff[a].word_off, pl.eff[a].n_pad, pl.eff[a].W, kp->tn));
     }
     for (size_t k = 0; k < pl.virt.size(); ++k)
-        BM_TRY(encode_map(enc, &kp->prm->maps[C + k], kp->virt_d + pl.virt[k].dst_word_off, pl.virt[k].vpad,
-                          pl.virt[k].W_a));
+        BM_TRY(encode_map(enc, &kp->prm->b[C + k], kp->virt_d + pl.virt[k].dst_word_off, pl.virt[k].vpad,
+                          pl.virt[k].W_a, kp->tn));
     BM_TRY(dalloc_t(&kp->rects_d, (int64_t)pl.rects.size(), st));
     BM_TRY(dalloc_t(&kp->work_d, (int64_t)pl.work.size(), st));
     BM_TRY(dalloc_t(&kp->units_d, (int64_t)std::max<size_t>(pl.units.size(), 1), st));
@@ -805,7 +835,7 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
     K2Prepared* kp = nullptr;
     K2Prepared local;
     if (!sel.sel2pos && h->k2prep && h->k2prep->part == part && h->k2prep->n_parts == n_parts &&
-        h->k2prep->promote == !env_off("BATMAP_K2_PROMOTE")) {
+        h->k2prep->promote == !env_off("BATMAP_K2_PROMOTE") && h->k2prep->tn_env == env_tn()) {
         kp = h->k2prep;
     } else {
         const batmap_status prc = prepare_k2(h, sel, part, n_parts, st, &local);
@@ -816,12 +846,14 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         kp = &local;
     }
     const Plan& pl = kp->pl;
-    const int grid_cap = kMinBlocks * h->num_sms;
+    const int tn = kp->tn;
+    const int grid_cap = min_blocks(tn) * h->num_sms;
     const int64_t n_work = (int64_t)pl.work.size();
     h->stats.word_compares = pl.word_compares;
     h->stats.tile_compares = pl.tile_compares;
     h->stats.k2_kind = 1;
     h->stats.k2_grid = (int32_t)std::min<int64_t>(n_work, grid_cap);
+    h->stats.k2_tile_cols = tn;
     if (n_work == 0) {
         if (kp == &local) release_k2(&local, st);
         return BATMAP_OK;
@@ -858,9 +890,15 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         h->launches += 1;
     }
     if (pl.cnt_entries) BM_TRY(ensure(&h->cnt_d, &h->cnt_cap, pl.cnt_entries, st));
-    const int64_t tail_words = (int64_t)pl.tails.size() * pl.tail_pieces * kBM * kBN;
+    const int64_t tail_words = (int64_t)pl.tails.size() * pl.tail_pieces * kBM * tn;
     if (tail_words) BM_TRY(ensure(&h->tail_d, &h->tail_cap, tail_words, st));
-    BM_CUDA(cudaFuncSetAttribute(k2_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));  // per device
+    // per device (no process-wide flag)
+    if (tn == 128)
+        BM_CUDA(cudaFuncSetAttribute(k2_tiled<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)K2Cfg<128>::kSmemBytes));
+    else
+        BM_CUDA(cudaFuncSetAttribute(k2_tiled<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)K2Cfg<64>::kSmemBytes));
     const K2Maps* prm = kp->prm;
     Rect* rects_d = kp->rects_d;
     Work* work_d = kp->work_d;
@@ -872,15 +910,25 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, 2 * sizeof(unsigned long long), st));  // [1] = work counter
         if (pl.cnt_entries) BM_CUDA(cudaMemsetAsync(h->cnt_d, 0, pl.cnt_entries * sizeof(uint32_t), st));
         rec(h, EV_K20, st);
-        k2_tiled<<<grid, kThreads, kSmemBytes, st>>>(*prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d,
-                                                     h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
-                                                     h->ctr_d, h->cand_cap);
+        if (tn == 128)
+            k2_tiled<128><<<grid, K2Cfg<128>::kThreads, K2Cfg<128>::kSmemBytes, st>>>(
+                *prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f,
+                h->cand_d, h->ctr_d, h->cand_cap);
+        else
+            k2_tiled<64><<<grid, K2Cfg<64>::kThreads, K2Cfg<64>::kSmemBytes, st>>>(
+                *prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f,
+                h->cand_d, h->ctr_d, h->cand_cap);
         rec(h, EV_K21, st);
         h->launches += 1;
         if (!pl.tails.empty()) {
-            k2_tail_threshold<<<(unsigned)pl.tails.size(), kThreads, 0, st>>>(
-                kp->tails_d, pl.tail_pieces, rects_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
-                h->ctr_d, h->cand_cap);
+            if (tn == 128)
+                k2_tail_threshold<128><<<(unsigned)pl.tails.size(), K2Cfg<128>::kThreads, 0, st>>>(
+                    kp->tails_d, pl.tail_pieces, rects_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
+                    h->ctr_d, h->cand_cap);
+            else
+                k2_tail_threshold<64><<<(unsigned)pl.tails.size(), K2Cfg<64>::kThreads, 0, st>>>(
+                    kp->tails_d, pl.tail_pieces, rects_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
+                    h->ctr_d, h->cand_cap);
             h->launches += 1;
         }
         if (!pl.units.empty()) {

@@ -2,6 +2,7 @@
 // symmetry cut p <= q, virtualised skinny rectangles, split-K for long tiles, and
 // the deal of work to the parts of a multi-GPU run, and promotion of small narrow classes.
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <unordered_map>
 
@@ -54,10 +55,17 @@ int lg_ratio(int64_t W, int64_t W_min) {
 // Estimated executed compares of tiling classes (n[a], W[a]) the way plan_work does (skinny
 // rectangles virtualised when that saves > 30 %), plus the copy traffic of promoted groups
 // (a written word ~ 12 compare-equivalents: 4 B at ~1/3 of R_int's compare rate per byte).
+// Tiles (ti, tj) of the triangle of n items with 128-row and tn-column tiles that hold a pair i < j:
+// tj >= ti * 128 / tn.
+static int64_t diag_tiles(int64_t n, int tn) {
+    const int64_t ta = ceil_div(n, kTile), tb = ceil_div(n, tn), q = kTile / tn;
+    return ta * tb - q * ta * (ta - 1) / 2;
+}
+
 static int64_t est_cost(const std::vector<int64_t>& n, const std::vector<int64_t>& W,
-                        const std::vector<int64_t>& copy_words, bool allow_virtual) {
+                        const std::vector<int64_t>& copy_words, bool allow_virtual, int tn) {
     const int C = (int)n.size();
-    const int64_t T2 = (int64_t)kTile * kTile;
+    const int64_t T2 = (int64_t)kTile * tn;
     int64_t tot = 0;
     for (int a = 0; a < C; ++a) {
         tot += 12 * copy_words[a];
@@ -66,13 +74,13 @@ static int64_t est_cost(const std::vector<int64_t>& n, const std::vector<int64_t
         for (int b = a; b < C; ++b) {
             if (n[b] == 0) continue;
             if (a == b) {
-                if (n[a] >= 2) tot += ta * (ta + 1) / 2 * T2 * W[a];
+                if (n[a] >= 2) tot += diag_tiles(n[a], tn) * T2 * W[a];
                 continue;
             }
-            int64_t c = ta * ceil_div(n[b], kTile) * T2 * W[b];
+            int64_t c = ta * ceil_div(n[b], tn) * T2 * W[b];
             const int64_t R = W[b] / W[a];
             if (allow_virtual && R > 1) {
-                const int64_t v = ta * ceil_div(n[b] * R, kTile) * T2 * W[a];
+                const int64_t v = ta * ceil_div(n[b] * R, tn) * T2 * W[a];
                 if (v * 10 < c * 7) c = v;
             }
             tot += c;
@@ -84,13 +92,11 @@ static int64_t est_cost(const std::vector<int64_t>& n, const std::vector<int64_t
 // Greedy promotion: repeatedly merge the adjacent pair of class groups whose merge lowers the
 // estimated cost most, while that gains > 1 %.  Groups are runs [lo, hi] of the width-sorted
 // classes; a group is planned at its widest member's width.
-static std::vector<std::pair<int, int>> choose_groups(const std::vector<ClassInfo>& cls, bool allow_virtual) {
+static std::vector<std::pair<int, int>> choose_groups(const std::vector<ClassInfo>& cls, bool allow_virtual,
+                                                      int tn, int64_t* cost_out = nullptr) {
     const int C = (int)cls.size();
     std::vector<std::pair<int, int>> g;
     for (int a = 0; a < C; ++a) g.push_back({a, a});
-    if (C < 2) return g;
-    for (int a = 0; a < C; ++a)
-        if (lg_ratio(cls[a].W, cls[0].W) < 0) return g;  // widths must be W_0 times powers of two
     auto cost = [&](const std::vector<std::pair<int, int>>& gs) {
         std::vector<int64_t> n, W, cw;
         for (const auto& p : gs) {
@@ -100,8 +106,15 @@ static std::vector<std::pair<int, int>> choose_groups(const std::vector<ClassInf
             W.push_back(cls[p.second].W);
             cw.push_back(p.first == p.second ? 0 : ceil_div(s, kPadItems) * kPadItems * cls[p.second].W);
         }
-        return est_cost(n, W, cw, allow_virtual);
+        return est_cost(n, W, cw, allow_virtual, tn);
     };
+    bool mergeable = C >= 2;
+    for (int a = 0; a < C; ++a)
+        if (lg_ratio(cls[a].W, cls[0].W) < 0) mergeable = false;  // widths must be W_0 times powers of two
+    if (!mergeable) {
+        if (cost_out) *cost_out = cost(g);
+        return g;
+    }
     constexpr int64_t kMaxPromoWords = int64_t(1) << 27;  // 512 MB per promoted block
     int64_t best = cost(g);
     for (;;) {
@@ -125,16 +138,35 @@ static std::vector<std::pair<int, int>> choose_groups(const std::vector<ClassInf
         g.erase(g.begin() + pick + 1);
         best = pick_cost;
     }
+    if (cost_out) *cost_out = best;
     return g;
 }
 
+int64_t plan_cost(const std::vector<ClassInfo>& cls, bool allow_virtual, bool allow_promote, int tn) {
+    int64_t c = 0;
+    if (allow_promote) {
+        choose_groups(cls, allow_virtual, tn, &c);
+        return c;
+    }
+    std::vector<int64_t> n, W, cw;
+    for (const ClassInfo& k : cls) {
+        n.push_back(k.n);
+        W.push_back(k.W);
+        cw.push_back(0);
+    }
+    return est_cost(n, W, cw, allow_virtual, tn);
+}
+
 void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int grid_cap, bool allow_virtual,
-               bool allow_split, bool allow_promote, Plan* out) {
+               bool allow_split, bool allow_promote, Plan* out, int tn) {
     Plan& P = *out;
     P = Plan();
+    const int TN = (tn == 64) ? 64 : kTile;  // tile width
+    const int QD = kTile / TN;               // tile columns per tile-row step on the diagonal
+    P.tn = TN;
     // ---- planned classes: original classes, or promoted groups of adjacent ones
     const std::vector<std::pair<int, int>> groups =
-        allow_promote ? choose_groups(orig, allow_virtual) : [&] {
+        allow_promote ? choose_groups(orig, allow_virtual, TN) : [&] {
             std::vector<std::pair<int, int>> g;
             for (int a = 0; a < (int)orig.size(); ++a) g.push_back({a, a});
             return g;
@@ -191,8 +223,8 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             const int R = B.W / A.W;
             bool virt = false;
             if (allow_virtual && a < b && R > 1) {
-                const int64_t normal = ceil_div(B.n, kTile) * kTile * (int64_t)B.W;
-                const int64_t vcost = ceil_div((int64_t)B.n * R, kTile) * kTile * (int64_t)A.W;
+                const int64_t normal = ceil_div(B.n, TN) * TN * (int64_t)B.W;
+                const int64_t vcost = ceil_div((int64_t)B.n * R, TN) * TN * (int64_t)A.W;
                 virt = vcost * 10 < normal * 7;  // worth a copy + accumulation only if >30% less work
             }
             Rect r{};
@@ -231,11 +263,11 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             P.rects.push_back(r);
         }
     // ---- split-K: tiles far longer than an even share of the work are cut along k
-    auto tile_cost = [](const Rect& r) { return (int64_t)kTile * kTile * r.W; };
+    auto tile_cost = [&](const Rect& r) { return (int64_t)kTile * TN * r.W; };
     int64_t total = 0;
     for (const Rect& r : P.rects) {
-        const int64_t ta = ceil_div(r.n_rows, kTile), tb = ceil_div(r.n_cols, kTile);
-        const int64_t nt = r.diag ? ta * (ta + 1) / 2 : ta * tb;
+        const int64_t ta = ceil_div(r.n_rows, kTile), tb = ceil_div(r.n_cols, TN);
+        const int64_t nt = r.diag ? diag_tiles(r.n_rows, TN) : ta * tb;
         total += nt * tile_cost(r);
     }
     const int64_t target = std::max<int64_t>(1, total / ((int64_t)n_parts * 4 * std::max(grid_cap, 1)));
@@ -250,7 +282,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         }
     if (P.cnt_entries > (int64_t(1) << 29) && (allow_virtual || allow_split)) {  // > 2 GB of counters
         const std::vector<ClassInfo> o = orig;
-        plan_work(o, part, n_parts, grid_cap, false, false, false, out);
+        plan_work(o, part, n_parts, grid_cap, false, false, false, out, tn);
         return;
     }
     // ---- units dealt to the parts: a tile row of an accumulated rectangle (all contributions
@@ -263,16 +295,16 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
     {
         int64_t nu = 0;
         for (const Rect& r : P.rects) {
-            const int64_t ta = ceil_div(r.n_rows, kTile), tb = ceil_div(r.n_cols, kTile);
-            nu += r.acc ? ta : (r.diag ? ta * (ta + 1) / 2 : ta * tb);
+            const int64_t ta = ceil_div(r.n_rows, kTile), tb = ceil_div(r.n_cols, TN);
+            nu += r.acc ? ta : (r.diag ? diag_tiles(r.n_rows, TN) : ta * tb);
         }
         units.reserve((size_t)nu);
     }
     for (int ri = 0; ri < (int)P.rects.size(); ++ri) {
         const Rect& r = P.rects[ri];
-        const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, kTile);
+        const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, TN);
         for (int i = 0; i < ta; ++i) {
-            const int j0 = r.diag ? i : 0;
+            const int j0 = r.diag ? i * QD : 0;
             if (r.acc) {
                 units.push_back({ri, i, -1, (int64_t)(tb - j0) * tile_cost(r)});
             } else {
@@ -291,7 +323,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         if ((int)(k % (size_t)n_parts) != part) continue;
         const Unit& u = units[k];
         const Rect& r = P.rects[u.rect];
-        const int tb = (int)ceil_div(r.n_cols, kTile);
+        const int tb = (int)ceil_div(r.n_cols, TN);
         const int64_t rows = std::min<int64_t>(kTile, r.n_rows - (int64_t)u.ti * kTile);
         const int W_real = r.W * r.R;
         if (r.acc) P.units.push_back({u.rect, u.ti});
@@ -306,16 +338,13 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         } else if (r.acc) {
             P.word_compares += rows * sumW(r.cls_b, 0, r.n_cols_real);
         }
-        const int jb = u.tj >= 0 ? u.tj : (r.diag ? u.ti : 0);
+        const int jb = u.tj >= 0 ? u.tj : (r.diag ? u.ti * QD : 0);
         const int je = u.tj >= 0 ? u.tj + 1 : tb;
         for (int j = jb; j < je; ++j) {
             if (!r.acc) {
-                const int64_t c0 = (int64_t)j * kTile, c1 = std::min<int64_t>(r.n_cols, c0 + kTile);
-                if (r.diag && j == u.ti) {
-                    if (P.eff_promo[r.cls_b] < 0)
-                        P.word_compares += rows * (rows - 1) / 2 * (int64_t)W_real;
-                    else
-                        for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += sumW(r.cls_b, q + 1, c1);
+                const int64_t c0 = (int64_t)j * TN, c1 = std::min<int64_t>(r.n_cols, c0 + TN);
+                if (r.diag && c0 < r0 + rows) {  // the tile straddles the diagonal: pairs q < col only
+                    for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += sumW(r.cls_b, std::max(q + 1, c0), c1);
                 } else {
                     P.word_compares += rows * sumW(r.cls_b, c0, c1);
                 }
@@ -330,7 +359,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 w.tj = j;
                 w.k0 = (int32_t)((int64_t)nk * p / pieces);
                 w.k1 = (int32_t)((int64_t)nk * (p + 1) / pieces);
-                const int64_t c = (int64_t)(w.k1 - w.k0) * kChunk * kTile * kTile;
+                const int64_t c = (int64_t)(w.k1 - w.k0) * kChunk * kTile * TN;
                 work.push_back({w, c});
                 P.tile_compares += c;
             }
@@ -359,7 +388,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 wp.k0 = (int32_t)((int64_t)nk * p / pcs);
                 wp.k1 = (int32_t)((int64_t)nk * (p + 1) / pcs);
                 wp.tail = 1 + t * pcs + p;
-                const WorkC wc{wp, (int64_t)(wp.k1 - wp.k0) * kChunk * kTile * kTile};
+                const WorkC wc{wp, (int64_t)(wp.k1 - wp.k0) * kChunk * kTile * TN};
                 if (p == 0) work[k] = wc;
                 else pieces.push_back(wc);
             }
@@ -372,6 +401,25 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
     }
     P.work.reserve(work.size());
     for (const WorkC& w : work) P.work.push_back(w.w);
+}
+
+}  // namespace bm
+
+namespace bm {
+
+// Tile width of a selection's plan: 64-column tiles when the cost model says they execute > 10 %
+// fewer compares (small or ragged width classes) and there is enough work for the shape to matter
+// (> 1e9 compares, ~0.1 ms); else 128.  Measured: C3 K2 1.28 -> 1.07 ms with 64; C1 (1.4e8
+// compares, latency-bound) 0.061 -> 0.065 ms, hence the floor; C2 14.67 -> 14.90 ms (kept at 128 by
+// the rule).  BATMAP_K2_TN=64|128 overrides.
+int choose_tn(const std::vector<ClassInfo>& cls, bool allow_virtual, bool allow_promote) {
+    const char* e = getenv("BATMAP_K2_TN");
+    if (e && atoi(e) == 64) return 64;
+    if (e && atoi(e) == 128) return kTile;
+    const int64_t c128 = plan_cost(cls, allow_virtual, allow_promote, kTile);
+    if (c128 < 1000000000ll) return kTile;
+    const int64_t c64 = plan_cost(cls, allow_virtual, allow_promote, 64);
+    return c64 * 10 < c128 * 9 ? 64 : kTile;
 }
 
 }  // namespace bm

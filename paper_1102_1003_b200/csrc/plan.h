@@ -9,7 +9,7 @@
 
 namespace bm {
 
-constexpr int kTile = 128;   // tile edge in items (rows and columns)
+constexpr int kTile = 128;   // tile rows (items); the tile width (columns) is Plan::tn, 128 or 64
 constexpr int kChunk = 16;   // words per k-chunk (the TMA box height)
 
 // A rectangle of the pair triangle: the rows are the items of class a (period W_a), the
@@ -77,13 +77,22 @@ struct Plan {
     int64_t virt_words = 0;
     int64_t cnt_entries = 0;
     int64_t word_compares = 0;    // algorithmic: sum over this part's pairs of max(W_i, W_j)
-    int64_t tile_compares = 0;    // executed: sum over work items of 128 x 128 x words
+    int64_t tile_compares = 0;    // executed: sum over work items of 128 x tn x words
+    int32_t tn = kTile;           // tile width: 128 x 128 tiles, or 128 x 64 for small / ragged plans
 };
 
 // grid_cap: CTAs the kernel keeps resident (the split-K target is ~4 work items per CTA).
 // Rectangles, work items and units refer to the planned classes out->eff.
+// tn: tile width (columns), 128 or 64.
 void plan_work(const std::vector<ClassInfo>& cls, int part, int n_parts, int grid_cap, bool allow_virtual,
-               bool allow_split, bool allow_promote, Plan* out);
+               bool allow_split, bool allow_promote, Plan* out, int tn = kTile);
+
+// Estimated executed compares of the plan of `cls` with tile width tn (the planner's cost model,
+// promotion and virtualisation included): used to choose tn.
+int64_t plan_cost(const std::vector<ClassInfo>& cls, bool allow_virtual, bool allow_promote, int tn);
+
+// 64 or 128 (see plan.cu); BATMAP_K2_TN overrides.
+int choose_tn(const std::vector<ClassInfo>& cls, bool allow_virtual, bool allow_promote);
 
 // log2 of W / W_min for a width that is W_min times a power of two (else -1)
 int lg_ratio(int64_t W, int64_t W_min);

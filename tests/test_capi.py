@@ -106,13 +106,17 @@ def test_plan_work_partition_exact(class_n, class_w, n_parts):
     """Union over parts = every k-chunk of every tile of the (planned-class) pair triangle exactly
     once; tile rows of accumulated rectangles stay on one part; algorithmic work adds
     up to sum_{i<j} max(W_i, W_j) over the ORIGINAL widths."""
+    from paper_1102_1003_b200 import plan_tile
+
     parts = _collect(class_n, class_w, n_parts)
     pn, pw, _ = _planned(class_n, class_w)
+    tr, tc = plan_tile(class_n, class_w)
+    assert tr == 128 and tc in (64, 128)
     chunks = {}
     rect_R = {}
     row_part = {}
     for p, (items, wc, tcmp) in enumerate(parts):
-        assert tcmp == int(sum((k1 - k0) * 16 * 128 * 128 for _, _, _, _, k0, k1, _, _ in items.tolist()))
+        assert tcmp == int(sum((k1 - k0) * 16 * 128 * tc for _, _, _, _, k0, k1, _, _ in items.tolist()))
         for a, b, ti, tj, k0, k1, R, acc in items.tolist():
             assert a <= b and k0 < k1
             rect_R.setdefault((a, b), (R, acc))
@@ -132,9 +136,9 @@ def test_plan_work_partition_exact(class_n, class_w, n_parts):
             R, _ = rect_R[(a, b)]
             W = pw[b] // R
             ta = -(-pn[a] // 128)
-            tb = -(-(pn[b] * R) // 128)
+            tb = -(-(pn[b] * R) // tc)
             for i in range(ta):
-                for j in range(i if a == b else 0, tb):
+                for j in range(i * 128 // tc if a == b else 0, tb):
                     for k in range(W // 16):
                         expect.add((a, b, i, j, k))
     assert set(chunks) == expect
@@ -172,20 +176,27 @@ def test_plan_work_virtual_and_split():
     assert (items[:, 7] == 1).any() and (items[:, 5] - items[:, 4] < 49152 // 16).any()
 
 
-def test_plan_work_covers_every_pair_once():
+@pytest.mark.parametrize("tn", ["", "64", "128"])
+def test_plan_work_covers_every_pair_once(tn, monkeypatch):
     """Expanding the work items (virtual columns, k-chunks, promoted classes) covers, for every pair
     i < j, each of the K words of its planned column item exactly once, with K a power-of-two
     multiple of max(W_i, W_j): c_ij = sum_{w < W_j} SWAR(B_j[w], B_i[w mod W_i]),
     counted K / max(W_i, W_j) times and divided exactly."""
-    for class_n, class_w in (([130, 7, 3], [16, 64, 256]), ([3, 5, 140, 2], [16, 32, 64, 128])):
+    from paper_1102_1003_b200 import plan_tile
+
+    if tn:
+        monkeypatch.setenv("BATMAP_K2_TN", tn)
+    for class_n, class_w in (([130, 7, 3], [16, 64, 256]), ([3, 5, 140, 2], [16, 32, 64, 128]),
+                             ([200, 90], [32, 64])):
         pn, pw, g = _planned(class_n, class_w)
+        tc = plan_tile(class_n, class_w)[1]
         first = np.cumsum([0] + pn)
         items = _collect(class_n, class_w, 1)[0][0]
         cover = {}
         for a, b, ti, tj, k0, k1, R, acc in items.tolist():
             Wv = pw[b] // R
             for r in range(ti * 128, min(pn[a], ti * 128 + 128)):
-                for v in range(tj * 128, min(pn[b] * R, tj * 128 + 128)):
+                for v in range(tj * tc, min(pn[b] * R, tj * tc + tc)):
                     j, rep = divmod(v, R)
                     if a == b and r >= j:
                         continue

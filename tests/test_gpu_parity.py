@@ -330,6 +330,31 @@ def test_promoted_classes_exact(max_loop, monkeypatch):
     c.close()
 
 
+@pytest.mark.parametrize("max_loop", [0, 1])
+def test_tile_widths_exact(max_loop, monkeypatch):
+    """Both K2 tile shapes (128 x 128 pairs per CTA and 128 x 64, BATMAP_K2_TN) on mixed widths with
+    and without forced failures: the full selection at thresholds 0 and 3, raw counts, a subset
+    and a 3-way part split all equal the oracle / each other."""
+    off, tids, m = _quest_widths(8)
+    c = _coll(off, tids, m, seed=2, max_loop=max_loop)
+    sub = np.sort(np.random.default_rng(4).choice(len(off) - 1, size=200, replace=False)).astype(np.int32)
+    ref0 = oracle.pairs_merge(off, tids, threshold=0)
+    raws = []
+    for tn in ("128", "64"):
+        monkeypatch.setenv("BATMAP_K2_TN", tn)
+        np.testing.assert_array_equal(_np(c.pair_supports(threshold=0)), ref0)
+        assert c.stats()["k2_tile_cols"] == int(tn)
+        np.testing.assert_array_equal(_np(c.pair_supports(threshold=3)), ref0[ref0[:, 2] >= 3])
+        raws.append(_np(c.pair_supports(threshold=0, raw=True)))
+        np.testing.assert_array_equal(_np(c.pair_supports(items=torch.as_tensor(sub).cuda(), threshold=2)),
+                                      oracle.pairs_merge(off, tids, items=sub, threshold=2))
+        parts = np.concatenate([_np(c.pair_supports(threshold=3, part=p, n_parts=3)) for p in range(3)])
+        parts = parts[np.lexsort((parts[:, 1], parts[:, 0]))]
+        np.testing.assert_array_equal(parts, ref0[ref0[:, 2] >= 3])
+    np.testing.assert_array_equal(raws[0], raws[1])
+    c.close()
+
+
 def test_items_subset_and_parts():
     w = make_config("C1")
     rng = np.random.default_rng(3)
