@@ -279,6 +279,100 @@ void run_pf(const char* name, const uint32_t* g, int sms, uint32_t* out, unsigne
            name, NT, MINB, per_block * sms / (ms * 1e-3) / 1e12, ms);
 }
 
+// Generalised micro-tile (MI rows x MJ columns per thread), operands and masks from shared memory,
+// the same explicitly pipelined 4-instruction compare.  Smaller micro-tiles need fewer registers,
+// so more warps fit per SM (better ALU-pipe scheduling) at the price of more LDS per compare.
+template <int MI, int MJ>
+__device__ __forceinline__ void step_pipelined_mt(const uint32_t (&x)[MI], const uint32_t (&y)[MJ],
+                                                  const uint32_t (&xm)[MI], const uint32_t (&ym)[MJ],
+                                                  uint32_t (&acc)[MI][MJ]) {
+    constexpr int N = MI * MJ;
+    uint32_t u[N], p[N], v[N];
+#pragma unroll
+    for (int q = 0; q < N + 3; ++q) {
+        if (q < N) asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[q]) : "r"(x[q / MJ]), "r"(y[q % MJ]));
+        if (q >= 1 && q - 1 < N) asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - 1]) : "r"(u[q - 1]));
+        if (q >= 2 && q - 2 < N)
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;"
+                         : "=r"(v[q - 2])
+                         : "r"(p[q - 2]), "r"(xm[(q - 2) / MJ]), "r"(ym[(q - 2) % MJ]));
+        if (q >= 3) asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;" : "+r"(acc[(q - 3) / MJ][(q - 3) % MJ]) : "r"(v[q - 3]));
+    }
+}
+
+template <int MI, int MJ, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) bench_mt(const uint32_t* __restrict__ g, int reps, uint32_t* out) {
+    // a 16 x RB row block and 16 x CB column block of words; each thread reads MI/4 (resp. MJ/4)
+    // consecutive 4-word groups with LDS.128
+    constexpr int TR = 16, TC = NT / TR;  // thread grid
+    constexpr int RB = TR * MI, CB = TC * MJ;
+    __shared__ __align__(16) uint32_t sA[16 * RB], sB[16 * CB], mA[16 * RB], mB[16 * CB];
+    for (int i = threadIdx.x; i < 16 * RB; i += NT) {
+        sA[i] = g[i % 4096];
+        mA[i] = sA[i] & 0x80808080u;
+    }
+    for (int i = threadIdx.x; i < 16 * CB; i += NT) {
+        sB[i] = g[4096 + i % 4096];
+        mB[i] = sB[i] & 0x80808080u;
+    }
+    __syncthreads();
+    const int tr = threadIdx.x % TR, tc = threadIdx.x / TR;
+    uint32_t acc[MI][MJ];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < MJ; ++j) acc[i][j] = 0;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int k = 0; k < 16; ++k) {
+            uint32_t x[MI], y[MJ], xm[MI], ym[MJ];
+#pragma unroll
+            for (int h = 0; h < MI / 4; ++h) {
+                const uint4 a = *reinterpret_cast<const uint4*>(sA + k * RB + h * (RB / (MI / 4)) + 4 * tr);
+                const uint4 b = *reinterpret_cast<const uint4*>(mA + k * RB + h * (RB / (MI / 4)) + 4 * tr);
+                x[4 * h] = a.x; x[4 * h + 1] = a.y; x[4 * h + 2] = a.z; x[4 * h + 3] = a.w;
+                xm[4 * h] = b.x; xm[4 * h + 1] = b.y; xm[4 * h + 2] = b.z; xm[4 * h + 3] = b.w;
+            }
+#pragma unroll
+            for (int h = 0; h < MJ / 4; ++h) {
+                const uint4 a = *reinterpret_cast<const uint4*>(sB + k * CB + h * (CB / (MJ / 4)) + 4 * tc);
+                const uint4 b = *reinterpret_cast<const uint4*>(mB + k * CB + h * (CB / (MJ / 4)) + 4 * tc);
+                y[4 * h] = a.x; y[4 * h + 1] = a.y; y[4 * h + 2] = a.z; y[4 * h + 3] = a.w;
+                ym[4 * h] = b.x; ym[4 * h + 1] = b.y; ym[4 * h + 2] = b.z; ym[4 * h + 3] = b.w;
+            }
+            step_pipelined_mt<MI, MJ>(x, y, xm, ym, acc);
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < MJ; ++j) s += acc[i][j] * (i * MJ + j + 1);
+    out[blockIdx.x * NT + threadIdx.x] = s;
+}
+
+template <int MI, int MJ, int NT, int MINB>
+void run_mt(const char* name, const uint32_t* g, int sms, uint32_t* out) {
+    const int reps = 2000;
+    const int blocks = sms * MINB;
+    bench_mt<MI, MJ, NT, MINB><<<blocks, NT>>>(g, 10, out);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    bench_mt<MI, MJ, NT, MINB><<<blocks, NT>>>(g, reps, out);
+    cudaEventRecord(e1);
+    CK(cudaDeviceSynchronize());
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double cmps = (double)blocks * NT * MI * MJ * 16.0 * reps;
+    const double tcmp = cmps / (ms * 1e-3) / 1e12;
+    printf("{\"variant\": \"%s\", \"micro_tile\": \"%dx%d\", \"threads\": %d, \"ctas_per_sm\": %d, "
+           "\"tcmp_per_s\": %.3f, \"frac_of_R_int_at_1965MHz\": %.3f, \"ms\": %.2f}\n",
+           name, MI, MJ, NT, MINB, tcmp, tcmp / (32.0 * sms * 1.965e9 / 1e12), ms);
+}
+
 int main() {
     int sms;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -305,5 +399,11 @@ int main() {
     run<5, 1, 512, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
     run<5, 1, 256, 2, 1, 1>("pipelined_volatile/masks_from_smem+sync", g, sms, out, cyc);
     run<4, 1, 256, 2, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run_mt<8, 8, 256, 2>("mt_pipelined/masks_from_smem", g, sms, out);
+    run_mt<8, 4, 256, 3>("mt_pipelined/masks_from_smem", g, sms, out);
+    run_mt<4, 8, 256, 3>("mt_pipelined/masks_from_smem", g, sms, out);
+    run_mt<8, 4, 128, 6>("mt_pipelined/masks_from_smem", g, sms, out);
+    run_mt<4, 4, 256, 4>("mt_pipelined/masks_from_smem", g, sms, out);
+    run_mt<4, 4, 512, 2>("mt_pipelined/masks_from_smem", g, sms, out);
     return 0;
 }
