@@ -446,35 +446,59 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads) k2_tail_threshold(const T
     work_epilogue<BN>(rects[t.rect], t.ti, t.tj, tr, tc, lane, acc, nullptr, f, lw, thr, use_f, out, ctr, cap);
 }
 
-// Accumulated rectangles: one CTA per owned tile row; candidate test on the summed counters.
-__global__ void __launch_bounds__(256) k2_acc_threshold(const AccUnit* __restrict__ units,
+// Accumulated rectangles: the counters of every owned tile row, spread over a 2-D grid (y: tile
+// row, x: chunks of its 128 x n_cols counters, columns fastest: coalesced), candidate test on the
+// summed counts, one output cursor atomic per warp.  (One CTA per tile row took 235 us on C1,
+// whose whole diagonal rectangle is split along k: 8 tile rows x 128 x 998 counters.)
+constexpr int kAccPerThread = 8;
+__global__ void __launch_bounds__(256) k2_acc_threshold(const AccUnit* __restrict__ units, int n_units,
                                                         const Rect* __restrict__ rects,
                                                         const uint32_t* __restrict__ cnt,
                                                         const int32_t* __restrict__ f,
                                                         const uint8_t* __restrict__ lw, uint32_t thr, uint32_t use_f,
                                                         Cand* __restrict__ out, unsigned long long* __restrict__ ctr,
                                                         int64_t cap) {
-    const AccUnit u = units[blockIdx.x];
-    const Rect r = rects[u.rect];
-    const int r0 = u.ti * kTile;
-    const int nr = min(kTile, r.n_rows - r0);
-    const int64_t total = (int64_t)nr * r.n_cols_real;
-    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-        const int row = r0 + (int)(e / r.n_cols_real);
-        const int col = (int)(e % r.n_cols_real);
-        if (r.diag && col <= row) continue;
-        uint32_t c = cnt[r.cnt_off + (int64_t)row * r.n_cols_real + col];
-        if (r.promo) c >>= r.lgK - max((int)lw[r.row_first + row], (int)lw[r.col_first + col]);
-        uint64_t t = c;
-        if (use_f) t += (uint32_t)f[r.row_first + row] + (uint32_t)f[r.col_first + col];
-        if (t >= thr) {
-            const unsigned long long at = atomicAdd(ctr, 1ull);
-            if ((int64_t)at < cap) {
-                Cand cd;
-                cd.i = (uint32_t)(r.row_first + row);
-                cd.j = (uint32_t)(r.col_first + col);
-                cd.c = c;
-                out[at] = cd;
+    const int lane = threadIdx.x & 31;
+    for (int ui = blockIdx.y; ui < n_units; ui += gridDim.y) {
+        const AccUnit u = units[ui];
+        const Rect& r = rects[u.rect];
+        const int r0 = u.ti * kTile;
+        const int nr = min(kTile, r.n_rows - r0);
+        const int ncol = r.n_cols_real;
+        const int total = nr * ncol;
+        // warp-uniform trip count (ballots below)
+        for (int base = blockIdx.x * blockDim.x * kAccPerThread; base < total;
+             base += gridDim.x * blockDim.x * kAccPerThread) {
+#pragma unroll
+            for (int q = 0; q < kAccPerThread; ++q) {
+                const int e = base + q * blockDim.x + threadIdx.x;
+                bool take = false;
+                int row = 0, col = 0;
+                uint32_t c = 0;
+                if (e < total) {
+                    row = r0 + e / ncol;
+                    col = e - (e / ncol) * ncol;
+                    if (!r.diag || col > row) {
+                        c = cnt[r.cnt_off + (int64_t)row * ncol + col];
+                        if (r.promo) c >>= r.lgK - max((int)lw[r.row_first + row], (int)lw[r.col_first + col]);
+                        uint64_t t = c;
+                        if (use_f) t += (uint32_t)f[r.row_first + row] + (uint32_t)f[r.col_first + col];
+                        take = t >= thr;
+                    }
+                }
+                const unsigned mask = __ballot_sync(0xFFFFFFFFu, take);
+                if (!mask) continue;
+                unsigned long long at = 0;
+                const int leader = __ffs(mask) - 1;
+                if (lane == leader) at = atomicAdd(ctr, (unsigned long long)__popc(mask));
+                at = __shfl_sync(0xFFFFFFFFu, at, leader) + __popc(mask & ((1u << lane) - 1));
+                if (take && (int64_t)at < cap) {
+                    Cand cd;
+                    cd.i = (uint32_t)(r.row_first + row);
+                    cd.j = (uint32_t)(r.col_first + col);
+                    cd.c = c;
+                    out[at] = cd;
+                }
             }
         }
     }
@@ -932,9 +956,15 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
             h->launches += 1;
         }
         if (!pl.units.empty()) {
-            k2_acc_threshold<<<(unsigned)pl.units.size(), 256, 0, st>>>(units_d, rects_d, h->cnt_d, sel.f, kp->lw_d,
-                                                                        threshold, use_f, h->cand_d, h->ctr_d,
-                                                                        h->cand_cap);
+            int64_t most = 1;  // counters of the largest owned tile row
+            for (const AccUnit& u : pl.units) {
+                const Rect& r = pl.rects[u.rect];
+                most = std::max<int64_t>(most, (int64_t)std::min(kTile, r.n_rows - u.ti * kTile) * r.n_cols_real);
+            }
+            const dim3 g((unsigned)std::min<int64_t>((most + 256 * kAccPerThread - 1) / (256 * kAccPerThread), 1024),
+                         (unsigned)std::min<size_t>(pl.units.size(), 65535));
+            k2_acc_threshold<<<g, 256, 0, st>>>(units_d, (int)pl.units.size(), rects_d, h->cnt_d, sel.f, kp->lw_d,
+                                                threshold, use_f, h->cand_d, h->ctr_d, h->cand_cap);
             h->launches += 1;
         }
         cudaError_t le = cudaGetLastError();
