@@ -495,10 +495,11 @@ __global__ void k_fill_padding(uint32_t* __restrict__ arena_cls, int n, int n_pa
 }
 
 // fail_off[p] = first index of position p in the sorted (pos << 32 | tid) list; f[p] = its count
-__global__ void k_fail_offsets(const uint64_t* __restrict__ keys, int64_t F, int64_t n, int64_t* __restrict__ off,
-                               int32_t* __restrict__ f) {
+__global__ void k_fail_offsets(const uint64_t* __restrict__ keys, const int* __restrict__ F_d, int64_t n,
+                               int64_t* __restrict__ off, int32_t* __restrict__ f) {
     int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p > n) return;
+    const int64_t F = *F_d;  // deduplicated count (device: no host round trip)
     auto lb = [&](uint64_t key) {
         int64_t lo = 0, hi = F;
         while (lo < hi) {
@@ -513,10 +514,10 @@ __global__ void k_fail_offsets(const uint64_t* __restrict__ keys, int64_t F, int
     if (p < n) f[p] = (int32_t)(lb((uint64_t)(p + 1) << 32) - a);
 }
 
-__global__ void k_fail_split(const uint64_t* __restrict__ keys, int64_t F, int32_t* __restrict__ tid,
+__global__ void k_fail_split(const uint64_t* __restrict__ keys, const int* __restrict__ F_d, int32_t* __restrict__ tid,
                              int32_t* __restrict__ mark, uint32_t* __restrict__ fbits) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= F) return;
+    if (i >= *F_d) return;
     uint32_t t = (uint32_t)keys[i];
     tid[i] = (int32_t)t;
     mark[t] = 1;
@@ -704,14 +705,11 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
         BM_CUDA(cub::DeviceSelect::Unique(h->cub_tmp, tb, sorted, uniq, n_uniq_d, (int)F, st));
         h->launches += 1;
     }
-    int n_uniq = 0;
-    BM_CUDA(cudaMemcpyAsync(&n_uniq, n_uniq_d, sizeof(int), cudaMemcpyDeviceToHost, st));
-    BM_CUDA(cudaStreamSynchronize(st));
-    F = n_uniq;
-    h->n_fail = F;
+    // every size below is bounded by F (before deduplication); the exact counts stay on the device
+    // until the one synchronisation before the A_b sort
     std::swap(sorted, uniq);
     // per-item offsets and counts from the deduplicated list
-    k_fail_offsets<<<grid_for(n + 1, 256), 256, 0, st>>>(sorted, F, n, h->fail_off_d, h->f_d);
+    k_fail_offsets<<<grid_for(n + 1, 256), 256, 0, st>>>(sorted, n_uniq_d, n, h->fail_off_d, h->f_d);
     h->launches += 1;
     BM_TRY(dalloc_t(&h->fail_tid_d, F, st));
     int32_t *mark = nullptr, *rank = nullptr;
@@ -721,7 +719,7 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     BM_TRY(dalloc_t(&mark, m + 1, st));
     BM_TRY(dalloc_t(&rank, m + 1, st));
     BM_CUDA(cudaMemsetAsync(mark, 0, (m + 1) * sizeof(int32_t), st));
-    k_fail_split<<<grid_for(F, 256), 256, 0, st>>>(sorted, F, h->fail_tid_d, mark, fbits);
+    k_fail_split<<<grid_for(F, 256), 256, 0, st>>>(sorted, n_uniq_d, h->fail_tid_d, mark, fbits);
     h->launches += 1;
     {
         size_t tb = 0;
@@ -732,31 +730,33 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     }
     k_fidx<<<grid_for(m, 256), 256, 0, st>>>(mark, rank, m, h->fidx_of_tid_d);
     h->launches += 1;
-    int32_t nft = 0;
-    BM_CUDA(cudaMemcpyAsync(&nft, rank + m, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    BM_CUDA(cudaStreamSynchronize(st));
-    h->n_ftid = nft;
-    // A_b: counts per failed tid, then (fidx, pos) keys sorted
+    // A_b: counts per failed tid (index < nft <= F; the rest stay 0), then (fidx, pos) keys sorted
     unsigned long long* cnt = nullptr;
-    BM_TRY(dalloc_t(&cnt, nft + 1, st));
-    BM_CUDA(cudaMemsetAsync(cnt, 0, (nft + 1) * sizeof(unsigned long long), st));
+    BM_TRY(dalloc_t(&cnt, F + 1, st));
+    BM_CUDA(cudaMemsetAsync(cnt, 0, (F + 1) * sizeof(unsigned long long), st));
     // one 128-entry step per warp: every gather chain and hit's binary search runs in parallel
     const unsigned scan_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(nnz, 1024), 1 << 30));
     k_ab_scan<false><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, fbits, cnt, nullptr,
                                                 nullptr);
     h->launches += 1;
-    BM_TRY(dalloc_t(&h->ab_off_d, nft + 1, st));
+    BM_TRY(dalloc_t(&h->ab_off_d, F + 1, st));
     {
         int64_t* c64 = reinterpret_cast<int64_t*>(cnt);
         size_t tb = 0;
-        BM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c64, h->ab_off_d, (int)(nft + 1), st));
+        BM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c64, h->ab_off_d, (int)(F + 1), st));
         BM_TRY(cub_tmp(h, tb, st));
-        BM_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp, tb, c64, h->ab_off_d, (int)(nft + 1), st));
+        BM_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp, tb, c64, h->ab_off_d, (int)(F + 1), st));
         h->launches += 1;
     }
+    int n_uniq = 0;
+    int32_t nft = 0;
     int64_t total = 0;
-    BM_CUDA(cudaMemcpyAsync(&total, h->ab_off_d + nft, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(&n_uniq, n_uniq_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(&nft, rank + m, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(&total, h->ab_off_d + F, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     BM_CUDA(cudaStreamSynchronize(st));
+    h->n_fail = n_uniq;
+    h->n_ftid = nft;
     uint64_t *keys = nullptr, *keys2 = nullptr;
     unsigned long long* cursor = nullptr;
     BM_TRY(dalloc_t(&keys, total, st));
