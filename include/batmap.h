@@ -388,6 +388,18 @@ batmap_status batmap_frequent_items(const int64_t* offsets, int64_t n_items, uin
                                     int32_t* items_out, int64_t* n_out, batmap_stream_t stream);
 
 /*
+ * batmap_select_csr -- the vertical database restricted to the items `items` (in that order; e.g.
+ * the output of batmap_frequent_items): offsets_out [device, n_sel + 1] is always written;
+ * tids_out [device, tids_capacity] receives the selected tidlists back to back.  *nnz_out [host] =
+ * their total length; if it exceeds tids_capacity the call returns E_CAPACITY after writing
+ * offsets_out (two-call protocol).  `items` are ids in [0, n_items) (not validated; duplicates are
+ * copied twice).  Synchronises `stream` once.  Errors: E_INVALID, E_CAPACITY, E_NOMEM, E_CUDA.
+ */
+batmap_status batmap_select_csr(const int64_t* offsets, const int32_t* tids, int64_t n_items, const int32_t* items,
+                                int64_t n_sel, int64_t* offsets_out, int32_t* tids_out, int64_t tids_capacity,
+                                int64_t* nnz_out, batmap_stream_t stream);
+
+/*
  * batmap_plan_groups -- host-only view of the planner's class promotion (no device needed).  The
  * planner may merge a run of adjacent width classes (typically small, narrow ones whose own
  * 128 x 128 tiles would be mostly padding) into ONE planned class of the widest member's width W:

@@ -17,6 +17,7 @@ from .batmap import (  # noqa: F401
     plan_groups,
     plan_tile,
     plan_work,
+    select_csr,
     sort_triples,
     swar_device,
     version,

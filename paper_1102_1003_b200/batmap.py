@@ -96,6 +96,7 @@ def load_library():
         "batmap_fimi_export": ([P, P, P, P, P], ctypes.c_int),
         "batmap_fimi_destroy": ([P], None),
         "batmap_frequent_items": ([P, I64, U32, P, PI64, P], ctypes.c_int),
+        "batmap_select_csr": ([P, P, I64, P, I64, P, P, I64, PI64, P], ctypes.c_int),
         "batmap_stats": ([P, ctypes.POINTER(Stats)], ctypes.c_int),
         "batmap_sort_triples": ([P, I64, P], ctypes.c_int),
         "batmap_dense_pair_supports": ([P, P, I64, I64, P, I64, U32, P, I64, PI64, ctypes.POINTER(ctypes.c_double), P],
@@ -430,6 +431,26 @@ def frequent_items(offsets, min_support: int, *, stream=None):
     _check(lib.batmap_frequent_items(_dptr(offsets), n, int(min_support), _dptr(out), ctypes.byref(k),
                                      _stream_ptr(stream)))
     return out[: k.value]
+
+
+def select_csr(offsets, tids, items, *, stream=None):
+    """batmap_select_csr: (offsets int64, tids int32) CUDA tensors of the tidlists of `items`."""
+    import torch
+
+    lib = load_library()
+    offsets = offsets.to(device="cuda", dtype=torch.int64).contiguous()
+    tids = tids.to(device="cuda", dtype=torch.int32).contiguous()
+    it = torch.as_tensor(items).to(device="cuda", dtype=torch.int32).contiguous()
+    n_sel = it.numel()
+    off_out = torch.empty(n_sel + 1, dtype=torch.int64, device="cuda")
+    nnz = ctypes.c_int64(0)
+    rc = lib.batmap_select_csr(_dptr(offsets), _dptr(tids), offsets.numel() - 1, _dptr(it), n_sel, _dptr(off_out),
+                               None, 0, ctypes.byref(nnz), _stream_ptr(stream))
+    _check(rc, ok=(BATMAP_OK, BATMAP_E_CAPACITY))
+    out = torch.empty(max(nnz.value, 1), dtype=torch.int32, device="cuda")
+    _check(lib.batmap_select_csr(_dptr(offsets), _dptr(tids), offsets.numel() - 1, _dptr(it), n_sel, _dptr(off_out),
+                                 _dptr(out), out.numel(), ctypes.byref(nnz), _stream_ptr(stream)))
+    return off_out, out[: nnz.value]
 
 
 def mine_fimi(text, threshold: int, **build_kw) -> np.ndarray:

@@ -13,6 +13,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbatmap.so")
+CLI_SRC = os.path.join(HERE, "cli", "batmap_mine.cpp")
+CLI = os.path.join(HERE, "batmap_mine")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -37,6 +39,7 @@ def up_to_date() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
+        build_cli()
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
@@ -62,7 +65,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    build_cli(force=True)
     return LIB
+
+
+def build_cli(force: bool = False) -> str:
+    """The command-line miner (cli/batmap_mine.cpp): C ABI + CUDA runtime only, rpath to the library."""
+    if not force and os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(CLI_SRC),
+                                                                          os.path.getmtime(LIB)):
+        return CLI
+    tmp = CLI + f".tmp{os.getpid()}"
+    cmd = [NVCC, "-O2", "-std=c++17", "-I" + INCLUDE, CLI_SRC, "-o", tmp, "-L" + HERE, "-lbatmap",
+           "-Xlinker", "-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"batmap_mine build failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, CLI)
+    return CLI
 
 
 if __name__ == "__main__":

@@ -566,6 +566,19 @@ batmap_status batmap_frequent_items(const int64_t* offsets, int64_t n_items, uin
     return frequent_items(offsets, n_items, min_support, items_out, n_out, reinterpret_cast<cudaStream_t>(stream));
 }
 
+batmap_status batmap_select_csr(const int64_t* offsets, const int32_t* tids, int64_t n_items, const int32_t* items,
+                                int64_t n_sel, int64_t* offsets_out, int32_t* tids_out, int64_t tids_capacity,
+                                int64_t* nnz_out, batmap_stream_t stream) {
+    if (!nnz_out || !offsets_out || n_items < 0 || n_sel < 0 || (n_sel && (!offsets || !tids || !items)) ||
+        tids_capacity < 0 || (tids_capacity && !tids_out)) {
+        set_error("bad arguments");
+        return BATMAP_E_INVALID;
+    }
+    init_pool();
+    return select_csr(offsets, tids, items, n_sel, offsets_out, tids_out, tids_capacity, nnz_out,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
 static bool promote_enabled() {
     const char* e = getenv("BATMAP_K2_PROMOTE");
     return !(e && e[0] == '0');

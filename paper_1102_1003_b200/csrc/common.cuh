@@ -260,6 +260,9 @@ batmap_status fimi_parse(const uint8_t* text, int64_t n, cudaStream_t st, batmap
 batmap_status fimi_filter(batmap_fimi* h, uint32_t min_support, cudaStream_t st);
 batmap_status frequent_items(const int64_t* off, int64_t n_items, uint32_t min_support, int32_t* items_out,
                              int64_t* n_out, cudaStream_t st);
+batmap_status select_csr(const int64_t* off, const int32_t* tids, const int32_t* items, int64_t n_sel,
+                         int64_t* offsets_out, int32_t* tids_out, int64_t tids_capacity, int64_t* nnz_out,
+                         cudaStream_t st);
 // dense.cu
 batmap_status dense_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t m,
                                   const int32_t* items, int64_t n_sel, uint32_t threshold, batmap_triple* out,

@@ -219,8 +219,9 @@ __global__ void k_gather_lists(const int64_t* __restrict__ off, const int32_t* _
         const int32_t i = __ldg(items + lo);
         new_tids[e] = __ldg(tids + __ldg(off + i) + (e - __ldg(new_off + lo)));
     }
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_sel; k += (int64_t)gridDim.x * blockDim.x)
-        new_labels[k] = labels[items[k]];
+    if (labels)
+        for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_sel; k += (int64_t)gridDim.x * blockDim.x)
+            new_labels[k] = labels[items[k]];
 }
 
 static int bits_for(uint64_t v) {  // bits needed to represent 0..v
@@ -473,6 +474,49 @@ batmap_status fimi_filter(batmap_fimi* h, uint32_t min_support, cudaStream_t st)
     new_tids = nullptr;
     new_labels = nullptr;
     return fail(BATMAP_OK);
+}
+
+// The vertical database restricted to `items` (in the given order): offsets_out [n_sel + 1] and,
+// when it fits, tids_out; *nnz_out = the selected entries.  One synchronisation (the size).
+batmap_status select_csr(const int64_t* off, const int32_t* tids, const int32_t* items, int64_t n_sel,
+                         int64_t* offsets_out, int32_t* tids_out, int64_t tids_capacity, int64_t* nnz_out,
+                         cudaStream_t st) {
+    int64_t* sizes = nullptr;
+    void* tmp = nullptr;
+    BM_TRY(dalloc_t(&sizes, n_sel + 1, st));
+    batmap_status rc = BATMAP_OK;
+    size_t need = 0;
+    if (cudaMemsetAsync(sizes + n_sel, 0, sizeof(int64_t), st) != cudaSuccess) rc = BATMAP_E_CUDA;
+    if (rc == BATMAP_OK && n_sel)
+        k_gather_sizes<<<(unsigned)((n_sel + 255) / 256), 256, 0, st>>>(off, items, n_sel, sizes);
+    if (rc == BATMAP_OK) {
+        cub::DeviceScan::ExclusiveSum(nullptr, need, sizes, offsets_out, n_sel + 1, st);
+        rc = dalloc(&tmp, need, st);
+    }
+    if (rc == BATMAP_OK && cub::DeviceScan::ExclusiveSum(tmp, need, sizes, offsets_out, n_sel + 1, st) != cudaSuccess)
+        rc = BATMAP_E_CUDA;
+    int64_t nnz = 0;
+    if (rc == BATMAP_OK &&
+        (cudaMemcpyAsync(&nnz, offsets_out + n_sel, sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+         cudaStreamSynchronize(st) != cudaSuccess))
+        rc = BATMAP_E_CUDA;
+    dfree(sizes, st);
+    dfree(tmp, st);
+    if (rc != BATMAP_OK) {
+        set_error("select_csr: %s", cudaGetErrorString(cudaGetLastError()));
+        return rc;
+    }
+    *nnz_out = nnz;
+    if (nnz > tids_capacity) {
+        set_error("capacity %lld < %lld tids", (long long)tids_capacity, (long long)nnz);
+        return BATMAP_E_CAPACITY;
+    }
+    if (n_sel && nnz) {
+        const unsigned g = (unsigned)std::min<int64_t>((nnz + 255) / 256, 148 * 16);
+        k_gather_lists<<<g, 256, 0, st>>>(off, tids, nullptr, items, n_sel, offsets_out, nnz, tids_out, nullptr);
+        BM_CUDA(cudaGetLastError());
+    }
+    return BATMAP_OK;
 }
 
 }  // namespace bm

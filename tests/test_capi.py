@@ -223,3 +223,17 @@ def test_plan_work_covers_every_pair_once(tn, monkeypatch):
             assert cnt == K and K % max(width[i], width[j]) == 0
             q = K // max(width[i], width[j])
             assert q & (q - 1) == 0
+
+
+def test_cli_builds_and_prints_usage():
+    """The native command-line miner (cli/batmap_mine.cpp, C ABI only) is built next to the library
+    and links it; without arguments it prints its usage and exits 2 (no device touched)."""
+    import subprocess
+
+    from paper_1102_1003_b200 import build_ext
+
+    exe = build_ext.build_cli()
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 2 and "usage" in r.stderr
+    r = subprocess.run([exe, "/nonexistent.dat", "0"], capture_output=True, text=True)
+    assert r.returncode == 2  # min_support 0 rejected before any I/O

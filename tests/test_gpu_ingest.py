@@ -108,3 +108,49 @@ def test_kosarak_shaped_round_trip():
     np.testing.assert_array_equal(lab, keep.astype(np.uint32))
     np.testing.assert_array_equal(off, fo)
     np.testing.assert_array_equal(tids, ft)
+
+
+def test_cli_mines_a_fimi_file(tmp_path):
+    """batmap_mine <file> <s> (native, C ABI only) prints exactly the oracle's frequent pairs as
+    "label_i label_j support" lines."""
+    import subprocess
+
+    from paper_1102_1003_b200 import build_ext
+
+    w = make_config("C1")
+    labels = np.arange(w.n, dtype=np.int64) * 11 + 3
+    path = tmp_path / "c1.dat"
+    path.write_bytes(fimi_text(w.offsets, w.tids, w.m, labels=labels, seed=2, messy=True))
+    r = subprocess.run([build_ext.build_cli(), str(path), str(w.threshold), "--seed", "3"], capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    got = np.array([list(map(int, ln.split())) for ln in r.stdout.splitlines()], dtype=np.int64).reshape(-1, 3)
+    ro, rt, rl, _ = parse_fimi(path.read_bytes())
+    ref = oracle.pairs_horizontal(ro, rt, w.m, threshold=w.threshold).astype(np.int64)
+    ref[:, 0] = rl[ref[:, 0]]
+    ref[:, 1] = rl[ref[:, 1]]
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_select_csr_and_prefiltered_mining():
+    """batmap_frequent_items + batmap_select_csr on a Zipf database: the selected CSR equals
+    the oracle's restriction, and mining it gives exactly the unfiltered frequent pairs (no pair with
+    support >= s contains an infrequent item)."""
+    from paper_1102_1003_b200 import Collection, frequent_items as gpu_frequent, select_csr
+
+    off, tids = zipf(4000, 6000, seed=12)
+    s = 15
+    keep = gpu_frequent(torch.as_tensor(off).cuda(), s)
+    ko, kt = select_csr(torch.as_tensor(off).cuda(), torch.as_tensor(tids).cuda(), keep)
+    ref_keep = frequent_items(off, s)
+    np.testing.assert_array_equal(keep.cpu().numpy(), ref_keep)
+    fo, ft = filter_csr(off, tids, ref_keep)
+    np.testing.assert_array_equal(ko.cpu().numpy(), fo)
+    np.testing.assert_array_equal(kt.cpu().numpy(), ft)
+    with Collection(ko, kt, 6000, seed=1) as c:
+        got = c.pair_supports(threshold=s).cpu().numpy().astype(np.int64)
+    got[:, 0] = ref_keep[got[:, 0]]
+    got[:, 1] = ref_keep[got[:, 1]]
+    np.testing.assert_array_equal(got, oracle.pairs_horizontal(off, tids, 6000, threshold=s).astype(np.int64))
+    empty_o, empty_t = select_csr(torch.as_tensor(off).cuda(), torch.as_tensor(tids).cuda(), np.zeros(0, np.int32))
+    assert empty_o.cpu().tolist() == [0] and empty_t.numel() == 0
