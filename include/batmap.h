@@ -55,6 +55,9 @@ typedef struct batmap_collection* batmap_handle; /* library-owned; free with bat
 /* pair_supports flags (batmap_pair_supports_ex) */
 #define BATMAP_PAIRS_RAW 0x1u      /* test hook: emit the raw BatMap counts (no failure corrections) */
 #define BATMAP_PAIRS_SIMPLE 0x2u   /* test hook: use the one-thread-per-pair kernel (cross-check)    */
+#define BATMAP_PAIRS_FREQUENT 0x4u /* intersect only items with |S_i| >= threshold (no pair with an
+                                      infrequent item reaches the threshold); same output, less work.
+                                      Ignored for threshold 0 and with BATMAP_PAIRS_RAW */
 
 /*
  * Build options.  Zero-initialised = defaults.
@@ -181,7 +184,7 @@ batmap_status batmap_shard_import(batmap_handle h, const int64_t* offsets, const
                                   const uint64_t* fails_all, const int64_t* n_fails,
                                   int64_t stride_fails, batmap_stream_t stream);
 
-/* General form: flags = BATMAP_PAIRS_RAW | BATMAP_PAIRS_SIMPLE (test hooks), else 0. */
+/* General form: flags = BATMAP_PAIRS_FREQUENT, and the test hooks BATMAP_PAIRS_RAW | BATMAP_PAIRS_SIMPLE. */
 batmap_status batmap_pair_supports_ex(batmap_handle h, const int32_t* items, int64_t n_sel,
                                       uint32_t threshold, int32_t part, int32_t n_parts,
                                       uint32_t flags, batmap_triple* out, int64_t capacity,
@@ -239,6 +242,7 @@ typedef struct {
     double build_post_ms;   /* batmap_build after the encode (failure list F, Fail(i), A_b)     */
     int32_t k2_tile_cols;   /* tiled K2: tile width in items (128, or 64 for small/ragged plans)  */
     int32_t reserved;
+    int64_t n_selected;     /* items intersected by the last pair_supports (after BATMAP_PAIRS_FREQUENT) */
 } batmap_stats_t;
 
 batmap_status batmap_stats(batmap_handle h, batmap_stats_t* out);

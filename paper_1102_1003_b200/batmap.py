@@ -26,6 +26,7 @@ BATMAP_CHECK_INPUT = 0x1
 BATMAP_BUILD_SERIAL = 0x2
 BATMAP_PAIRS_RAW = 0x1
 BATMAP_PAIRS_SIMPLE = 0x2
+BATMAP_PAIRS_FREQUENT = 0x4
 
 
 class BatMapError(RuntimeError):
@@ -46,7 +47,7 @@ class Stats(ctypes.Structure):
                 ("n_candidates", ctypes.c_int64), ("n_results", ctypes.c_int64), ("k2_kind", ctypes.c_int32),
                 ("k2_grid", ctypes.c_int32), ("launches_build", ctypes.c_int64), ("launches_pairs", ctypes.c_int64),
                 ("build_pre_ms", ctypes.c_double), ("build_post_ms", ctypes.c_double),
-                ("k2_tile_cols", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("k2_tile_cols", ctypes.c_int32), ("reserved", ctypes.c_int32), ("n_selected", ctypes.c_int64)]
 
 
 class Info(ctypes.Structure):
@@ -223,12 +224,14 @@ class Collection:
         return {k: getattr(st, k) for k, _ in Stats._fields_}
 
     def pair_supports(self, items=None, threshold: int = 1, *, part: int = 0, n_parts: int = 1,
-                      raw: bool = False, simple: bool = False, stream=None):
-        """int32 tensor [K, 3] of (i, j, support), i < j, support >= threshold, sorted by (i, j)."""
+                      frequent_only: bool = False, raw: bool = False, simple: bool = False, stream=None):
+        """int32 tensor [K, 3] of (i, j, support), i < j, support >= threshold, sorted by (i, j).
+        frequent_only: intersect only items with |S_i| >= threshold; same output."""
         import torch
 
         lib = load_library()
-        flags = (BATMAP_PAIRS_RAW if raw else 0) | (BATMAP_PAIRS_SIMPLE if simple else 0)
+        flags = ((BATMAP_PAIRS_RAW if raw else 0) | (BATMAP_PAIRS_SIMPLE if simple else 0) |
+                 (BATMAP_PAIRS_FREQUENT if frequent_only else 0))
         it = None
         n_sel = 0
         if items is not None:

@@ -868,6 +868,8 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     }
     const int64_t nnz = off_h[n];
     h->nnz = nnz;
+    h->size_orig_h.resize(n);
+    for (int64_t i = 0; i < n; ++i) h->size_orig_h[i] = (int32_t)(off_h[i + 1] - off_h[i]);
     // ---- sort by width, stable by id (reading #16): counting sort over log2 r
     h->pos2orig_h.resize(n);
     h->orig2pos_h.resize(n);

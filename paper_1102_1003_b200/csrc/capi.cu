@@ -206,11 +206,36 @@ batmap_status batmap_pair_supports_ex(batmap_handle h, const int32_t* items, int
         h->res_n = -1;
         rec(h, EV_P0, st);
         Selection sel;
-        if (items) {
+        const bool frequent = (flags & BATMAP_PAIRS_FREQUENT) && threshold >= 1 && !(flags & BATMAP_PAIRS_RAW);
+        if (frequent) {  // drop the items whose support |S_i| is below the threshold
+            std::vector<int32_t> req;
+            if (items) {
+                req.resize(n_sel);
+                if (n_sel) {
+                    BM_CUDA(cudaMemcpyAsync(req.data(), items, n_sel * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                    BM_CUDA(cudaStreamSynchronize(st));
+                }
+            } else {
+                req.resize(h->n);
+                for (int64_t i = 0; i < h->n; ++i) req[i] = (int32_t)i;
+            }
+            std::vector<int32_t> keep;
+            keep.reserve(req.size());
+            for (int32_t i : req) {
+                if (i < 0 || i >= h->n) {
+                    set_error("items: id %d out of range [0, %lld)", i, (long long)h->n);
+                    return BATMAP_E_INVALID;
+                }
+                if ((uint32_t)h->size_orig_h[i] >= threshold) keep.push_back(i);
+            }
+            if (!items && (int64_t)keep.size() == h->n) full_selection(h, &sel);
+            else BM_TRY(gather_selection_host(h, keep, st, &sel));
+        } else if (items) {
             BM_TRY(gather_selection(h, items, n_sel, st, &sel));
         } else {
             full_selection(h, &sel);
         }
+        h->stats.n_selected = sel.n_sel;
         int64_t n_cand = 0, n_res = 0;
         h->stats.word_compares = h->stats.tile_compares = 0;
         h->stats.k2_kind = h->stats.k2_grid = 0;

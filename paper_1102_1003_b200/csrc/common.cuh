@@ -131,6 +131,7 @@ struct batmap_collection {
     bm::PiParams pi{};
 
     std::vector<int32_t> pos2orig_h, orig2pos_h;
+    std::vector<int32_t> size_orig_h;  // |S_i| by caller id (the frequent-item filter)
     std::vector<bm::ClassInfo> classes;
     int64_t arena_bytes_raw = 0;  // sum 3 r_i
     int64_t arena_words = 0;      // incl. padding
@@ -254,6 +255,8 @@ batmap_status run_finalize(batmap_collection* h, const Selection& sel, int64_t n
                            uint32_t threshold, uint32_t flags, cudaStream_t st, int64_t* n_res);
 batmap_status gather_selection(batmap_collection* h, const int32_t* items_d, int64_t n_sel,
                                cudaStream_t st, Selection* sel);
+batmap_status gather_selection_host(batmap_collection* h, const std::vector<int32_t>& items, cudaStream_t st,
+                                    Selection* sel);
 batmap_status sort_triples(batmap_triple* t, int64_t n, cudaStream_t st);
 // ingest.cu
 batmap_status fimi_parse(const uint8_t* text, int64_t n, cudaStream_t st, batmap_fimi* h, int64_t* bad_line);

@@ -207,6 +207,12 @@ batmap_status gather_selection(batmap_collection* h, const int32_t* items_d, int
         BM_CUDA(cudaMemcpyAsync(items.data(), items_d, n_sel * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         BM_CUDA(cudaStreamSynchronize(st));
     }
+    return gather_selection_host(h, items, st, sel);
+}
+
+batmap_status gather_selection_host(batmap_collection* h, const std::vector<int32_t>& items, cudaStream_t st,
+                                    Selection* sel) {
+    const int64_t n_sel = (int64_t)items.size();
     std::vector<int32_t> pos(n_sel);
     for (int64_t k = 0; k < n_sel; ++k) {
         if (items[k] < 0 || items[k] >= h->n) {

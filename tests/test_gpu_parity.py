@@ -355,6 +355,27 @@ def test_tile_widths_exact(max_loop, monkeypatch):
     c.close()
 
 
+def test_frequent_only_same_output():
+    """BATMAP_PAIRS_FREQUENT intersects only items with |S_i| >= threshold and returns exactly
+    the same triples: full selection, a subset, parts, with forced failures; ignored at threshold 0."""
+    off, tids = zipf(3000, 5000, seed=21)
+    c = _coll(off, tids, 5000, seed=2, max_loop=1)
+    sizes = np.diff(off)
+    for s in (2, 9, 40):
+        ref = oracle.pairs_horizontal(off, tids, 5000, threshold=s)
+        np.testing.assert_array_equal(_np(c.pair_supports(threshold=s, frequent_only=True)), ref)
+        assert c.stats()["n_selected"] == int((sizes >= s).sum()) < len(sizes)
+        parts = np.concatenate([_np(c.pair_supports(threshold=s, frequent_only=True, part=p, n_parts=2))
+                                for p in range(2)])
+        np.testing.assert_array_equal(parts[np.lexsort((parts[:, 1], parts[:, 0]))], ref)
+    sub = np.arange(0, 3000, 3, dtype=np.int32)
+    np.testing.assert_array_equal(_np(c.pair_supports(items=torch.as_tensor(sub).cuda(), threshold=5, frequent_only=True)),
+                                  oracle.pairs_horizontal(off, tids, 5000, items=sub, threshold=5))
+    c.pair_supports(threshold=0, frequent_only=True)
+    assert c.stats()["n_selected"] == len(sizes)
+    c.close()
+
+
 def test_items_subset_and_parts():
     w = make_config("C1")
     rng = np.random.default_rng(3)
