@@ -56,7 +56,7 @@ struct Counts {
 __device__ __forceinline__ Counts count16(const uint8_t* __restrict__ text, int64_t n, int64_t pos, bool aligned,
                                           uint8_t (&b)[kIngBytes], unsigned long long* err_pos) {
     load16(text, n, pos, aligned, b);
-    uint32_t prev = pos > 0 ? __ldg(text + pos - 1) : 32u;
+    uint32_t prev = (pos > 0 && pos <= n) ? __ldg(text + pos - 1) : 32u;  // threads past the end read nothing
     Counts c{0, 0};
 #pragma unroll
     for (int k = 0; k < kIngBytes; ++k) {
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kIngThreads) k_fimi_keys(const uint8_t* __rest
     unsigned int mx = 0;
     // a token is parsed from the registers while it lies in this thread's 16 bytes; digits that
     // continue a token from the previous thread's bytes belong to that thread (it reads on)
-    bool skipping = pos > 0 && is_digit(__ldg(text + pos - 1));
+    bool skipping = pos > 0 && pos <= n && is_digit(__ldg(text + pos - 1));
     bool in = false, ovf = false;
     uint64_t v = 0;
     int64_t start = 0;
