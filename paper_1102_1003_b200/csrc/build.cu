@@ -660,10 +660,8 @@ static batmap_status cub_tmp(batmap_collection* h, size_t need, cudaStream_t st)
     return BATMAP_OK;
 }
 
-static int ilog2_u64(uint64_t v) {
-    int l = 0;
-    while ((1ull << l) < v) ++l;
-    return l;
+static int ilog2_u64(uint64_t v) {  // ceil(log2 v), 0 for v <= 1
+    return v <= 1 ? 0 : 64 - __builtin_clzll(v - 1);
 }
 
 // Failure list F sorted by (pos, tid), per-item offsets and A_b of failed tids.
