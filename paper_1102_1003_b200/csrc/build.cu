@@ -831,7 +831,8 @@ static batmap_status launch_cluster_tier(batmap_collection* h, const ClassInfo& 
 }
 
 batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
-                               const batmap_build_opts* o, int part, int n_parts, cudaStream_t st) {
+                               const batmap_build_opts* o, int part, int n_parts, cudaStream_t st,
+                               const int64_t* offsets_host) {
     const int64_t n = h->n, m = h->m;
     const int64_t l0 = h->launches;
     rec(h, EV_B0, st);
@@ -843,8 +844,12 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     h->pi = make_pi(h->seed, s, o ? o->pi_table : nullptr);
 
     std::vector<int64_t> off_h(n + 1);
-    BM_CUDA(cudaMemcpyAsync(off_h.data(), offsets, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    BM_CUDA(cudaStreamSynchronize(st));
+    if (offsets_host) {  // host copy supplied (batmap_mine_host): no read-back, planning overlaps the upload
+        std::copy(offsets_host, offsets_host + n + 1, off_h.begin());
+    } else {
+        BM_CUDA(cudaMemcpyAsync(off_h.data(), offsets, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+    }
     if (off_h[0] != 0) {
         set_error("offsets[0] must be 0");
         return BATMAP_E_INVALID;

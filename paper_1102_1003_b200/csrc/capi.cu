@@ -62,9 +62,11 @@ batmap_status batmap_build(const int64_t* offsets, const int32_t* tids, int64_t 
     return batmap_build_shard(offsets, tids, n_items, n_transactions, opts, 0, 1, stream, out);
 }
 
-batmap_status batmap_build_shard(const int64_t* offsets, const int32_t* tids, int64_t n_items,
-                                 int64_t n_transactions, const batmap_build_opts* opts, int32_t part,
-                                 int32_t n_parts, batmap_stream_t stream, batmap_handle* out) {
+// offsets_host: the same offsets already on the host (batmap_mine_host), or NULL: spares the
+// build's read-back and lets its host planning overlap the tidlist upload.
+static batmap_status build_impl(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t n_transactions,
+                                const batmap_build_opts* opts, int32_t part, int32_t n_parts, batmap_stream_t stream,
+                                batmap_handle* out, const int64_t* offsets_host) {
     if (n_parts < 1 || part < 0 || part >= n_parts) {
         set_error("need 0 <= part < n_parts (got %d of %d)", part, n_parts);
         return BATMAP_E_INVALID;
@@ -111,7 +113,7 @@ batmap_status batmap_build_shard(const int64_t* offsets, const int32_t* tids, in
     h->seed = opts ? opts->seed : 0;
     h->r_min = r_min;
     h->max_loop_opt = opts ? opts->max_loop : 0;
-    batmap_status rc = build_collection(h, offsets, tids, opts, part, n_parts, st);
+    batmap_status rc = build_collection(h, offsets, tids, opts, part, n_parts, st, offsets_host);
     if (rc != BATMAP_OK) {
         free_all(h);
         delete h;
@@ -119,6 +121,12 @@ batmap_status batmap_build_shard(const int64_t* offsets, const int32_t* tids, in
     }
     *out = h;
     return BATMAP_OK;
+}
+
+batmap_status batmap_build_shard(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                                 int64_t n_transactions, const batmap_build_opts* opts, int32_t part,
+                                 int32_t n_parts, batmap_stream_t stream, batmap_handle* out) {
+    return build_impl(offsets, tids, n_items, n_transactions, opts, part, n_parts, stream, out, nullptr);
 }
 
 batmap_status batmap_shard_sizes(batmap_handle h, int32_t part, int64_t* words, int64_t* n_fail) {
@@ -438,7 +446,7 @@ batmap_status batmap_mine_host(const int64_t* offsets, const int32_t* tids, int6
         cleanup();
         return BATMAP_E_CUDA;
     }
-    rc = batmap_build(off_d, tids_d, n_items, n_transactions, opts, stream, &h);
+    rc = build_impl(off_d, tids_d, n_items, n_transactions, opts, 0, 1, stream, &h, offsets);
     if (rc == BATMAP_OK)
         rc = batmap_pair_supports(h, items ? items_d : nullptr, n_sel, threshold, out_d, capacity, n_out, stream);
     if (rc == BATMAP_OK && *n_out > 0) {

@@ -226,7 +226,8 @@ batmap_status ensure(T** p, int64_t* cap, int64_t need, cudaStream_t s) {
 
 // build.cu
 batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
-                               const batmap_build_opts* o, int part, int n_parts, cudaStream_t st);
+                               const batmap_build_opts* o, int part, int n_parts, cudaStream_t st,
+                               const int64_t* offsets_host = nullptr);
 int64_t shard_words(const batmap_collection* h, int p, int n_parts);
 batmap_status emit_sorted_keys(uint64_t* keys, uint32_t* vals, int64_t K, int64_t cap, batmap_triple* out,
                                cudaStream_t st);
