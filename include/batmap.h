@@ -312,7 +312,7 @@ batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n
  * batmap_plan_work -- host-only view of the intersection planner (no device needed).  For width
  * classes a = 0..n_classes-1 with class_n[a] items of class_w[a] words (class_w ascending, each a
  * multiple of 16), lists the work items of `part` of `n_parts` in execution order.  A work item is
- * the 128 x 128 tile (ti, tj) of the class rectangle (a, b) of PLANNED classes (see
+ * the 128 x tile_cols tile (ti, tj) (see batmap_plan_tile) of the class rectangle (a, b) of PLANNED classes (see
  * batmap_plan_groups; equal to the input classes when nothing is promoted), a <= b (tj >= ti when a == b), over
  * k-chunks [k0, k1) of 16 words; R > 1 marks a virtualised rectangle (each class-b BatMap viewed as
  * R columns of class_w[a] words); acc = 1 marks rectangles whose partial counts are summed in
@@ -320,7 +320,7 @@ batmap_status batmap_swar_device(const uint32_t* x, const uint32_t* y, int64_t n
  *   grid_cap  resident CTAs assumed for the split-K target (0 => 2 x 148, or 4 x 148 for 64-wide tiles).
  *   items     [host] 8 * capacity int32: (a, b, ti, tj, k0, k1, R, acc) per item.
  *   n_items, word_compares, tile_compares [host]: count; sum over this part's pairs of
- *             max(W_i, W_j); words x 128 x 128 summed over its items.
+ *             max(W_i, W_j); words x 128 x tile_cols summed over its items.
  */
 batmap_status batmap_plan_work(int32_t n_classes, const int64_t* class_n, const int64_t* class_w,
                                int32_t part, int32_t n_parts, int32_t grid_cap, int32_t* items,

@@ -5,7 +5,7 @@
 // SWAR(x, y) = #byte lanes with equal 7 element bits and (b_x OR b_y).
 //
 // How (B200): the planner (plan.cu) cuts the pair triangle into width-class rectangles
-// and 128 x 128 tiles (symmetry cut p <= q); skinny rectangles are
+// and 128 x 128 (or 128 x 64) tiles (symmetry cut p <= q); skinny rectangles are
 // virtualised and long tiles split along k.  A persistent kernel, 2 CTAs x 8 warps per SM,
 // claims work items longest-first from a global counter; thread 0 of each CTA streams
 // [16 words x 128 items] boxes of both operands with TMA (cp.async.bulk.tensor, 3-stage mbarrier

@@ -1,4 +1,4 @@
-// plan.cu -- host-side planner of ★K2: width-class rectangles, 128 x 128 tiles with the
+// plan.cu -- host-side planner of ★K2: width-class rectangles, 128 x tn tiles with the
 // symmetry cut p <= q, virtualised skinny rectangles, split-K for long tiles, and
 // the deal of work to the parts of a multi-GPU run, and promotion of small narrow classes.
 #include <algorithm>
