@@ -567,3 +567,43 @@ def test_merge_long_rows_from_global(long_len):
     tids = np.concatenate(rows)
     got, _, _ = _merge(off, tids, m, 1)
     np.testing.assert_array_equal(got, oracle.pairs_merge(off, tids, threshold=1))
+
+
+@pytest.mark.parametrize("case", range(64))
+def test_randomized_plans_exact(case, monkeypatch):
+    """Randomised stress of the planner features on the device: random item counts, universes,
+    size mixes (uniform / Zipf / wide outliers), thresholds, MaxLoop (forced failures), tile width,
+    promotion and virtualisation switches, item subsets and part splits -- every result equal to
+    the oracle."""
+    rng = np.random.default_rng(1000 + case)
+    n = int(rng.integers(2, 420))
+    m = int(rng.choice([1, 7, 127, 128, 1000, 20000, 60000]))
+    kind = case % 3
+    rows = []
+    for i in range(n):
+        if kind == 0:
+            k = int(rng.integers(0, min(m, 400) + 1))
+        elif kind == 1:
+            k = int(min(m, max(0, rng.zipf(1.6) - 1)))
+        else:
+            k = int(min(m, rng.integers(0, 60) if rng.random() < 0.9 else rng.integers(0, m + 1)))
+        rows.append(np.sort(rng.choice(m, size=k, replace=False)).astype(np.int32))
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    tids = np.concatenate(rows) if off[-1] else np.zeros(0, np.int32)
+    monkeypatch.setenv("BATMAP_K2_TN", str(rng.choice(["0", "64", "128"])))
+    monkeypatch.setenv("BATMAP_K2_PROMOTE", str(rng.choice(["0", "1"])))
+    monkeypatch.setenv("BATMAP_K2_VIRTUAL", str(rng.choice(["0", "1"])))
+    c = _coll(off, tids, m, seed=int(rng.integers(0, 1 << 30)), max_loop=int(rng.choice([0, 0, 1])))
+    thr = int(rng.choice([0, 1, 2, 3, 5]))
+    ref = oracle.pairs_merge(off, tids, threshold=thr)
+    np.testing.assert_array_equal(_np(c.pair_supports(threshold=thr)), ref)
+    if n >= 4:
+        sub = np.sort(rng.choice(n, size=int(rng.integers(2, n + 1)), replace=False)).astype(np.int32)
+        np.testing.assert_array_equal(_np(c.pair_supports(items=torch.as_tensor(sub).cuda(), threshold=max(thr, 1))),
+                                      oracle.pairs_merge(off, tids, items=sub, threshold=max(thr, 1)))
+        k = int(rng.integers(2, 5))
+        parts = np.concatenate([_np(c.pair_supports(threshold=thr, part=p, n_parts=k)) for p in range(k)])
+        parts = parts[np.lexsort((parts[:, 1], parts[:, 0]))] if len(parts) else parts.reshape(0, 3)
+        np.testing.assert_array_equal(parts, ref)
+    c.close()
