@@ -127,8 +127,19 @@ def _cpu_baseline(w, target_s: float = 8.0):
     dt = time.perf_counter() - t0
     pairs = sum(n - 1 - u for u in range(rows))
     return {"value": pairs / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "cpu_model": _cpu_model(),
             "sample": f"sorted-merge oracle, first {rows} of {n} items x all later items "
                       f"({pairs} pair intersections, {len(res)} frequent) of {w.name}, {dt:.1f} s"}
+
+
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, rank, world):
