@@ -607,3 +607,52 @@ def test_randomized_plans_exact(case, monkeypatch):
         parts = parts[np.lexsort((parts[:, 1], parts[:, 0]))] if len(parts) else parts.reshape(0, 3)
         np.testing.assert_array_equal(parts, ref)
     c.close()
+
+
+def test_c_abi_status_codes_on_device():
+    """Status semantics of the C ABI with live device buffers: the two-call capacity protocol of
+    pair_supports and select_csr (E_CAPACITY with the required size), out-of-range ids under
+    BATMAP_PAIRS_FREQUENT, pair queries on an un-imported shard, NULL outputs of fimi_export."""
+    import ctypes
+
+    from paper_1102_1003_b200 import batmap
+
+    lib = batmap.load_library()
+    w = make_config("C1")
+    o, t = torch.as_tensor(w.offsets).cuda(), torch.as_tensor(w.tids).cuda()
+    c = _coll(w.offsets, w.tids, w.m, seed=1)
+    ref = oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=w.threshold)
+    n_out = ctypes.c_int64(-1)
+    out = torch.empty((8, 3), dtype=torch.int32, device="cuda")
+    st = batmap._stream_ptr(None)
+    rc = lib.batmap_pair_supports(c._h, None, 0, w.threshold, batmap._dptr(out), 8, ctypes.byref(n_out), st)
+    assert rc == batmap.BATMAP_E_CAPACITY and n_out.value == len(ref)
+    big = torch.empty((n_out.value, 3), dtype=torch.int32, device="cuda")
+    rc = lib.batmap_pair_supports(c._h, None, 0, w.threshold, batmap._dptr(big), n_out.value, ctypes.byref(n_out), st)
+    assert rc == batmap.BATMAP_OK
+    np.testing.assert_array_equal(big.cpu().numpy().astype(np.uint32), ref)
+    bad = torch.tensor([0, w.n + 5], dtype=torch.int32, device="cuda")
+    rc = lib.batmap_pair_supports_ex(c._h, batmap._dptr(bad), 2, 3, 0, 1, batmap.BATMAP_PAIRS_FREQUENT,
+                                     batmap._dptr(big), big.shape[0], ctypes.byref(n_out), st)
+    assert rc == batmap.BATMAP_E_INVALID and "out of range" in batmap.load_library().batmap_last_error().decode()
+    c.close()
+    # select_csr two-call protocol
+    items = torch.arange(0, w.n, 2, dtype=torch.int32, device="cuda")
+    off_out = torch.empty(items.numel() + 1, dtype=torch.int64, device="cuda")
+    tids_out = torch.empty(4, dtype=torch.int32, device="cuda")
+    nnz = ctypes.c_int64(-1)
+    rc = lib.batmap_select_csr(batmap._dptr(o), batmap._dptr(t), w.n, batmap._dptr(items), items.numel(),
+                               batmap._dptr(off_out), batmap._dptr(tids_out), 4, ctypes.byref(nnz), st)
+    assert rc == batmap.BATMAP_E_CAPACITY
+    assert nnz.value == int(np.diff(w.offsets)[::2].sum()) == int(off_out[-1])
+    # a shard must be completed (batmap_shard_import) before it is queried
+    part = _coll(w.offsets, w.tids, w.m, seed=1, part=0, n_parts=2)
+    rc = lib.batmap_pair_supports(part._h, None, 0, 1, batmap._dptr(big), big.shape[0], ctypes.byref(n_out), st)
+    assert rc == batmap.BATMAP_E_INVALID
+    part.close()
+    # fimi_export with NULL outputs copies nothing and succeeds
+    text = torch.frombuffer(bytearray(b"1 2\n2 3\n"), dtype=torch.uint8).cuda()
+    h, bad_line = ctypes.c_void_p(), ctypes.c_int64()
+    assert lib.batmap_fimi_parse(batmap._dptr(text), text.numel(), st, ctypes.byref(h), ctypes.byref(bad_line)) == 0
+    assert lib.batmap_fimi_export(h, None, None, None, st) == 0
+    lib.batmap_fimi_destroy(h)
