@@ -456,10 +456,15 @@ def select_csr(offsets, tids, items, *, stream=None):
     return off_out, out[: nnz.value]
 
 
-def mine_fimi(text, threshold: int, **build_kw) -> np.ndarray:
+def mine_fimi(text, threshold, **build_kw) -> np.ndarray:
     """End to end from a FIMI file: parse + frequent-item filter on the device, build the BatMaps
-    of the frequent items, emit every pair with support >= threshold.  Returns int64 [K, 3] of
+    of the frequent items, emit every pair with support >= threshold.  `threshold` is a count, or
+    a float in (0, 1) meaning that fraction of the transactions (ceil).  Returns int64 [K, 3] of
     (label_i, label_j, support), label_i < label_j, sorted."""
+    if isinstance(threshold, float) and 0.0 < threshold < 1.0:
+        m = parse_fimi(text, min_support=0).m
+        threshold = max(1, int(np.ceil(threshold * m - 1e-9)))
+    threshold = int(threshold)
     db = parse_fimi(text, min_support=threshold)
     if db.n_items < 2:
         return np.zeros((0, 3), np.int64)

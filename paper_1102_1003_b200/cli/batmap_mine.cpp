@@ -3,6 +3,9 @@
 //
 //   batmap_mine <file.dat> <min_support> [--seed S] [--quiet]
 //
+// min_support is a transaction count (e.g. 100), or a fraction of the transactions written as a
+// percentage ("0.5%") or a number below 1 ("0.005"): s = ceil(fraction * m), at least 1.
+//
 // Reads the file (one transaction per line, whitespace-separated item labels), parses it on the
 // device (batmap_fimi_parse), drops items with support below min_support (batmap_fimi_filter,
 // P:118), builds the BatMaps (batmap_build) and emits every pair of items whose support is at
@@ -15,6 +18,7 @@
 #include <string.h>
 
 #include <chrono>
+#include <cmath>
 #include <vector>
 
 #include "batmap.h"
@@ -39,14 +43,19 @@ int main(int argc, char** argv) {
         return 2;
     }
     const char* path = argv[1];
-    const long long s = atoll(argv[2]);
+    const char* s_arg = argv[2];
+    const size_t s_len = strlen(s_arg);
+    const bool percent = s_len > 0 && s_arg[s_len - 1] == '%';
+    const double s_val = strtod(s_arg, nullptr);
+    const bool relative = percent || (s_val > 0.0 && s_val < 1.0);
+    long long s = relative ? 1 : atoll(s_arg);
     uint64_t seed = 0;
     bool quiet = false;
     for (int a = 3; a < argc; ++a) {
         if (!strcmp(argv[a], "--seed") && a + 1 < argc) seed = strtoull(argv[++a], nullptr, 10);
         else if (!strcmp(argv[a], "--quiet")) quiet = true;
     }
-    if (s < 1 || s > 0xFFFFFFFFll) {
+    if (!(s_val > 0.0) || (!relative && (s < 1 || s > 0xFFFFFFFFll))) {
         fprintf(stderr, "batmap_mine: min_support must be in [1, 2^32)\n");
         return 2;
     }
@@ -80,6 +89,11 @@ int main(int argc, char** argv) {
     if (rc != BATMAP_OK) return fail("parse", rc);
     int64_t n_all = 0, nnz_all = 0, m = 0;
     batmap_fimi_info(db, &n_all, &nnz_all, &m);
+    if (relative) {  // a fraction of the transactions (support counts transactions)
+        const double frac = percent ? s_val / 100.0 : s_val;
+        s = (long long)std::ceil(frac * (double)m - 1e-9);
+        if (s < 1) s = 1;
+    }
     if ((rc = batmap_fimi_filter(db, (uint32_t)s, (batmap_stream_t)st)) != BATMAP_OK) return fail("filter", rc);
     int64_t n = 0, nnz = 0;
     batmap_fimi_info(db, &n, &nnz, &m);

@@ -88,6 +88,7 @@ def test_mine_fimi_end_to_end():
     labels = np.arange(w.n, dtype=np.int64) * 3 + 1000
     text = fimi_text(w.offsets, w.tids, w.m, labels=labels, seed=5, messy=True)
     got = mine_fimi(text, w.threshold, seed=1)
+    np.testing.assert_array_equal(mine_fimi(text, w.threshold / w.m, seed=2), got)  # as a fraction of m
     ro, rt, rl, _ = parse_fimi(text)
     ref = oracle.pairs_horizontal(ro, rt, w.m, threshold=w.threshold).astype(np.int64)
     ref[:, 0] = rl[ref[:, 0]]
@@ -123,6 +124,9 @@ def test_cli_mines_a_fimi_file(tmp_path):
     path.write_bytes(fimi_text(w.offsets, w.tids, w.m, labels=labels, seed=2, messy=True))
     r = subprocess.run([build_ext.build_cli(), str(path), str(w.threshold), "--seed", "3"], capture_output=True,
                        text=True, timeout=120)
+    rel = subprocess.run([build_ext.build_cli(), str(path), f"{100.0 * w.threshold / w.m}%", "--quiet"],
+                         capture_output=True, text=True, timeout=120)  # the same threshold as a percentage
+    assert rel.returncode == 0 and rel.stdout == r.stdout
     assert r.returncode == 0, r.stderr
     got = np.array([list(map(int, ln.split())) for ln in r.stdout.splitlines()], dtype=np.int64).reshape(-1, 3)
     ro, rt, rl, _ = parse_fimi(path.read_bytes())
