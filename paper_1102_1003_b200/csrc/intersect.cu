@@ -124,26 +124,31 @@ __device__ __forceinline__ void load_ops(Ops& o, const uint32_t* sA, const uint3
 
 // The 64 compare-and-counts of one k step, written as a software pipeline over the pairs so
 // that every ALU-pipe LOP3 is followed by an FMA-pipe op (IADD, IDP4A): the ALU pipe, which
-// binds, can then accept an instruction every other cycle.  asm volatile keeps this order.
-// (tools/swar_ubench.cu: 0.84 vs 0.81 of R_int for the compiler-scheduled loop.)
+// binds, can then accept an instruction every other cycle.  Dependent instructions sit kD
+// pipeline steps apart (kD = 2: two independent compares between a producer and its consumer).
+// asm volatile keeps this order.  (tools/swar_ubench.cu: distance 2 runs 1.5 % faster than 1, 3
+// and 4 are slower again; the compiler-scheduled loop is ~4 % slower.)
 __device__ __forceinline__ void compute_ops(const Ops& o, uint32_t (&acc)[8][8]) {
+    constexpr int kD = 2;
     const uint32_t x[8] = {o.xa.x, o.xa.y, o.xa.z, o.xa.w, o.xb.x, o.xb.y, o.xb.z, o.xb.w};
     const uint32_t y[8] = {o.ya.x, o.ya.y, o.ya.z, o.ya.w, o.yb.x, o.yb.y, o.yb.z, o.yb.w};
     const uint32_t xm[8] = {o.ma.x, o.ma.y, o.ma.z, o.ma.w, o.mb.x, o.mb.y, o.mb.z, o.mb.w};
     const uint32_t ym[8] = {o.na.x, o.na.y, o.na.z, o.na.w, o.nb.x, o.nb.y, o.nb.z, o.nb.w};
     uint32_t u[64], p[64], v[64];
 #pragma unroll
-    for (int q = 0; q < 64 + 3; ++q) {
+    for (int q = 0; q < 64 + 3 * kD; ++q) {
         if (q < 64)  // u = (x ^ y) | 0x80808080
             asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[q]) : "r"(x[q >> 3]), "r"(y[q & 7]));
-        if (q >= 1 && q - 1 < 64)  // p = u - 0x01010101
-            asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - 1]) : "r"(u[q - 1]));
-        if (q >= 2 && q - 2 < 64)  // v = ~p & (xm | ym)
-            asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;"
-                         : "=r"(v[q - 2])
-                         : "r"(p[q - 2]), "r"(xm[(q - 2) >> 3]), "r"(ym[(q - 2) & 7]));
-        if (q >= 3)  // acc += 128 * matches
-            asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;" : "+r"(acc[(q - 3) >> 3][(q - 3) & 7]) : "r"(v[q - 3]));
+        if (q >= kD && q - kD < 64)  // p = u - 0x01010101
+            asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - kD]) : "r"(u[q - kD]));
+        if (q >= 2 * kD && q - 2 * kD < 64) {  // v = ~p & (xm | ym)
+            const int e = q - 2 * kD;
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v[e]) : "r"(p[e]), "r"(xm[e >> 3]), "r"(ym[e & 7]));
+        }
+        if (q >= 3 * kD) {  // acc += 128 * matches
+            const int e = q - 3 * kD;
+            asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;" : "+r"(acc[e >> 3][e & 7]) : "r"(v[e]));
+        }
     }
 }
 

@@ -300,6 +300,105 @@ __device__ __forceinline__ void step_pipelined_mt(const uint32_t (&x)[MI], const
     }
 }
 
+// Pipeline-schedule variants of the 8x8 step (same 4 instructions per compare):
+//   S = 0: [lop3 u_q, sub p_q-1, lop3 v_q-2, dp4a q-3]   (k2_tiled's order)
+//   S = 1: [lop3 u_q, lop3 v_q-2, sub p_q-1, dp4a q-3]   (ALU pair, FMA pair)
+//   S = 2, 3, 4: distances D = 2, 3, 4: u_q, p_q-D, v_q-2D, acc_q-3D (more independent work between
+//          dependent instructions)
+template <int S>
+__device__ __forceinline__ void step_sched(const uint32_t (&x)[8], const uint32_t (&y)[8], const uint32_t (&xm)[8],
+                                           const uint32_t (&ym)[8], uint32_t (&acc)[8][8]) {
+    constexpr int D = S == 2 ? 2 : (S == 3 ? 3 : (S == 4 ? 4 : 1));
+    uint32_t u[64], p[64], v[64];
+#pragma unroll
+    for (int q = 0; q < 64 + 3 * D; ++q) {
+        const bool du = q < 64, dp = q >= D && q - D < 64, dv = q >= 2 * D && q - 2 * D < 64, da = q >= 3 * D;
+        if (du) asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[q]) : "r"(x[q >> 3]), "r"(y[q & 7]));
+        if (S == 1) {
+            if (dv)
+                asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;"
+                             : "=r"(v[q - 2]) : "r"(p[q - 2]), "r"(xm[(q - 2) >> 3]), "r"(ym[(q - 2) & 7]));
+            if (dp) asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - 1]) : "r"(u[q - 1]));
+        } else {
+            if (dp) asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - D]) : "r"(u[q - D]));
+            if (dv)
+                asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;"
+                             : "=r"(v[q - 2 * D]) : "r"(p[q - 2 * D]), "r"(xm[(q - 2 * D) >> 3]), "r"(ym[(q - 2 * D) & 7]));
+        }
+        if (da)
+            asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;"
+                         : "+r"(acc[(q - 3 * D) >> 3][(q - 3 * D) & 7]) : "r"(v[q - 3 * D]));
+    }
+}
+
+template <int S, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) bench_sched(const uint32_t* __restrict__ g, int reps, uint32_t* out) {
+    __shared__ __align__(16) uint32_t sA[16 * 128], sB[16 * 128], mA[16 * 128], mB[16 * 128];
+    for (int i = threadIdx.x; i < 16 * 128; i += NT) {
+        sA[i] = g[i];
+        sB[i] = g[i + 32 * 128];
+        mA[i] = g[i] & 0x80808080u;
+        mB[i] = g[i + 32 * 128] & 0x80808080u;
+    }
+    __syncthreads();
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
+    const int tr = ((warp & 1) << 3) | (lane & 7);
+    const int tc = ((warp >> 1) << 2) | (lane >> 3);
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int k = 0; k < 16; ++k) {
+            uint32_t x[8], y[8], xm[8], ym[8];
+            const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * 128 + 4 * tr);
+            const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * 128 + 64 + 4 * tr);
+            const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * 128 + 4 * tc);
+            const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * 128 + 64 + 4 * tc);
+            const uint4 a = *reinterpret_cast<const uint4*>(mA + k * 128 + 4 * tr);
+            const uint4 b = *reinterpret_cast<const uint4*>(mA + k * 128 + 64 + 4 * tr);
+            const uint4 c = *reinterpret_cast<const uint4*>(mB + k * 128 + 4 * tc);
+            const uint4 d = *reinterpret_cast<const uint4*>(mB + k * 128 + 64 + 4 * tc);
+            x[0] = xa.x; x[1] = xa.y; x[2] = xa.z; x[3] = xa.w; x[4] = xb.x; x[5] = xb.y; x[6] = xb.z; x[7] = xb.w;
+            y[0] = ya.x; y[1] = ya.y; y[2] = ya.z; y[3] = ya.w; y[4] = yb.x; y[5] = yb.y; y[6] = yb.z; y[7] = yb.w;
+            xm[0] = a.x; xm[1] = a.y; xm[2] = a.z; xm[3] = a.w; xm[4] = b.x; xm[5] = b.y; xm[6] = b.z; xm[7] = b.w;
+            ym[0] = c.x; ym[1] = c.y; ym[2] = c.z; ym[3] = c.w; ym[4] = d.x; ym[5] = d.y; ym[6] = d.z; ym[7] = d.w;
+            step_sched<S>(x, y, xm, ym, acc);
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += acc[i][j] * (i * 8 + j + 1);
+    out[blockIdx.x * NT + threadIdx.x] = s;
+}
+
+template <int S>
+void run_sched(const char* name, const uint32_t* g, int sms, uint32_t* out) {
+    const int reps = 2000, blocks = sms * 2;
+    bench_sched<S, 256, 2><<<blocks, 256>>>(g, 10, out);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int t = 0; t < 3; ++t) {
+        cudaEventRecord(e0);
+        bench_sched<S, 256, 2><<<blocks, 256>>>(g, reps, out);
+        cudaEventRecord(e1);
+        CK(cudaDeviceSynchronize());
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    const double tcmp = (double)blocks * 256 * 64.0 * 16.0 * reps / (best * 1e-3) / 1e12;
+    printf("{\"variant\": \"%s\", \"schedule\": %d, \"tcmp_per_s\": %.3f, \"frac_of_R_int_at_1965MHz\": %.3f, "
+           "\"ms\": %.2f}\n", name, S, tcmp, tcmp / (32.0 * sms * 1.965e9 / 1e12), best);
+}
+
 template <int MI, int MJ, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) bench_mt(const uint32_t* __restrict__ g, int reps, uint32_t* out) {
     // a 16 x RB row block and 16 x CB column block of words; each thread reads MI/4 (resp. MJ/4)
@@ -399,6 +498,12 @@ int main() {
     run<5, 1, 512, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
     run<5, 1, 256, 2, 1, 1>("pipelined_volatile/masks_from_smem+sync", g, sms, out, cyc);
     run<4, 1, 256, 2, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run_sched<0>("sched/k2_order", g, sms, out);
+    run_sched<1>("sched/alu_pair_fma_pair", g, sms, out);
+    run_sched<2>("sched/double_distance", g, sms, out);
+    run_sched<3>("sched/triple_distance", g, sms, out);
+    run_sched<4>("sched/quad_distance", g, sms, out);
+    run_sched<0>("sched/k2_order(again)", g, sms, out);
     run_mt<8, 8, 256, 2>("mt_pipelined/masks_from_smem", g, sms, out);
     run_mt<8, 4, 256, 3>("mt_pipelined/masks_from_smem", g, sms, out);
     run_mt<4, 8, 256, 3>("mt_pipelined/masks_from_smem", g, sms, out);
