@@ -331,6 +331,100 @@ __device__ __forceinline__ void step_sched(const uint32_t (&x)[8], const uint32_
     }
 }
 
+// General schedule: stage offsets D1 (u -> p), D2 (p -> v), D3 (v -> acc); pair order O:
+// 0 = i-major (q -> (q/8, q%8)), 1 = j-major, 2 = diagonal (j = (q + q/8) % 8).
+template <int O>
+__device__ __forceinline__ int pi_(int q) { return O == 1 ? (q & 7) : (q >> 3); }
+template <int O>
+__device__ __forceinline__ int pj_(int q) { return O == 1 ? (q >> 3) : (O == 2 ? ((q + (q >> 3)) & 7) : (q & 7)); }
+
+template <int D1, int D2, int D3, int O>
+__device__ __forceinline__ void step_gen(const uint32_t (&x)[8], const uint32_t (&y)[8], const uint32_t (&xm)[8],
+                                         const uint32_t (&ym)[8], uint32_t (&acc)[8][8]) {
+    uint32_t u[64], p[64], v[64];
+#pragma unroll
+    for (int q = 0; q < 64 + D1 + D2 + D3; ++q) {
+        if (q < 64) asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[q]) : "r"(x[pi_<O>(q)]), "r"(y[pj_<O>(q)]));
+        if (q >= D1 && q - D1 < 64) asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - D1]) : "r"(u[q - D1]));
+        if (q >= D1 + D2 && q - D1 - D2 < 64) {
+            const int e = q - D1 - D2;
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v[e]) : "r"(p[e]), "r"(xm[pi_<O>(e)]), "r"(ym[pj_<O>(e)]));
+        }
+        if (q >= D1 + D2 + D3) {
+            const int e = q - D1 - D2 - D3;
+            asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;" : "+r"(acc[pi_<O>(e)][pj_<O>(e)]) : "r"(v[e]));
+        }
+    }
+}
+
+template <int D1, int D2, int D3, int O>
+__global__ void __launch_bounds__(256, 2) bench_gen(const uint32_t* __restrict__ g, int reps, uint32_t* out) {
+    __shared__ __align__(16) uint32_t sA[16 * 128], sB[16 * 128], mA[16 * 128], mB[16 * 128];
+    for (int i = threadIdx.x; i < 16 * 128; i += 256) {
+        sA[i] = g[i];
+        sB[i] = g[i + 32 * 128];
+        mA[i] = g[i] & 0x80808080u;
+        mB[i] = g[i + 32 * 128] & 0x80808080u;
+    }
+    __syncthreads();
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
+    const int tr = ((warp & 1) << 3) | (lane & 7);
+    const int tc = ((warp >> 1) << 2) | (lane >> 3);
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int k = 0; k < 16; ++k) {
+            uint32_t x[8], y[8], xm[8], ym[8];
+            const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * 128 + 4 * tr);
+            const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * 128 + 64 + 4 * tr);
+            const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * 128 + 4 * tc);
+            const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * 128 + 64 + 4 * tc);
+            const uint4 a = *reinterpret_cast<const uint4*>(mA + k * 128 + 4 * tr);
+            const uint4 b = *reinterpret_cast<const uint4*>(mA + k * 128 + 64 + 4 * tr);
+            const uint4 c = *reinterpret_cast<const uint4*>(mB + k * 128 + 4 * tc);
+            const uint4 d = *reinterpret_cast<const uint4*>(mB + k * 128 + 64 + 4 * tc);
+            x[0] = xa.x; x[1] = xa.y; x[2] = xa.z; x[3] = xa.w; x[4] = xb.x; x[5] = xb.y; x[6] = xb.z; x[7] = xb.w;
+            y[0] = ya.x; y[1] = ya.y; y[2] = ya.z; y[3] = ya.w; y[4] = yb.x; y[5] = yb.y; y[6] = yb.z; y[7] = yb.w;
+            xm[0] = a.x; xm[1] = a.y; xm[2] = a.z; xm[3] = a.w; xm[4] = b.x; xm[5] = b.y; xm[6] = b.z; xm[7] = b.w;
+            ym[0] = c.x; ym[1] = c.y; ym[2] = c.z; ym[3] = c.w; ym[4] = d.x; ym[5] = d.y; ym[6] = d.z; ym[7] = d.w;
+            step_gen<D1, D2, D3, O>(x, y, xm, ym, acc);
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += acc[i][j] * (i * 8 + j + 1);
+    out[blockIdx.x * 256 + threadIdx.x] = s;
+}
+
+template <int D1, int D2, int D3, int O>
+void run_gen(const uint32_t* g, int sms, uint32_t* out) {
+    const int reps = 2000, blocks = sms * 2;
+    bench_gen<D1, D2, D3, O><<<blocks, 256>>>(g, 10, out);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int t = 0; t < 3; ++t) {
+        cudaEventRecord(e0);
+        bench_gen<D1, D2, D3, O><<<blocks, 256>>>(g, reps, out);
+        cudaEventRecord(e1);
+        CK(cudaDeviceSynchronize());
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    const double tcmp = (double)blocks * 256 * 64.0 * 16.0 * reps / (best * 1e-3) / 1e12;
+    printf("{\"variant\": \"gen\", \"D\": [%d, %d, %d], \"order\": %d, \"tcmp_per_s\": %.3f, "
+           "\"frac_of_R_int_at_1965MHz\": %.3f}\n", D1, D2, D3, O, tcmp, tcmp / (32.0 * sms * 1.965e9 / 1e12));
+}
+
 template <int S, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) bench_sched(const uint32_t* __restrict__ g, int reps, uint32_t* out) {
     __shared__ __align__(16) uint32_t sA[16 * 128], sB[16 * 128], mA[16 * 128], mB[16 * 128];
@@ -498,6 +592,17 @@ int main() {
     run<5, 1, 512, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
     run<5, 1, 256, 2, 1, 1>("pipelined_volatile/masks_from_smem+sync", g, sms, out, cyc);
     run<4, 1, 256, 2, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run_gen<2, 2, 2, 0>(g, sms, out);
+    run_gen<2, 2, 2, 1>(g, sms, out);
+    run_gen<2, 2, 2, 2>(g, sms, out);
+    run_gen<1, 2, 1, 0>(g, sms, out);
+    run_gen<2, 1, 2, 0>(g, sms, out);
+    run_gen<2, 2, 1, 0>(g, sms, out);
+    run_gen<1, 1, 2, 0>(g, sms, out);
+    run_gen<2, 3, 2, 0>(g, sms, out);
+    run_gen<3, 2, 1, 0>(g, sms, out);
+    run_gen<1, 3, 1, 0>(g, sms, out);
+    run_gen<2, 2, 2, 0>(g, sms, out);
     run_sched<0>("sched/k2_order", g, sms, out);
     run_sched<1>("sched/alu_pair_fma_pair", g, sms, out);
     run_sched<2>("sched/double_distance", g, sms, out);
