@@ -425,6 +425,86 @@ void run_gen(const uint32_t* g, int sms, uint32_t* out) {
            "\"frac_of_R_int_at_1965MHz\": %.3f}\n", D1, D2, D3, O, tcmp, tcmp / (32.0 * sms * 1.965e9 / 1e12));
 }
 
+// Chunk length between CTA barriers (k2_tiled: the per-chunk mask transform + __syncthreads), with
+// the distance-2 schedule: KPS k-steps per barrier.
+template <int KPS>
+__global__ void __launch_bounds__(256, 2) bench_chunk(const uint32_t* __restrict__ g, int reps, uint32_t* out) {
+    __shared__ __align__(16) uint32_t sA[KPS * 128], sB[KPS * 128], mA[KPS * 128], mB[KPS * 128];
+    for (int i = threadIdx.x; i < KPS * 128; i += 256) {
+        sA[i] = g[i % 4096];
+        sB[i] = g[(i + 32 * 128) % 8192];
+    }
+    __syncthreads();
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
+    const int tr = ((warp & 1) << 3) | (lane & 7);
+    const int tc = ((warp >> 1) << 2) | (lane >> 3);
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    const int chunks = reps * 16 / KPS;  // the same number of k-steps for every KPS
+    for (int r = 0; r < chunks; ++r) {
+        for (int i = threadIdx.x; i < KPS * 128 / 4; i += 256) {  // mask transform, as in k2_tiled
+            uint4 v = reinterpret_cast<const uint4*>(sA)[i];
+            v.x &= 0x80808080u; v.y &= 0x80808080u; v.z &= 0x80808080u; v.w &= 0x80808080u;
+            reinterpret_cast<uint4*>(mA)[i] = v;
+            uint4 w = reinterpret_cast<const uint4*>(sB)[i];
+            w.x &= 0x80808080u; w.y &= 0x80808080u; w.z &= 0x80808080u; w.w &= 0x80808080u;
+            reinterpret_cast<uint4*>(mB)[i] = w;
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int k = 0; k < KPS; ++k) {
+            uint32_t x[8], y[8], xm[8], ym[8];
+            const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * 128 + 4 * tr);
+            const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * 128 + 64 + 4 * tr);
+            const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * 128 + 4 * tc);
+            const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * 128 + 64 + 4 * tc);
+            const uint4 a = *reinterpret_cast<const uint4*>(mA + k * 128 + 4 * tr);
+            const uint4 b = *reinterpret_cast<const uint4*>(mA + k * 128 + 64 + 4 * tr);
+            const uint4 c = *reinterpret_cast<const uint4*>(mB + k * 128 + 4 * tc);
+            const uint4 d = *reinterpret_cast<const uint4*>(mB + k * 128 + 64 + 4 * tc);
+            x[0] = xa.x; x[1] = xa.y; x[2] = xa.z; x[3] = xa.w; x[4] = xb.x; x[5] = xb.y; x[6] = xb.z; x[7] = xb.w;
+            y[0] = ya.x; y[1] = ya.y; y[2] = ya.z; y[3] = ya.w; y[4] = yb.x; y[5] = yb.y; y[6] = yb.z; y[7] = yb.w;
+            xm[0] = a.x; xm[1] = a.y; xm[2] = a.z; xm[3] = a.w; xm[4] = b.x; xm[5] = b.y; xm[6] = b.z; xm[7] = b.w;
+            ym[0] = c.x; ym[1] = c.y; ym[2] = c.z; ym[3] = c.w; ym[4] = d.x; ym[5] = d.y; ym[6] = d.z; ym[7] = d.w;
+            step_gen<2, 2, 2, 0>(x, y, xm, ym, acc);
+        }
+        __syncthreads();  // the next chunk's transform overwrites the planes
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += acc[i][j] * (i * 8 + j + 1);
+    out[blockIdx.x * 256 + threadIdx.x] = s;
+}
+
+template <int KPS>
+void run_chunk(const uint32_t* g, int sms, uint32_t* out) {
+    const int reps = 2400, blocks = sms * 2;  // 2400 * 16 k-steps: divisible by 16, 24, 32, 48
+    bench_chunk<KPS><<<blocks, 256>>>(g, 48, out);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int t = 0; t < 3; ++t) {
+        cudaEventRecord(e0);
+        bench_chunk<KPS><<<blocks, 256>>>(g, reps, out);
+        cudaEventRecord(e1);
+        CK(cudaDeviceSynchronize());
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    const double tcmp = (double)blocks * 256 * 64.0 * 16.0 * reps / (best * 1e-3) / 1e12;
+    printf("{\"variant\": \"chunk\", \"k_steps_per_barrier\": %d, \"tcmp_per_s\": %.3f, "
+           "\"frac_of_R_int_at_1965MHz\": %.3f}\n", KPS, tcmp, tcmp / (32.0 * sms * 1.965e9 / 1e12));
+}
+
 template <int S, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) bench_sched(const uint32_t* __restrict__ g, int reps, uint32_t* out) {
     __shared__ __align__(16) uint32_t sA[16 * 128], sB[16 * 128], mA[16 * 128], mB[16 * 128];
@@ -592,6 +672,8 @@ int main() {
     run<5, 1, 512, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
     run<5, 1, 256, 2, 1, 1>("pipelined_volatile/masks_from_smem+sync", g, sms, out, cyc);
     run<4, 1, 256, 2, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run_chunk<16>(g, sms, out);
+    run_chunk<24>(g, sms, out);
     run_gen<2, 2, 2, 0>(g, sms, out);
     run_gen<2, 2, 2, 1>(g, sms, out);
     run_gen<2, 2, 2, 2>(g, sms, out);
