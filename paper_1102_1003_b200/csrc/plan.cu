@@ -286,41 +286,62 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         return;
     }
     // ---- units dealt to the parts: a tile row of an accumulated rectangle (all contributions
-    // to its pairs stay on one part), or a single tile otherwise
+    // to its pairs stay on one part), or a single tile otherwise.  Units are ordered by cost,
+    // longest first, stable in creation order (rectangle, row, column), and dealt round-robin.
+    // They are kept as segments -- all tiles of an ordinary rectangle (equal cost, contiguous in
+    // creation order), or one accumulated tile row -- so a part touches only its own 1/n_parts of
+    // the units (C4: 3e5 tiles).
     struct Unit {
         int32_t rect, ti, tj;  // tj = -1: whole tile row
         int64_t cost;
     };
-    std::vector<Unit> units;
-    {
-        int64_t nu = 0;
-        for (const Rect& r : P.rects) {
-            const int64_t ta = ceil_div(r.n_rows, kTile), tb = ceil_div(r.n_cols, TN);
-            nu += r.acc ? ta : (r.diag ? diag_tiles(r.n_rows, TN) : ta * tb);
-        }
-        units.reserve((size_t)nu);
-    }
+    struct Seg {
+        int32_t rect, ti;  // ti: the accumulated tile row, or -1 for all tiles of an ordinary rectangle
+        int64_t count, cost;
+    };
+    std::vector<Seg> segs;
     for (int ri = 0; ri < (int)P.rects.size(); ++ri) {
         const Rect& r = P.rects[ri];
         const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, TN);
-        for (int i = 0; i < ta; ++i) {
-            const int j0 = r.diag ? i * QD : 0;
-            if (r.acc) {
-                units.push_back({ri, i, -1, (int64_t)(tb - j0) * tile_cost(r)});
-            } else {
-                for (int j = j0; j < tb; ++j) units.push_back({ri, i, j, tile_cost(r)});
-            }
+        if (r.acc) {
+            for (int i = 0; i < ta; ++i) segs.push_back({ri, i, 1, (int64_t)(tb - (r.diag ? i * QD : 0)) * tile_cost(r)});
+        } else {
+            const int64_t nt = r.diag ? diag_tiles(r.n_rows, TN) : (int64_t)ta * tb;
+            if (nt) segs.push_back({ri, -1, nt, tile_cost(r)});
         }
     }
-    stable_sort_desc(units, [](const Unit& x) { return x.cost; });
+    stable_sort_desc(segs, [](const Seg& x) { return x.cost; });
+    std::vector<Unit> units;  // this part's units, in deal order
+    {
+        int64_t at = 0;  // global index of the segment's first unit
+        for (const Seg& g : segs) {
+            const int64_t t0 = (((int64_t)part - at) % n_parts + n_parts) % n_parts;
+            if (g.ti >= 0) {
+                if (t0 == 0) units.push_back({g.rect, g.ti, -1, g.cost});
+            } else if (t0 < g.count) {
+                const Rect& r = P.rects[g.rect];
+                const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, TN);
+                int64_t t = 0, next = t0;  // unit index at the start of row i; next unit of this part
+                for (int i = 0; i < ta && next < g.count; ++i) {
+                    const int j0 = r.diag ? i * QD : 0;
+                    const int64_t row_n = tb - j0;
+                    while (next < t + row_n) {  // the row's tiles this part takes
+                        units.push_back({g.rect, i, (int32_t)(j0 + (next - t)), g.cost});
+                        next += n_parts;
+                    }
+                    t += row_n;
+                }
+            }
+            at += g.count;
+        }
+    }
     struct WorkC {
         Work w;
         int64_t cost;
     };
     std::vector<WorkC> work;
-    work.reserve(units.size() / (size_t)n_parts + 16);
+    work.reserve(units.size() + 16);
     for (size_t k = 0; k < units.size(); ++k) {
-        if ((int)(k % (size_t)n_parts) != part) continue;
         const Unit& u = units[k];
         const Rect& r = P.rects[u.rect];
         const int tb = (int)ceil_div(r.n_cols, TN);
