@@ -275,7 +275,7 @@ void run_pf(const char* name, const uint32_t* g, int sms, uint32_t* out, unsigne
     cudaEventElapsedTime(&ms, e0, e1);
     const double per_block = (double)NT * 64.0 * 16.0 * reps;
     printf("{\"variant\": \"%s\", \"threads\": %d, \"ctas_per_sm\": %d, \"unroll\": 0, \"cmp_per_clk_per_sm\": 0, "
-           "\"frac_of_32\": 0, \"tcmp_per_s\": %.3f, \"ms\": %.2f, \"eff_mhz\": 0}\\n",
+           "\"frac_of_32\": 0, \"tcmp_per_s\": %.3f, \"ms\": %.2f, \"eff_mhz\": 0}\n",
            name, NT, MINB, per_block * sms / (ms * 1e-3) / 1e12, ms);
 }
 
@@ -355,6 +355,105 @@ __device__ __forceinline__ void step_gen(const uint32_t (&x)[8], const uint32_t 
             asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;" : "+r"(acc[pi_<O>(e)][pj_<O>(e)]) : "r"(v[e]));
         }
     }
+}
+
+// Instruction-choice variants on the distance-2 schedule: SUBK 0 = sub.u32 (ptxas: VIADD),
+// 1 = mad.lo.u32 u * 1 + 0xFEFEFEFF (IMAD); ACCK 0 = dp4a, 1 = mad.hi.u32 v * 2^25 + acc (IMAD.HI,
+// lanes folded at the end -- exact for this benchmark's trip counts).
+template <int SUBK, int ACCK>
+__device__ __forceinline__ void step_ins(const uint32_t (&x)[8], const uint32_t (&y)[8], const uint32_t (&xm)[8],
+                                         const uint32_t (&ym)[8], uint32_t (&acc)[8][8], uint32_t one,
+                                         uint32_t sh25) {
+    constexpr int D = 2;
+    uint32_t u[64], p[64], v[64];
+#pragma unroll
+    for (int q = 0; q < 64 + 3 * D; ++q) {
+        if (q < 64) asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[q]) : "r"(x[q >> 3]), "r"(y[q & 7]));
+        if (q >= D && q - D < 64) {
+            if (SUBK == 0) asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - D]) : "r"(u[q - D]));
+            else asm volatile("mad.lo.u32 %0, %1, %2, 0xFEFEFEFF;" : "=r"(p[q - D]) : "r"(u[q - D]), "r"(one));
+        }
+        if (q >= 2 * D && q - 2 * D < 64) {
+            const int e = q - 2 * D;
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v[e]) : "r"(p[e]), "r"(xm[e >> 3]), "r"(ym[e & 7]));
+        }
+        if (q >= 3 * D) {
+            const int e = q - 3 * D;
+            if (ACCK == 0) asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;" : "+r"(acc[e >> 3][e & 7]) : "r"(v[e]));
+            else asm volatile("mad.hi.u32 %0, %1, %2, %0;" : "+r"(acc[e >> 3][e & 7]) : "r"(v[e]), "r"(sh25));
+        }
+    }
+}
+
+template <int SUBK, int ACCK>
+__global__ void __launch_bounds__(256, 2) bench_ins(const uint32_t* __restrict__ g, int reps, uint32_t one,
+                                                   uint32_t sh25, uint32_t* out) {
+    __shared__ __align__(16) uint32_t sA[16 * 128], sB[16 * 128], mA[16 * 128], mB[16 * 128];
+    for (int i = threadIdx.x; i < 16 * 128; i += 256) {
+        sA[i] = g[i];
+        sB[i] = g[i + 32 * 128];
+        mA[i] = g[i] & 0x80808080u;
+        mB[i] = g[i + 32 * 128] & 0x80808080u;
+    }
+    __syncthreads();
+    const int warp = (threadIdx.x >> 5) & 7, lane = threadIdx.x & 31;
+    const int tr = ((warp & 1) << 3) | (lane & 7);
+    const int tc = ((warp >> 1) << 2) | (lane >> 3);
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int k = 0; k < 16; ++k) {
+            uint32_t x[8], y[8], xm[8], ym[8];
+            const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * 128 + 4 * tr);
+            const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * 128 + 64 + 4 * tr);
+            const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * 128 + 4 * tc);
+            const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * 128 + 64 + 4 * tc);
+            const uint4 a = *reinterpret_cast<const uint4*>(mA + k * 128 + 4 * tr);
+            const uint4 b = *reinterpret_cast<const uint4*>(mA + k * 128 + 64 + 4 * tr);
+            const uint4 c = *reinterpret_cast<const uint4*>(mB + k * 128 + 4 * tc);
+            const uint4 d = *reinterpret_cast<const uint4*>(mB + k * 128 + 64 + 4 * tc);
+            x[0] = xa.x; x[1] = xa.y; x[2] = xa.z; x[3] = xa.w; x[4] = xb.x; x[5] = xb.y; x[6] = xb.z; x[7] = xb.w;
+            y[0] = ya.x; y[1] = ya.y; y[2] = ya.z; y[3] = ya.w; y[4] = yb.x; y[5] = yb.y; y[6] = yb.z; y[7] = yb.w;
+            xm[0] = a.x; xm[1] = a.y; xm[2] = a.z; xm[3] = a.w; xm[4] = b.x; xm[5] = b.y; xm[6] = b.z; xm[7] = b.w;
+            ym[0] = c.x; ym[1] = c.y; ym[2] = c.z; ym[3] = c.w; ym[4] = d.x; ym[5] = d.y; ym[6] = d.z; ym[7] = d.w;
+            step_ins<SUBK, ACCK>(x, y, xm, ym, acc, one, sh25);
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += acc[i][j] * (i * 8 + j + 1);
+    out[blockIdx.x * 256 + threadIdx.x] = s;
+}
+
+template <int SUBK, int ACCK>
+void run_ins(const uint32_t* g, int sms, uint32_t* out) {
+    const int reps = 2000, blocks = sms * 2;
+    bench_ins<SUBK, ACCK><<<blocks, 256>>>(g, 10, 1u, 1u << 25, out);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int t = 0; t < 3; ++t) {
+        cudaEventRecord(e0);
+        bench_ins<SUBK, ACCK><<<blocks, 256>>>(g, reps, 1u, 1u << 25, out);
+        cudaEventRecord(e1);
+        CK(cudaDeviceSynchronize());
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    const double tcmp = (double)blocks * 256 * 64.0 * 16.0 * reps / (best * 1e-3) / 1e12;
+    printf("{\"variant\": \"ins\", \"sub\": \"%s\", \"acc\": \"%s\", \"tcmp_per_s\": %.3f, "
+           "\"frac_of_R_int_at_1965MHz\": %.3f}\n", SUBK ? "imad" : "sub(viadd)", ACCK ? "imad.hi" : "dp4a", tcmp,
+           tcmp / (32.0 * sms * 1.965e9 / 1e12));
 }
 
 template <int D1, int D2, int D3, int O>
@@ -672,6 +771,10 @@ int main() {
     run<5, 1, 512, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
     run<5, 1, 256, 2, 1, 1>("pipelined_volatile/masks_from_smem+sync", g, sms, out, cyc);
     run<4, 1, 256, 2, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run_ins<0, 0>(g, sms, out);
+    run_ins<1, 0>(g, sms, out);
+    run_ins<0, 1>(g, sms, out);
+    run_ins<1, 1>(g, sms, out);
     run_chunk<16>(g, sms, out);
     run_chunk<24>(g, sms, out);
     run_gen<2, 2, 2, 0>(g, sms, out);
