@@ -1,0 +1,59 @@
+"""The driver's bench.py contract, checked on the device: one JSON line with the required keys and
+types for both arms (our kernels, and --impl reference = the CPU oracle), the roofline /
+cpu_baseline / e2e / clocks / gpu_launches objects, and consistent arithmetic (value = pairs per
+second of the timed steps)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_bench_line_contract():
+    d = _run("--steps", "3", "--warmup", "3")
+    for k, t in [("metric", str), ("value", float), ("unit", str), ("n_gpus", int), ("steps", int), ("warmup", int),
+                 ("ms_per_step", float), ("higher_is_better", bool), ("scaling", str), ("dtype", str),
+                 ("data", str), ("config", dict), ("roofline", dict), ("cpu_baseline", dict), ("e2e", dict),
+                 ("gpu_launches", int), ("clocks", dict)]:
+        assert isinstance(d[k], t), (k, d.get(k))
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["higher_is_better"] is True
+    assert d["vs_baseline"] is None and d["scaling"] == "weak" and "workload" in d["config"]
+    pairs = d["config"]["pairs_per_step"]
+    assert abs(d["value"] - pairs / (d["ms_per_step"] / 1e3)) / d["value"] < 1e-6
+    r = d["roofline"]
+    assert r["bound"] == "alu" and r["unit"] == "Tcmp/s" and 0.3 < r["frac"] < 1.0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and r["traffic"] and r["traffic"] > 0
+    c = d["cpu_baseline"]
+    assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_reference_arm_contract():
+    d = _run("--impl", "reference", "--steps", "1", "--warmup", "1")
+    assert d["impl"] == "reference" and d["metric"] and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
