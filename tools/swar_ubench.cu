@@ -360,6 +360,81 @@ __device__ __forceinline__ void step_gen(const uint32_t (&x)[8], const uint32_t 
 // Instruction-choice variants on the distance-2 schedule: SUBK 0 = sub.u32 (ptxas: VIADD),
 // 1 = mad.lo.u32 u * 1 + 0xFEFEFEFF (IMAD); ACCK 0 = dp4a, 1 = mad.hi.u32 v * 2^25 + acc (IMAD.HI,
 // lanes folded at the end -- exact for this benchmark's trip counts).
+// One CTA of 16 warps per SM (a 256 x 128 tile) against two CTAs of 8 warps (128 x 128), both with
+// the distance-2 schedule and masks from shared memory.
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) bench_big(const uint32_t* __restrict__ g, int reps, uint32_t* out) {
+    constexpr int RB = NT / 2;  // rows per tile: 128 (256 threads) or 256 (512 threads)
+    __shared__ __align__(16) uint32_t sA[16 * RB], sB[16 * 128], mA[16 * RB], mB[16 * 128];
+    for (int i = threadIdx.x; i < 16 * RB; i += NT) {
+        sA[i] = g[i % 4096];
+        mA[i] = sA[i] & 0x80808080u;
+    }
+    for (int i = threadIdx.x; i < 16 * 128; i += NT) {
+        sB[i] = g[4096 + i];
+        mB[i] = sB[i] & 0x80808080u;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int RG = RB / 64;  // row groups of 32 threads-rows: 2 or 4
+    const int tr = ((warp % RG) << 3) | (lane & 7);
+    const int tc = ((warp / RG) << 2) | (lane >> 3);
+    uint32_t acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int k = 0; k < 16; ++k) {
+            uint32_t x[8], y[8], xm[8], ym[8];
+            const uint4 xa = *reinterpret_cast<const uint4*>(sA + k * RB + 4 * tr);
+            const uint4 xb = *reinterpret_cast<const uint4*>(sA + k * RB + RB / 2 + 4 * tr);
+            const uint4 ya = *reinterpret_cast<const uint4*>(sB + k * 128 + 4 * tc);
+            const uint4 yb = *reinterpret_cast<const uint4*>(sB + k * 128 + 64 + 4 * tc);
+            const uint4 a = *reinterpret_cast<const uint4*>(mA + k * RB + 4 * tr);
+            const uint4 b = *reinterpret_cast<const uint4*>(mA + k * RB + RB / 2 + 4 * tr);
+            const uint4 c = *reinterpret_cast<const uint4*>(mB + k * 128 + 4 * tc);
+            const uint4 d = *reinterpret_cast<const uint4*>(mB + k * 128 + 64 + 4 * tc);
+            x[0] = xa.x; x[1] = xa.y; x[2] = xa.z; x[3] = xa.w; x[4] = xb.x; x[5] = xb.y; x[6] = xb.z; x[7] = xb.w;
+            y[0] = ya.x; y[1] = ya.y; y[2] = ya.z; y[3] = ya.w; y[4] = yb.x; y[5] = yb.y; y[6] = yb.z; y[7] = yb.w;
+            xm[0] = a.x; xm[1] = a.y; xm[2] = a.z; xm[3] = a.w; xm[4] = b.x; xm[5] = b.y; xm[6] = b.z; xm[7] = b.w;
+            ym[0] = c.x; ym[1] = c.y; ym[2] = c.z; ym[3] = c.w; ym[4] = d.x; ym[5] = d.y; ym[6] = d.z; ym[7] = d.w;
+            step_gen<2, 2, 2, 0>(x, y, xm, ym, acc);
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += acc[i][j] * (i * 8 + j + 1);
+    out[blockIdx.x * NT + threadIdx.x] = s;
+}
+
+template <int NT, int MINB>
+void run_big(const uint32_t* g, int sms, uint32_t* out) {
+    const int reps = 2000, blocks = sms * MINB;
+    bench_big<NT, MINB><<<blocks, NT>>>(g, 10, out);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int t = 0; t < 3; ++t) {
+        cudaEventRecord(e0);
+        bench_big<NT, MINB><<<blocks, NT>>>(g, reps, out);
+        cudaEventRecord(e1);
+        CK(cudaDeviceSynchronize());
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    const double tcmp = (double)blocks * NT * 64.0 * 16.0 * reps / (best * 1e-3) / 1e12;
+    printf("{\"variant\": \"big\", \"threads\": %d, \"ctas_per_sm\": %d, \"tcmp_per_s\": %.3f, "
+           "\"frac_of_R_int_at_1965MHz\": %.3f}\n", NT, MINB, tcmp, tcmp / (32.0 * sms * 1.965e9 / 1e12));
+}
+
 template <int SUBK, int ACCK>
 __device__ __forceinline__ void step_ins(const uint32_t (&x)[8], const uint32_t (&y)[8], const uint32_t (&xm)[8],
                                          const uint32_t (&ym)[8], uint32_t (&acc)[8][8], uint32_t one,
@@ -771,6 +846,10 @@ int main() {
     run<5, 1, 512, 1, 1>("pipelined_volatile/masks_from_smem", g, sms, out, cyc);
     run<5, 1, 256, 2, 1, 1>("pipelined_volatile/masks_from_smem+sync", g, sms, out, cyc);
     run<4, 1, 256, 2, 4>("iadd3_idp4a/masks_from_smem", g, sms, out, cyc);
+    run_big<256, 2>(g, sms, out);
+    run_big<512, 1>(g, sms, out);
+    run_big<256, 2>(g, sms, out);
+    run_big<512, 1>(g, sms, out);
     run_ins<0, 0>(g, sms, out);
     run_ins<1, 0>(g, sms, out);
     run_ins<0, 1>(g, sms, out);
