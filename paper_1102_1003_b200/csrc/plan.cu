@@ -311,38 +311,24 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         }
     }
     stable_sort_desc(segs, [](const Seg& x) { return x.cost; });
-    std::vector<Unit> units;  // this part's units, in deal order
-    {
-        int64_t at = 0;  // global index of the segment's first unit
-        for (const Seg& g : segs) {
-            const int64_t t0 = (((int64_t)part - at) % n_parts + n_parts) % n_parts;
-            if (g.ti >= 0) {
-                if (t0 == 0) units.push_back({g.rect, g.ti, -1, g.cost});
-            } else if (t0 < g.count) {
-                const Rect& r = P.rects[g.rect];
-                const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, TN);
-                int64_t t = 0, next = t0;  // unit index at the start of row i; next unit of this part
-                for (int i = 0; i < ta && next < g.count; ++i) {
-                    const int j0 = r.diag ? i * QD : 0;
-                    const int64_t row_n = tb - j0;
-                    while (next < t + row_n) {  // the row's tiles this part takes
-                        units.push_back({g.rect, i, (int32_t)(j0 + (next - t)), g.cost});
-                        next += n_parts;
-                    }
-                    t += row_n;
-                }
-            }
-            at += g.count;
-        }
-    }
     struct WorkC {
         Work w;
         int64_t cost;
     };
     std::vector<WorkC> work;
-    work.reserve(units.size() + 16);
-    for (size_t k = 0; k < units.size(); ++k) {
-        const Unit& u = units[k];
+    {  // capacity: this part's share of the tiles, split tiles counted per piece
+        int64_t items = 0;
+        for (const Rect& r : P.rects) {
+            const int64_t ta = ceil_div(r.n_rows, kTile), tb = ceil_div(r.n_cols, TN);
+            const int64_t nt = r.diag ? diag_tiles(r.n_rows, TN) : ta * tb;
+            const int64_t nk = r.W / kChunk;
+            const int64_t pieces = (r.acc && tile_cost(r) > 2 * target) ? std::min(nk, ceil_div(tile_cost(r), target)) : 1;
+            items += nt * pieces;
+        }
+        work.reserve((size_t)(items / n_parts + 1024));
+    }
+    // one unit of this part, in deal order: its algorithmic compares and its work items
+    auto emit = [&](const Unit& u) {
         const Rect& r = P.rects[u.rect];
         const int tb = (int)ceil_div(r.n_cols, TN);
         const int64_t rows = std::min<int64_t>(kTile, r.n_rows - (int64_t)u.ti * kTile);
@@ -385,8 +371,33 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 P.tile_compares += c;
             }
         }
+    };
+    {
+        int64_t at = 0;  // global index of the segment's first unit
+        for (const Seg& g : segs) {
+            const int64_t t0 = (((int64_t)part - at) % n_parts + n_parts) % n_parts;
+            if (g.ti >= 0) {
+                if (t0 == 0) emit(Unit{g.rect, g.ti, -1, g.cost});
+            } else if (t0 < g.count) {
+                const Rect& r = P.rects[g.rect];
+                const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, TN);
+                int64_t t = 0, next = t0;  // unit index at the start of row i; next unit of this part
+                for (int i = 0; i < ta && next < g.count; ++i) {
+                    const int j0 = r.diag ? i * QD : 0;
+                    const int64_t row_n = tb - j0;
+                    while (next < t + row_n) {  // the row's tiles this part takes
+                        emit(Unit{g.rect, i, (int32_t)(j0 + (next - t)), g.cost});
+                        next += n_parts;
+                    }
+                    t += row_n;
+                }
+            }
+            at += g.count;
+        }
     }
-    stable_sort_desc(work, [](const WorkC& x) { return x.cost; });
+    // units come in cost order; only split rows (pieces cheaper than their unit) can break it
+    if (!std::is_sorted(work.begin(), work.end(), [](const WorkC& x, const WorkC& y) { return x.cost > y.cost; }))
+        stable_sort_desc(work, [](const WorkC& x) { return x.cost; });
     // ---- the tail of the schedule: the last grid_cap items (the shortest, claimed last) are whole
     // tiles of ordinary rectangles; cut each into pieces along k so that the CTAs finish within a
     // piece of each other (C2: makespan/mean 1.046 -> 1.005 in the planner's cost model).  The
@@ -414,10 +425,13 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 else pieces.push_back(wc);
             }
         }
-        if (!P.tails.empty()) {
+        if (!P.tails.empty()) {  // everything before `begin` costs at least as much: re-sort the tail only
             P.tail_pieces = pcs;
-            work.insert(work.end(), pieces.begin(), pieces.end());
-            stable_sort_desc(work, [](const WorkC& x) { return x.cost; });
+            std::vector<WorkC> tail(work.begin() + (long)begin, work.end());
+            tail.insert(tail.end(), pieces.begin(), pieces.end());
+            stable_sort_desc(tail, [](const WorkC& x) { return x.cost; });
+            work.resize(begin);
+            work.insert(work.end(), tail.begin(), tail.end());
         }
     }
     P.work.reserve(work.size());
