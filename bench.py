@@ -291,6 +291,11 @@ def main():
                             f"(sm_max_mhz {src}); 4 integer instructions per 32-bit word compare",
                 "k2_share_of_step": float(np.mean([s["k2_ms"] for s in stats])) / (tot_ms / args.steps),
                 "k2_ms": k2_ms, "word_compares_per_launch": wc,
+                # executed = the kernel's tiles incl. padding (ragged edges, diagonal lower halves);
+                # tile_frac is the rate of the inner loop itself, frac the algorithmic one
+                "tile_compares_per_launch": int(stats[-1]["tile_compares"]),
+                "padding_frac": 1.0 - wc / max(int(stats[-1]["tile_compares"]), 1),
+                "tile_frac": int(stats[-1]["tile_compares"]) / (k2_ms / 1e3) / peak_cmp,
                 "logical_GBps": 8.0 * wc / (k2_ms / 1e3) / 1e9}
 
     e2e = None
