@@ -687,6 +687,22 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     uint64_t* sorted = nullptr;
     uint64_t* uniq = nullptr;
     int* n_uniq_d = nullptr;
+    int32_t *mark = nullptr, *rank = nullptr;
+    uint32_t* fbits = nullptr;
+    unsigned long long* cnt = nullptr;
+    uint64_t *keys = nullptr, *keys2 = nullptr;
+    unsigned long long* cursor = nullptr;
+    Scratch scratch(st);
+    scratch.own(&sorted);
+    scratch.own(&uniq);
+    scratch.own(&n_uniq_d);
+    scratch.own(&mark);
+    scratch.own(&rank);
+    scratch.own(&fbits);
+    scratch.own(&cnt);
+    scratch.own(&keys);
+    scratch.own(&keys2);
+    scratch.own(&cursor);
     BM_TRY(dalloc_t(&sorted, F, st));
     BM_TRY(dalloc_t(&uniq, F, st));
     BM_TRY(dalloc_t(&n_uniq_d, 1, st));
@@ -710,8 +726,6 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     k_fail_offsets<<<grid_for(n + 1, 256), 256, 0, st>>>(sorted, n_uniq_d, n, h->fail_off_d, h->f_d);
     h->launches += 1;
     BM_TRY(dalloc_t(&h->fail_tid_d, F, st));
-    int32_t *mark = nullptr, *rank = nullptr;
-    uint32_t* fbits = nullptr;
     BM_TRY(dalloc_t(&fbits, (m + 31) / 32, st));
     BM_CUDA(cudaMemsetAsync(fbits, 0, (m + 31) / 32 * sizeof(uint32_t), st));
     BM_TRY(dalloc_t(&mark, m + 1, st));
@@ -729,7 +743,6 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     k_fidx<<<grid_for(m, 256), 256, 0, st>>>(mark, rank, m, h->fidx_of_tid_d);
     h->launches += 1;
     // A_b: counts per failed tid (index < nft <= F; the rest stay 0), then (fidx, pos) keys sorted
-    unsigned long long* cnt = nullptr;
     BM_TRY(dalloc_t(&cnt, F + 1, st));
     BM_CUDA(cudaMemsetAsync(cnt, 0, (F + 1) * sizeof(unsigned long long), st));
     // one 128-entry step per warp: every gather chain and hit's binary search runs in parallel
@@ -755,8 +768,6 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     BM_CUDA(cudaStreamSynchronize(st));
     h->n_fail = n_uniq;
     h->n_ftid = nft;
-    uint64_t *keys = nullptr, *keys2 = nullptr;
-    unsigned long long* cursor = nullptr;
     BM_TRY(dalloc_t(&keys, total, st));
     BM_TRY(dalloc_t(&keys2, total, st));
     BM_TRY(dalloc_t(&cursor, 1, st));
@@ -775,16 +786,6 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     BM_TRY(dalloc_t(&h->ab_pos_d, total, st));
     k_low32<<<grid_for(total, 256), 256, 0, st>>>(keys2, total, h->ab_pos_d);
     h->launches += 1;
-    dfree(keys, st);
-    dfree(keys2, st);
-    dfree(cursor, st);
-    dfree(cnt, st);
-    dfree(mark, st);
-    dfree(fbits, st);
-    dfree(rank, st);
-    dfree(sorted, st);
-    dfree(uniq, st);
-    dfree(n_uniq_d, st);
     return BATMAP_OK;
 }
 
@@ -970,10 +971,21 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     int64_t* work_off_d = nullptr;
     uint8_t* lr_d = nullptr;
     uint32_t* work = nullptr;
+    GChunk* gchunks_d = nullptr;
+    uint64_t* fails = nullptr;
+    unsigned long long* fail_ctr = nullptr;
+    int* bad = nullptr;
+    Scratch scratch(st);
+    scratch.own(&work_off_d);
+    scratch.own(&lr_d);
+    scratch.own(&work);
+    scratch.own(&gchunks_d);
+    scratch.own(&fails);
+    scratch.own(&fail_ctr);
+    scratch.own(&bad);
     BM_TRY(dalloc_t(&work_off_d, n_big + 1, st));
     BM_TRY(dalloc_t(&lr_d, n, st));
     BM_TRY(dalloc_t(&work, work_entries, st));
-    GChunk* gchunks_d = nullptr;
     BM_TRY(dalloc_t(&gchunks_d, (int64_t)gchunks.size(), st));
     if (!gchunks.empty())
         BM_CUDA(cudaMemcpyAsync(gchunks_d, gchunks.data(), gchunks.size() * sizeof(GChunk), cudaMemcpyHostToDevice, st));
@@ -984,7 +996,6 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         BM_CUDA(cudaMemcpyAsync(lr_d, lr_pos.data(), n, cudaMemcpyHostToDevice, st));
     }
     if (o && (o->flags & BATMAP_CHECK_INPUT) && n) {
-        int* bad = nullptr;
         BM_TRY(dalloc_t(&bad, 1, st));
         BM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
         k1_check<<<grid_for(n * 32, 256), 256, 0, st>>>(offsets, tids, n, m, bad);
@@ -992,20 +1003,13 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         int bad_h = 0;
         BM_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
         BM_CUDA(cudaStreamSynchronize(st));
-        dfree(bad, st);
         if (bad_h) {
-            dfree(work_off_d, st);
-            dfree(lr_d, st);
-            dfree(work, st);
-            dfree(gchunks_d, st);
             set_error("invalid tidlists: every tidlist must be strictly increasing in [0, n_transactions)");
             return BATMAP_E_INVALID;
         }
     }
     // failure buffer: generous first guess, exact retry if exceeded (the build is deterministic)
     int64_t fail_cap = std::max<int64_t>(1 << 16, nnz / 16);
-    uint64_t* fails = nullptr;
-    unsigned long long* fail_ctr = nullptr;
     BM_TRY(dalloc_t(&fail_ctr, 1, st));
     int64_t F = 0;
     // per device (no process-wide flag: a process may drive several GPUs)
@@ -1091,6 +1095,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         F = (int64_t)Fh;
         if (F <= fail_cap) break;
         dfree(fails, st);
+        fails = nullptr;
         fail_cap = 2 * F + 1024;  // the concurrent build is not deterministic: leave headroom
     }
     h->n_fail = F;
@@ -1117,13 +1122,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         h->shard_pending = true;
     }
     BM_CUDA(cudaGetLastError());
-    dfree(fails, st);
-    dfree(fail_ctr, st);
-    dfree(work, st);
-    dfree(work_off_d, st);
-    dfree(lr_d, st);
-    dfree(gchunks_d, st);
-    rec(h, EV_B1, st);
+    rec(h, EV_B1, st);  // the scratch buffers are freed on return
     h->build_timed = true;
     h->stats.launches_build = h->launches - l0;
     return BATMAP_OK;
@@ -1171,6 +1170,8 @@ batmap_status shard_import(batmap_collection* h, const int64_t* offsets, const i
     int64_t F = 0;
     for (int p = 0; p < N; ++p) F += n_fails[p];
     uint64_t* fails = nullptr;
+    Scratch scratch(st);
+    scratch.own(&fails);
     BM_TRY(dalloc_t(&fails, std::max<int64_t>(F, 1), st));
     int64_t at = 0;
     for (int p = 0; p < N; ++p) {
@@ -1180,7 +1181,6 @@ batmap_status shard_import(batmap_collection* h, const int64_t* offsets, const i
         at += n_fails[p];
     }
     BM_TRY(post_failures(h, offsets, tids, h->nnz, fails, F, st));
-    dfree(fails, st);
     dfree(h->shard_fails_d, st);
     h->shard_fails_d = nullptr;
     h->shard_pending = false;

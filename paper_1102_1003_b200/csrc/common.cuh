@@ -213,6 +213,29 @@ template <typename T>
 batmap_status dalloc_t(T** p, int64_t count, cudaStream_t s) {
     return dalloc(reinterpret_cast<void**>(p), (size_t)(count > 0 ? count : 1) * sizeof(T), s);
 }
+// Frees a function's scratch buffers on every return path, early error returns included
+// (stream-ordered; each registered pointer is freed once and reset to nullptr).
+class Scratch {
+  public:
+    explicit Scratch(cudaStream_t s) : st_(s) {}
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    template <typename T>
+    void own(T** p) {
+        slots_[n_++] = reinterpret_cast<void**>(p);
+    }
+    ~Scratch() {
+        for (int i = 0; i < n_; ++i) {
+            dfree(*slots_[i], st_);
+            *slots_[i] = nullptr;
+        }
+    }
+
+  private:
+    cudaStream_t st_;
+    void** slots_[16];
+    int n_ = 0;
+};
 template <typename T>
 batmap_status ensure(T** p, int64_t* cap, int64_t need, cudaStream_t s) {
     if (*p && *cap >= need) return BATMAP_OK;

@@ -156,6 +156,11 @@ batmap_status sort_triples(batmap_triple* t, int64_t n, cudaStream_t st) {
     if (n <= 1) return BATMAP_OK;
     uint64_t* kb = nullptr;
     uint32_t* vb = nullptr;
+    void* tmp = nullptr;
+    Scratch scratch(st);
+    scratch.own(&kb);
+    scratch.own(&vb);
+    scratch.own(&tmp);
     BM_TRY(dalloc_t(&kb, 2 * n, st));
     BM_TRY(dalloc_t(&vb, 2 * n, st));
     k_triple_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(t, n, kb, vb);
@@ -163,14 +168,10 @@ batmap_status sort_triples(batmap_triple* t, int64_t n, cudaStream_t st) {
     cub::DoubleBuffer<uint32_t> dv(vb, vb + n);
     size_t tb = 0;
     BM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)n, 0, 64, st));
-    void* tmp = nullptr;
     BM_TRY(dalloc(&tmp, tb + 16, st));
     BM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)n, 0, 64, st));
     k3_emit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dk.Current(), dv.Current(), n, t);
     BM_CUDA(cudaGetLastError());
-    dfree(tmp, st);
-    dfree(kb, st);
-    dfree(vb, st);
     return BATMAP_OK;
 }
 

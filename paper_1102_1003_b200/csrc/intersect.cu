@@ -687,6 +687,9 @@ static batmap_status run_simple(batmap_collection* h, const Selection& sel, uint
                  (int32_t)sel.classes[a].first};
     int4* tiles_d = nullptr;
     SimpleClass* scls_d = nullptr;
+    Scratch scratch(st);
+    scratch.own(&tiles_d);
+    scratch.own(&scls_d);
     BM_TRY(dalloc_t(&tiles_d, n_tiles, st));
     BM_TRY(dalloc_t(&scls_d, (int64_t)sc.size(), st));
     BM_CUDA(cudaMemcpyAsync(tiles_d, tl.tiles.data(), n_tiles * sizeof(int4), cudaMemcpyHostToDevice, st));
@@ -708,8 +711,6 @@ static batmap_status run_simple(batmap_collection* h, const Selection& sel, uint
         rc = ensure_cand(h, (int64_t)cnt, st);
         if (rc != BATMAP_OK) break;
     }
-    dfree(tiles_d, st);
-    dfree(scls_d, st);
     return rc;
 }
 
