@@ -185,6 +185,20 @@ __global__ void __launch_bounds__(32) k1_small(
 // timing; the pair supports do not.  BATMAP_BUILD_SERIAL selects the deterministic
 // one-thread-per-item INSERT order instead (byte-identical to oracle/batmap_ref.py).
 constexpr int kConcThreads = 128;
+
+// Encode of the concurrent tiers: the thread of element x reads x's three slots, then rewrites
+// each slot that holds x as kTagged | byte, byte = (x also in table t+1 ? 0 : 1) << 7 | code
+// (Fig. 5).  Only x's thread writes x's slots, and a tagged slot (bit 31 set, low byte the entry)
+// never equals an element (element indices and tids are < 2^31), so the reads of the other
+// threads are unaffected.  Afterwards every slot is kEmpty (⊥) or tagged.
+constexpr uint32_t kTagged = 0x80000000u;
+__device__ __forceinline__ uint32_t pack_tagged(uint4 v) {
+    const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+    uint32_t word = 0;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) word |= (e[l] == kEmpty ? (uint32_t)kNullByte : (e[l] & 0xFFu)) << (8 * l);
+    return word;
+}
 constexpr int kConcFailCap = 512;  // per-item failure list in shared memory (overflow -> global rescan)
 
 __device__ __forceinline__ void record_failure(uint32_t* fl, int* nfl, uint64_t* fails, unsigned long long* fail_ctr,
@@ -261,24 +275,22 @@ __global__ void __launch_bounds__(kConcThreads) k1_conc_small(
     }
     __syncthreads();
     if (threadIdx.x == 0) fcount[pos] = nf;
-    const uint32_t sb = 3u * r0;
-    for (int w = threadIdx.x; w < W; w += blockDim.x) {
-        uint32_t word = 0;
+    // encode (Fig. 5) element by element, then pack
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        uint32_t q[3];
+        bool in[3];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) {
-            const uint32_t q = 4u * (uint32_t)w + l;
-            const uint32_t e = A[q];
-            uint32_t byte = kNullByte;
-            if (e != kEmpty) {
-                const int t = (int)((q % sb) >> log2r0);
-                const int t1 = (t + 1) % 3;
-                const uint32_t bit = (A[slot[t1 * maxS + e]] == e) ? 0u : 1u;  // Fig. 5
-                byte = (bit << 7) | code[t * maxS + e];
-            }
-            word |= byte << (8 * l);
+        for (int t = 0; t < 3; ++t) {
+            q[t] = slot[t * maxS + e];
+            in[t] = A[q[t]] == (uint32_t)e;
         }
-        arena_cls[(int64_t)w * n_pad + c] = word;
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+            if (in[t]) A[q[t]] = kTagged | (in[(t + 1) % 3] ? 0u : 0x80u) | code[t * maxS + e];
     }
+    __syncthreads();
+    for (int w = threadIdx.x; w < W; w += blockDim.x)
+        arena_cls[(int64_t)w * n_pad + c] = pack_tagged(reinterpret_cast<const uint4*>(A)[w]);
 }
 
 // Concurrent tier for medium tables (kSmallMaxR < r <= kClusterMaxR): one thread-block cluster
@@ -306,6 +318,9 @@ __device__ __forceinline__ uint32_t cl_ld(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
     return v;
+}
+__device__ __forceinline__ void cl_st(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 template <int CS, int NT>
@@ -350,6 +365,16 @@ __global__ void __launch_bounds__(NT) k1_conc_cluster(
         uint32_t a;
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(T_loc + 4u * off), "r"(k));
         return cl_ld(a);
+    };
+    auto store = [&](uint32_t q, uint32_t v) {
+        const uint32_t k = owner(q), off = q - k * slice;
+        if (CS == 1 || k == rank) {
+            T[off] = v;
+            return;
+        }
+        uint32_t a;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(T_loc + 4u * off), "r"(k));
+        cl_st(a, v);
     };
     for (uint32_t q = threadIdx.x; q < slice; q += NT) T[q] = kEmpty;
     if (threadIdx.x == 0) {
@@ -403,29 +428,27 @@ __global__ void __launch_bounds__(NT) k1_conc_cluster(
     }
     if (CS > 1) cl.sync();
     else __syncthreads();
-    // encode the words of this CTA's slice into the word-major class block
-    const uint32_t sb = 3u * r0;
-    const uint32_t q0 = rank * slice;
-    for (uint32_t wl = threadIdx.x; wl < slice / 4; wl += NT) {
-        const uint4 e4 = reinterpret_cast<const uint4*>(T)[wl];
-        const uint32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};
-        uint32_t word = 0;
+    // encode (Fig. 5) element by element, then every CTA packs the words of its slice
+    for (int e = (int)rank * NT + threadIdx.x; e < n; e += CS * NT) {
+        const uint32_t x = (uint32_t)__ldg(S + e);
+        uint32_t q[3], code[3];
+        bool in[3];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) {
-            const uint32_t x = xs[l];
-            uint32_t byte = kNullByte;
-            if (x != kEmpty) {
-                const uint32_t q = q0 + 4u * wl + l;
-                const int t = (int)((q % sb) >> log2r0);  // table of entry q
-                const uint32_t code = pi_eval(P, t, x) >> P.s;
-                const int t1 = (t + 1) % 3;
-                const uint32_t bit = (load(slot_of(t1, pi_eval(P, t1, x), r, r0, log2r0)) == x) ? 0u : 1u;  // Fig. 5
-                byte = (bit << 7) | code;
-            }
-            word |= byte << (8 * l);
+        for (int t = 0; t < 3; ++t) {
+            const uint32_t v = pi_eval(P, t, x);
+            q[t] = slot_of(t, v, r, r0, log2r0);
+            code[t] = v >> P.s;
+            in[t] = load(q[t]) == x;
         }
-        arena_cls[(int64_t)(q0 / 4 + wl) * n_pad + c] = word;
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+            if (in[t]) store(q[t], kTagged | (in[(t + 1) % 3] ? 0u : 0x80u) | code[t]);
     }
+    if (CS > 1) cl.sync();
+    else __syncthreads();
+    const uint32_t q0 = rank * slice;
+    for (uint32_t wl = threadIdx.x; wl < slice / 4; wl += NT)
+        arena_cls[(int64_t)(q0 / 4 + wl) * n_pad + c] = pack_tagged(reinterpret_cast<const uint4*>(T)[wl]);
     if (CS > 1) cl.sync();  // no CTA may exit while another still reads its slice
 }
 
@@ -822,12 +845,18 @@ static batmap_status launch_cluster_tier(batmap_collection* h, const ClassInfo& 
                                          const int32_t* tids, uint64_t* fails, unsigned long long* fail_ctr,
                                          int64_t fail_cap, cudaStream_t st) {
     const int64_t bytes = 12ll * c.r;
-    if (c.r <= 4096) return launch_cluster<1, 256>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
-    if (bytes <= kClSliceBytesMax) return launch_cluster<1, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
-    if (bytes <= 2ll * kClSliceBytesMax)
-        return launch_cluster<2, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
-    if (bytes <= 4ll * kClSliceBytesMax)
-        return launch_cluster<4, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    int cs = bytes <= kClSliceBytesMax ? 1 : bytes <= 2ll * kClSliceBytesMax ? 2 : bytes <= 4ll * kClSliceBytesMax ? 4 : 8;
+    // a class of few items would leave most SMs idle: spread each item over more CTAs (and threads),
+    // which shortens every thread's chain of dependent swaps (C3: 11 items of r = 2^15)
+    // (BATMAP_K1_SPREAD=0 keeps the smallest cluster: test hook for every cluster size)
+    const char* sp = getenv("BATMAP_K1_SPREAD");
+    const bool spread = !(sp && sp[0] == '0');
+    while (spread && cs < 8 && (int64_t)c.n * cs * 2 <= h->num_sms) cs *= 2;
+    const bool narrow = c.r <= 4096 && cs == 1 && (!spread || c.n >= h->num_sms);
+    if (narrow) return launch_cluster<1, 256>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    if (cs == 1) return launch_cluster<1, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    if (cs == 2) return launch_cluster<2, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    if (cs == 4) return launch_cluster<4, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
     return launch_cluster<8, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
 }
 

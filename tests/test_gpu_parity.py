@@ -179,8 +179,12 @@ def _tiers(seed, m=300000):
     return off, np.concatenate(rows), m
 
 
+@pytest.mark.parametrize("spread", ["0", "1"])
 @pytest.mark.parametrize("max_loop", [0, 1])
-def test_cluster_and_global_tiers(max_loop):
+def test_cluster_and_global_tiers(max_loop, spread, monkeypatch):
+    # spread=0: the smallest cluster per table size (1, 2, 4, 8 CTAs); spread=1 (default): these
+    # one-item classes spread over clusters of 8
+    monkeypatch.setenv("BATMAP_K1_SPREAD", spread)
     off, tids, m = _tiers(21)
     c = _coll(off, tids, m, seed=6, max_loop=max_loop)
     rs = sorted({len(c.export_entries(i)) // 3 for i in range(len(off) - 1)})

@@ -35,7 +35,8 @@ tids = np.concatenate(rows)
 n = len(rows)
 ref = oracle.pairs_horizontal(off, tids, m, threshold=2)
 o, t = torch.as_tensor(off).cuda(), torch.as_tensor(tids).cuda()
-for serial in (False, True):
+for serial, spread in ((False, "0"), (False, "1"), (True, "1")):
+    os.environ["BATMAP_K1_SPREAD"] = spread  # "0": smallest clusters (1/2/4 CTAs); "1": clusters of 8
     c = Collection(o, t, m, seed=3, max_loop=2, serial=serial)  # forced failures exercise K3
     got = c.pair_supports(threshold=2).cpu().numpy().astype(np.uint32)
     assert np.array_equal(got, ref)
@@ -43,6 +44,7 @@ for serial in (False, True):
     got = c.pair_supports(torch.as_tensor(sub).cuda(), threshold=2).cpu().numpy().astype(np.uint32)
     assert np.array_equal(got, oracle.pairs_horizontal(off, tids, m, items=sub, threshold=2))
     c.close()
+os.environ.pop("BATMAP_K1_SPREAD")
 # sharded build, two parts exchanged in this process
 parts = [Collection(o, t, m, seed=4, max_loop=2, part=p, n_parts=2) for p in range(2)]
 sw = max(parts[0].shard_sizes(p)[0] for p in range(2))
