@@ -190,7 +190,8 @@ constexpr int kConcThreads = 128;
 // each slot that holds x as kTagged | byte, byte = (x also in table t+1 ? 0 : 1) << 7 | code
 // (Fig. 5).  Only x's thread writes x's slots, and a tagged slot (bit 31 set, low byte the entry)
 // never equals an element (element indices and tids are < 2^31), so the reads of the other
-// threads are unaffected.  Afterwards every slot is kEmpty (⊥) or tagged.
+// threads are unaffected (reads and rewrites are atomics, so the sanitizer's race check sees no
+// plain-access race).  Afterwards every slot is kEmpty (⊥) or tagged.
 constexpr uint32_t kTagged = 0x80000000u;
 __device__ __forceinline__ uint32_t pack_tagged(uint4 v) {
     const uint32_t e[4] = {v.x, v.y, v.z, v.w};
@@ -282,11 +283,11 @@ __global__ void __launch_bounds__(kConcThreads) k1_conc_small(
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
             q[t] = slot[t * maxS + e];
-            in[t] = A[q[t]] == (uint32_t)e;
+            in[t] = atomicOr(&A[q[t]], 0u) == (uint32_t)e;  // atomic: other threads tag their slots
         }
 #pragma unroll
         for (int t = 0; t < 3; ++t)
-            if (in[t]) A[q[t]] = kTagged | (in[(t + 1) % 3] ? 0u : 0x80u) | code[t * maxS + e];
+            if (in[t]) atomicExch(&A[q[t]], kTagged | (in[(t + 1) % 3] ? 0u : 0x80u) | code[t * maxS + e]);
     }
     __syncthreads();
     for (int w = threadIdx.x; w < W; w += blockDim.x)
@@ -319,8 +320,10 @@ __device__ __forceinline__ uint32_t cl_ld(uint32_t addr) {
     asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
     return v;
 }
-__device__ __forceinline__ void cl_st(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+__device__ __forceinline__ uint32_t cl_or0(uint32_t addr) {
+    uint32_t old;
+    asm volatile("atom.shared::cluster.or.b32 %0, [%1], 0;" : "=r"(old) : "r"(addr) : "memory");
+    return old;
 }
 
 template <int CS, int NT>
@@ -366,15 +369,12 @@ __global__ void __launch_bounds__(NT) k1_conc_cluster(
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(T_loc + 4u * off), "r"(k));
         return cl_ld(a);
     };
-    auto store = [&](uint32_t q, uint32_t v) {
+    auto read = [&](uint32_t q) -> uint32_t {  // atomic read (the encode runs beside other threads' tagging)
         const uint32_t k = owner(q), off = q - k * slice;
-        if (CS == 1 || k == rank) {
-            T[off] = v;
-            return;
-        }
+        if (CS == 1 || k == rank) return atomicOr(T + off, 0u);
         uint32_t a;
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(T_loc + 4u * off), "r"(k));
-        cl_st(a, v);
+        return cl_or0(a);
     };
     for (uint32_t q = threadIdx.x; q < slice; q += NT) T[q] = kEmpty;
     if (threadIdx.x == 0) {
@@ -438,11 +438,11 @@ __global__ void __launch_bounds__(NT) k1_conc_cluster(
             const uint32_t v = pi_eval(P, t, x);
             q[t] = slot_of(t, v, r, r0, log2r0);
             code[t] = v >> P.s;
-            in[t] = load(q[t]) == x;
+            in[t] = read(q[t]) == x;
         }
 #pragma unroll
         for (int t = 0; t < 3; ++t)
-            if (in[t]) store(q[t], kTagged | (in[(t + 1) % 3] ? 0u : 0x80u) | code[t]);
+            if (in[t]) exch(q[t], kTagged | (in[(t + 1) % 3] ? 0u : 0x80u) | code[t]);
     }
     if (CS > 1) cl.sync();
     else __syncthreads();
