@@ -785,10 +785,12 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     int n_uniq = 0;
     int32_t nft = 0;
     int64_t total = 0;
-    BM_CUDA(cudaMemcpyAsync(&n_uniq, n_uniq_d, sizeof(int), cudaMemcpyDeviceToHost, st));
-    BM_CUDA(cudaMemcpyAsync(&nft, rank + m, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    BM_CUDA(cudaMemcpyAsync(&total, h->ab_off_d + F, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    BM_CUDA(cudaStreamSynchronize(st));
+    {
+        const void* src[3] = {n_uniq_d, rank + m, h->ab_off_d + F};
+        const size_t bytes[3] = {sizeof(int), sizeof(int32_t), sizeof(int64_t)};
+        void* dst[3] = {&n_uniq, &nft, &total};
+        BM_TRY(read_scalars(st, 3, src, bytes, dst));
+    }
     h->n_fail = n_uniq;
     h->n_ftid = nft;
     BM_TRY(dalloc_t(&keys, total, st));
@@ -1030,8 +1032,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         k1_check<<<grid_for(n * 32, 256), 256, 0, st>>>(offsets, tids, n, m, bad);
         h->launches += 1;
         int bad_h = 0;
-        BM_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-        BM_CUDA(cudaStreamSynchronize(st));
+        BM_TRY(read_scalar(st, bad, &bad_h));
         if (bad_h) {
             set_error("invalid tidlists: every tidlist must be strictly increasing in [0, n_transactions)");
             return BATMAP_E_INVALID;
@@ -1119,8 +1120,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         // plan the intersection of the full selection on the host while the build kernels run
         if (attempt == 0) BM_TRY(prepare_full_k2(h, part, n_parts, st));
         unsigned long long Fh = 0;
-        BM_CUDA(cudaMemcpyAsync(&Fh, fail_ctr, sizeof(Fh), cudaMemcpyDeviceToHost, st));
-        BM_CUDA(cudaStreamSynchronize(st));
+        BM_TRY(read_scalar(st, fail_ctr, &Fh));
         F = (int64_t)Fh;
         if (F <= fail_cap) break;
         dfree(fails, st);

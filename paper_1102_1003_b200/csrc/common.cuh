@@ -209,6 +209,15 @@ inline void rec(batmap_collection* h, int idx, cudaStream_t st) {
 // allocation helpers (stream-ordered pool)
 batmap_status dalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
+// k scalar device -> host copies (each <= 8 bytes) then one synchronisation of st
+batmap_status read_scalars(cudaStream_t st, int k, const void* const* src, const size_t* bytes, void* const* dst);
+template <typename T>
+batmap_status read_scalar(cudaStream_t st, const T* src, T* dst) {
+    const void* s[1] = {src};
+    const size_t b[1] = {sizeof(T)};
+    void* d[1] = {dst};
+    return read_scalars(st, 1, s, b, d);
+}
 template <typename T>
 batmap_status dalloc_t(T** p, int64_t count, cudaStream_t s) {
     return dalloc(reinterpret_cast<void**>(p), (size_t)(count > 0 ? count : 1) * sizeof(T), s);

@@ -120,8 +120,7 @@ batmap_status run_finalize(batmap_collection* h, const Selection& sel, int64_t n
         h->ctr_d + 1);
     BM_CUDA(cudaGetLastError());
     unsigned long long cnt = 0;
-    BM_CUDA(cudaMemcpyAsync(&cnt, h->ctr_d + 1, sizeof(cnt), cudaMemcpyDeviceToHost, st));
-    BM_CUDA(cudaStreamSynchronize(st));
+    BM_TRY(read_scalar(st, h->ctr_d + 1, &cnt));
     const int64_t K = (int64_t)cnt;
     *n_res = K;
     BM_TRY(ensure(&h->res_d, &h->res_cap, std::max<int64_t>(K, 1), st));

@@ -705,8 +705,7 @@ static batmap_status run_simple(batmap_collection* h, const Selection& sel, uint
         h->launches += 1;
         BM_CUDA(cudaGetLastError());
         unsigned long long cnt = 0;
-        BM_CUDA(cudaMemcpyAsync(&cnt, h->ctr_d, sizeof(cnt), cudaMemcpyDeviceToHost, st));
-        BM_CUDA(cudaStreamSynchronize(st));
+        BM_TRY(read_scalar(st, h->ctr_d, &cnt));
         *n_cand = (int64_t)cnt;
         if ((int64_t)cnt <= h->cand_cap) break;
         rc = ensure_cand(h, (int64_t)cnt, st);
@@ -981,8 +980,7 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
             break;
         }
         unsigned long long cnt = 0;
-        BM_CUDA(cudaMemcpyAsync(&cnt, h->ctr_d, sizeof(cnt), cudaMemcpyDeviceToHost, st));
-        BM_CUDA(cudaStreamSynchronize(st));
+        BM_TRY(read_scalar(st, h->ctr_d, &cnt));
         *n_cand = (int64_t)cnt;
         if ((int64_t)cnt <= h->cand_cap) break;
         rc = ensure_cand(h, (int64_t)cnt, st);

@@ -1,6 +1,7 @@
 // util.cu -- errors, allocation, π parameters.
 #include <stdarg.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -30,6 +31,30 @@ batmap_status dalloc(void** p, size_t bytes, cudaStream_t s) {
 
 void dfree(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
+}
+
+// Scalar readbacks through a small pinned buffer (one per host thread, allocated once): the
+// copies are queued without blocking the host and one stream synchronisation covers them all;
+// device -> pageable copies would each block until the stream drains.
+batmap_status read_scalars(cudaStream_t st, int k, const void* const* src, const size_t* bytes, void* const* dst) {
+    static thread_local uint64_t* pin = nullptr;
+    static thread_local bool tried = false;
+    if (!tried) {
+        tried = true;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&pin), 16 * sizeof(uint64_t), cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            pin = nullptr;
+        }
+    }
+    for (int i = 0; i < k; ++i) {
+        void* to = pin && k <= 16 && bytes[i] <= 8 ? static_cast<void*>(pin + i) : dst[i];
+        BM_CUDA(cudaMemcpyAsync(to, src[i], bytes[i], cudaMemcpyDeviceToHost, st));
+    }
+    BM_CUDA(cudaStreamSynchronize(st));
+    if (pin && k <= 16)
+        for (int i = 0; i < k; ++i)
+            if (bytes[i] <= 8) memcpy(dst[i], pin + i, bytes[i]);
+    return BATMAP_OK;
 }
 
 static uint64_t splitmix64(uint64_t x) {
