@@ -205,7 +205,7 @@ def main():
     import torch.distributed as dist
 
     from paper_1102_1003_b200 import Collection, batmap, mine_host
-    from paper_1102_1003_b200.dist import build_distributed, gather_triples
+    from paper_1102_1003_b200.dist import build_distributed, gather_triples, mine_distributed
 
     # test hooks (not used by the driver): run several ranks on one GPU over gloo
     dev_idx = int(os.environ.get("BENCH_FORCE_DEVICE", local_rank))
@@ -323,6 +323,33 @@ def main():
         e2e = {"value": pairs / (np.mean(e_ms) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(w.offsets.nbytes + w.tids.nbytes), "d2h_bytes_per_step": int(K * 12),
                "ms_per_step": float(np.mean(e_ms)), "api": "batmap_mine_host (host buffers)"}
+    if world > 1 and not args.no_e2e:  # every rank: H2D of the CSR, sharded build, pairs, gather, D2H on rank 0
+        import torch as _t
+
+        off_h = _t.from_numpy(np.ascontiguousarray(w.offsets)).pin_memory()
+        tids_h = _t.from_numpy(np.ascontiguousarray(w.tids)).pin_memory()
+        for _ in range(2):
+            r = mine_distributed(off_h, tids_h, w.m, threshold=w.threshold, device=dev, seed=1)
+        e_ms = []
+        for _ in range(max(3, args.steps // 4)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r = mine_distributed(off_h, tids_h, w.m, threshold=w.threshold, device=dev, seed=1)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        t = torch.tensor([float(np.sum(e_ms))], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_tot = float(t.item())
+        if rank == 0:
+            assert r.shape[0] == K
+            e2e = {"value": pairs * len(e_ms) / (e_tot / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(world * (w.offsets.nbytes + w.tids.nbytes)),
+                   "d2h_bytes_per_step": int(K * 12), "ms_per_step": e_tot / len(e_ms),
+                   "api": "dist.mine_distributed (host buffers on every rank; max over ranks)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(w)
 

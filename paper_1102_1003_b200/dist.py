@@ -80,3 +80,31 @@ def pair_supports_distributed(coll, items=None, threshold: int = 1, dst: int = 0
     if allp is None:
         return None
     return sort_triples(allp)
+
+
+def mine_distributed(offsets, tids, n_transactions: int, threshold: int = 1, dst: int = 0, group=None,
+                     device=None, **kw):
+    """End to end from host buffers at N ranks (the multi-GPU counterpart of mine_host): every rank
+    copies the vertical CSR (pinned host memory preferred) to its GPU, runs the sharded build and
+    its share of the pairs, and `dst` receives the gathered, sorted triples as a host int32
+    [K, 3] array (None on the other ranks)."""
+    import numpy as np
+
+    from .batmap import sort_triples
+
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    off_d = torch.as_tensor(offsets).to(dev, non_blocking=True)
+    tids_d = torch.as_tensor(tids).to(dev, non_blocking=True)
+    c = build_distributed(off_d, tids_d, n_transactions, group=group, **kw)
+    try:
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        local = c.pair_supports(None, threshold, part=rank, n_parts=world)
+        if dist.get_backend(group) != "nccl":
+            local = local.cpu()  # gloo (tests): host staging
+        allp = gather_triples(local, dst=dst, group=group)
+        if allp is None:
+            return None
+        return np.asarray(sort_triples(allp.to(dev)).cpu())
+    finally:
+        c.close()
