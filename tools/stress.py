@@ -2,7 +2,7 @@
 random shapes (uniform or Zipf tidlists, a few long items to reach the cluster and global build
 tiers), forced insertion failures, item subsets, both K1 cluster policies and both K2 tile widths.
 The concurrent build is timing-dependent (reading #9b), so rare interleavings only show up over
-many runs; every run must be bit-exact.
+many runs; every run must be bit-exact.  (K1 side stream on/off too.)
 
     python tools/stress.py [seconds]
 """
@@ -49,6 +49,7 @@ def main():
         n = len(off) - 1
         os.environ["BATMAP_K1_SPREAD"] = str(int(rng.integers(0, 2)))
         os.environ["BATMAP_K2_TN"] = str(int(rng.choice([64, 128])))
+        os.environ["BATMAP_K1_SIDE"] = str(int(rng.integers(0, 2)))
         max_loop = int(rng.choice([0, 0, 1, 2]))
         thr = int(rng.choice([1, 2, 3, 10]))
         items = None
