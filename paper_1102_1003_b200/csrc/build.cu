@@ -10,6 +10,8 @@
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace bm {
@@ -878,6 +880,10 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     std::vector<int64_t> off_h(n + 1);
     if (offsets_host) {  // host copy supplied (batmap_mine_host): no read-back, planning overlaps the upload
         std::copy(offsets_host, offsets_host + n + 1, off_h.begin());
+    } else if (void* pin = host_staging((size_t)(n + 1) * sizeof(int64_t))) {
+        BM_CUDA(cudaMemcpyAsync(pin, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        memcpy(off_h.data(), pin, (n + 1) * sizeof(int64_t));
     } else {
         BM_CUDA(cudaMemcpyAsync(off_h.data(), offsets, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         BM_CUDA(cudaStreamSynchronize(st));
@@ -1018,13 +1024,31 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     BM_TRY(dalloc_t(&lr_d, n, st));
     BM_TRY(dalloc_t(&work, work_entries, st));
     BM_TRY(dalloc_t(&gchunks_d, (int64_t)gchunks.size(), st));
-    if (!gchunks.empty())
-        BM_CUDA(cudaMemcpyAsync(gchunks_d, gchunks.data(), gchunks.size() * sizeof(GChunk), cudaMemcpyHostToDevice, st));
-    if (n) {
-        BM_CUDA(cudaMemcpyAsync(h->pos2orig_d, h->pos2orig_h.data(), n * 4, cudaMemcpyHostToDevice, st));
-        BM_CUDA(cudaMemcpyAsync(h->orig2pos_d, h->orig2pos_h.data(), n * 4, cudaMemcpyHostToDevice, st));
-        BM_CUDA(cudaMemcpyAsync(work_off_d, work_off.data(), (n_big + 1) * 8, cudaMemcpyHostToDevice, st));
-        BM_CUDA(cudaMemcpyAsync(lr_d, lr_pos.data(), n, cudaMemcpyHostToDevice, st));
+    {  // host tables -> device, staged through pinned memory (asynchronous copies)
+        struct Up {
+            void* dst;
+            const void* src;
+            size_t bytes;
+        };
+        const Up ups[5] = {{gchunks_d, gchunks.data(), gchunks.size() * sizeof(GChunk)},
+                           {h->pos2orig_d, h->pos2orig_h.data(), (size_t)n * 4},
+                           {h->orig2pos_d, h->orig2pos_h.data(), (size_t)n * 4},
+                           {work_off_d, work_off.data(), n ? (size_t)(n_big + 1) * 8 : 0},
+                           {lr_d, lr_pos.data(), (size_t)n}};
+        size_t total = 0;
+        for (const Up& u : ups) total += (u.bytes + 15) / 16 * 16;
+        char* pin = static_cast<char*>(host_staging(total));
+        size_t at = 0;
+        for (const Up& u : ups) {
+            if (!u.bytes) continue;
+            const void* from = u.src;
+            if (pin) {
+                memcpy(pin + at, u.src, u.bytes);
+                from = pin + at;
+                at += (u.bytes + 15) / 16 * 16;
+            }
+            BM_CUDA(cudaMemcpyAsync(u.dst, from, u.bytes, cudaMemcpyHostToDevice, st));
+        }
     }
     if (o && (o->flags & BATMAP_CHECK_INPUT) && n) {
         BM_TRY(dalloc_t(&bad, 1, st));

@@ -209,6 +209,7 @@ inline void rec(batmap_collection* h, int idx, cudaStream_t st) {
 // allocation helpers (stream-ordered pool)
 batmap_status dalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
+void* host_staging(size_t bytes);
 // k scalar device -> host copies (each <= 8 bytes) then one synchronisation of st
 batmap_status read_scalars(cudaStream_t st, int k, const void* const* src, const size_t* bytes, void* const* dst);
 template <typename T>

@@ -33,6 +33,27 @@ void dfree(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
+// Per-thread pinned staging for the build's small host <-> device arrays (grown on demand, kept
+// for the thread's lifetime).  Copies from / to it are asynchronous; every build synchronises its
+// stream (the failure count) before it returns, so the next build of the thread never overwrites
+// bytes still in flight.  Returns nullptr (callers fall back to pageable copies) if pinning fails.
+void* host_staging(size_t bytes) {
+    static thread_local void* buf = nullptr;
+    static thread_local size_t cap = 0;
+    if (bytes <= cap) return buf;
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 2 + 4096;
+    if (cudaHostAlloc(&buf, want, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        buf = nullptr;
+        return nullptr;
+    }
+    cap = want;
+    return buf;
+}
+
 // Scalar readbacks through a small pinned buffer (one per host thread, allocated once): the
 // copies are queued without blocking the host and one stream synchronisation covers them all;
 // device -> pageable copies would each block until the stream drains.
