@@ -619,14 +619,14 @@ __global__ void __launch_bounds__(256) k1_gchunk_cleanup(
 
 // Flat over the CSR entries, 4 per thread per step so that the fidx gathers of a thread are
 // independent (the pass is latency-bound otherwise).  An entry whose tid failed somewhere
-// (fidx >= 0, rare) finds its item by binary search in offsets, then counts / emits
-// (fidx << 32 | pos); emits take one cursor atomic per warp.
-template <bool kEmit>
+// (fidx >= 0, rare) finds its item by binary search in offsets and emits (fidx << 32 | pos);
+// emits take one cursor atomic per warp.  Writes beyond `cap` are dropped (the caller re-runs
+// with the exact count, which the cursor holds either way).
 __global__ void __launch_bounds__(256) k_ab_scan(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
                                                  const int32_t* __restrict__ orig2pos, int64_t n, int64_t nnz,
                                                  const int32_t* __restrict__ fidx, const uint32_t* __restrict__ fbits,
-                                                 unsigned long long* __restrict__ cnt,
-                                                 uint64_t* __restrict__ keys, unsigned long long* __restrict__ cursor) {
+                                                 uint64_t* __restrict__ keys, unsigned long long* __restrict__ cursor,
+                                                 int64_t cap) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
     for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4 - lane * 4 + lane;
@@ -646,16 +646,12 @@ __global__ void __launch_bounds__(256) k_ab_scan(const int64_t* __restrict__ off
         for (int q = 0; q < 4; ++q) {
             const int64_t k = base + 32 * q;
             const bool hit = f[q] >= 0;
-            if (!kEmit) {
-                if (hit) atomicAdd(cnt + f[q], 1ull);
-                continue;
-            }
             const unsigned mask = __ballot_sync(0xFFFFFFFFu, hit);
             if (!mask) continue;
             unsigned long long at = 0;
             if (lane == __ffs(mask) - 1) at = atomicAdd(cursor, (unsigned long long)__popc(mask));
             at = __shfl_sync(0xFFFFFFFFu, at, __ffs(mask) - 1) + __popc(mask & ((1u << lane) - 1));
-            if (hit) {
+            if (hit && (int64_t)at < cap) {
                 int64_t lo = 0, hi = n - 1;  // last item with offsets[item] <= k
                 while (lo < hi) {
                     const int64_t mid = (lo + hi + 1) >> 1;
@@ -666,6 +662,20 @@ __global__ void __launch_bounds__(256) k_ab_scan(const int64_t* __restrict__ off
             }
         }
     }
+}
+
+// A_b offsets from the (fidx, pos)-sorted keys: ab_off[k] = first key of failed tid k (k <= nft).
+__global__ void k_ab_offsets(const uint64_t* __restrict__ keys, int64_t total, int64_t nft, int64_t* __restrict__ off) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > nft) return;
+    int64_t lo = 0, hi = total;
+    const uint64_t key = (uint64_t)k << 32;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    off[k] = lo;
 }
 
 __global__ void k_low32(const uint64_t* __restrict__ keys, int64_t n, int32_t* __restrict__ out) {
@@ -714,7 +724,6 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     int* n_uniq_d = nullptr;
     int32_t *mark = nullptr, *rank = nullptr;
     uint32_t* fbits = nullptr;
-    unsigned long long* cnt = nullptr;
     uint64_t *keys = nullptr, *keys2 = nullptr;
     unsigned long long* cursor = nullptr;
     Scratch scratch(st);
@@ -724,7 +733,6 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     scratch.own(&mark);
     scratch.own(&rank);
     scratch.own(&fbits);
-    scratch.own(&cnt);
     scratch.own(&keys);
     scratch.own(&keys2);
     scratch.own(&cursor);
@@ -767,41 +775,34 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     }
     k_fidx<<<grid_for(m, 256), 256, 0, st>>>(mark, rank, m, h->fidx_of_tid_d);
     h->launches += 1;
-    // A_b: counts per failed tid (index < nft <= F; the rest stay 0), then (fidx, pos) keys sorted
-    BM_TRY(dalloc_t(&cnt, F + 1, st));
-    BM_CUDA(cudaMemsetAsync(cnt, 0, (F + 1) * sizeof(unsigned long long), st));
-    // one 128-entry step per warp: every gather chain and hit's binary search runs in parallel
+    // A_b: one pass over the CSR emits (fidx << 32 | pos) for every entry whose tid failed,
+    // into a buffer sized by a guess (F failed elements x 4 x the mean item count of a tid); the one
+    // synchronisation reads the exact count, and an overflow re-runs the pass at that size
     const unsigned scan_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(nnz, 1024), 1 << 30));
-    k_ab_scan<false><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, fbits, cnt, nullptr,
-                                                nullptr);
-    h->launches += 1;
-    BM_TRY(dalloc_t(&h->ab_off_d, F + 1, st));
-    {
-        int64_t* c64 = reinterpret_cast<int64_t*>(cnt);
-        size_t tb = 0;
-        BM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c64, h->ab_off_d, (int)(F + 1), st));
-        BM_TRY(cub_tmp(h, tb, st));
-        BM_CUDA(cub::DeviceScan::ExclusiveSum(h->cub_tmp, tb, c64, h->ab_off_d, (int)(F + 1), st));
-        h->launches += 1;
-    }
+    int64_t cap = std::max<int64_t>(4096, 4 * F * std::max<int64_t>(1, nnz / std::max<int64_t>(m, 1)) + 1024);
+    cap = std::min<int64_t>(cap, std::max<int64_t>(nnz, 1));
+    BM_TRY(dalloc_t(&cursor, 1, st));
     int n_uniq = 0;
     int32_t nft = 0;
     int64_t total = 0;
-    {
-        const void* src[3] = {n_uniq_d, rank + m, h->ab_off_d + F};
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        BM_TRY(dalloc_t(&keys, cap, st));
+        BM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+        k_ab_scan<<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, fbits, keys,
+                                              cursor, cap);
+        h->launches += 1;
+        const void* src[3] = {n_uniq_d, rank + m, cursor};
         const size_t bytes[3] = {sizeof(int), sizeof(int32_t), sizeof(int64_t)};
         void* dst[3] = {&n_uniq, &nft, &total};
         BM_TRY(read_scalars(st, 3, src, bytes, dst));
+        if (total <= cap) break;
+        dfree(keys, st);
+        keys = nullptr;
+        cap = total;
     }
     h->n_fail = n_uniq;
     h->n_ftid = nft;
-    BM_TRY(dalloc_t(&keys, total, st));
     BM_TRY(dalloc_t(&keys2, total, st));
-    BM_TRY(dalloc_t(&cursor, 1, st));
-    BM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
-    k_ab_scan<true><<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, fbits, nullptr, keys,
-                                               cursor);
-    h->launches += 1;
     {
         int eb = 32 + std::max(1, ilog2_u64((uint64_t)nft + 1));
         size_t tb = 0;
@@ -810,6 +811,9 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
         BM_CUDA(cub::DeviceRadixSort::SortKeys(h->cub_tmp, tb, keys, keys2, (int)total, 0, eb, st));
         h->launches += 1;
     }
+    BM_TRY(dalloc_t(&h->ab_off_d, (int64_t)nft + 1, st));
+    k_ab_offsets<<<grid_for((int64_t)nft + 1, 256), 256, 0, st>>>(keys2, total, nft, h->ab_off_d);
+    h->launches += 1;
     BM_TRY(dalloc_t(&h->ab_pos_d, total, st));
     k_low32<<<grid_for(total, 256), 256, 0, st>>>(keys2, total, h->ab_pos_d);
     h->launches += 1;
