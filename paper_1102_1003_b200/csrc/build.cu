@@ -781,6 +781,7 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     const unsigned scan_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(nnz, 1024), 1 << 30));
     int64_t cap = std::max<int64_t>(4096, 4 * F * std::max<int64_t>(1, nnz / std::max<int64_t>(m, 1)) + 1024);
     cap = std::min<int64_t>(cap, std::max<int64_t>(nnz, 1));
+    if (const char* e = getenv("BATMAP_AB_CAP")) cap = std::max<int64_t>(1, atoll(e));  // test hook: overflow path
     BM_TRY(dalloc_t(&cursor, 1, st));
     int n_uniq = 0;
     int32_t nft = 0;

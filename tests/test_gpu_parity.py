@@ -281,6 +281,17 @@ def test_mixed_widths_exact_with_failures(seed):
             assert c.info()["n_failures"] > 0
 
 
+@pytest.mark.parametrize("ab_cap", ["1", "4096"])
+def test_ab_overflow_rerun_exact(ab_cap, monkeypatch):
+    """The A_b pass emits into a buffer of a guessed size and re-runs at the exact size when the
+    guess is short; BATMAP_AB_CAP forces the guess down so that the re-run path is taken."""
+    monkeypatch.setenv("BATMAP_AB_CAP", ab_cap)
+    off, tids = uniform(400, 4000, 0.05, 17)
+    c, _ = _check_exact(off, tids, 4000, 2, max_loop=1)
+    assert c.info()["n_failures"] > 0
+    assert len(c.failures()) == c.info()["n_failures"]
+
+
 def test_colliding_pi_forces_failures_exact():
     off, tids = uniform(60, 3000, 0.1, 5)
     s, U = br.derive_params(3000)
