@@ -57,3 +57,27 @@ def test_reference_arm_contract():
     assert d["impl"] == "reference" and d["metric"] and d["value"] > 0 and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_bench_two_ranks_contract():
+    """N = 2 under torchrun (both ranks on this GPU over gloo, the bench's test hook): rank 0 alone
+    prints one line with n_gpus = 2, the instance scaled by sqrt(2), and an e2e through
+    dist.mine_distributed."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo", BENCH_FORCE_DEVICE="0")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["n_items"] == int(round(10000 * 2 ** 0.5))
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and "mine_distributed" in d["e2e"]["api"]
+    assert d["cpu_baseline"] is None  # rank 0 at N = 1 only
