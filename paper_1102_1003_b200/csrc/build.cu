@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(256) k1_gchunk_cleanup(
 
 // Flat over the CSR entries, 4 per thread per step so that the fidx gathers of a thread are
 // independent (the pass is latency-bound otherwise).  An entry whose tid failed somewhere
-// (fidx >= 0, rare) finds its item by binary search in offsets and emits (fidx << 32 | pos);
+// (fidx >= 0, rare) finds its item by binary search in offsets and emits fidx * n + pos;
 // emits take one cursor atomic per warp.  Writes beyond `cap` are dropped (the caller re-runs
 // with the exact count, which the cursor holds either way).
 __global__ void __launch_bounds__(256) k_ab_scan(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
@@ -658,30 +658,26 @@ __global__ void __launch_bounds__(256) k_ab_scan(const int64_t* __restrict__ off
                     if (__ldg(offsets + mid) <= k) lo = mid;
                     else hi = mid - 1;
                 }
-                keys[at] = ((uint64_t)(uint32_t)f[q] << 32) | (uint32_t)orig2pos[lo];
+                keys[at] = (uint64_t)(uint32_t)f[q] * (uint64_t)n + (uint32_t)orig2pos[lo];
             }
         }
     }
 }
 
-// A_b offsets from the (fidx, pos)-sorted keys: ab_off[k] = first key of failed tid k (k <= nft).
-__global__ void k_ab_offsets(const uint64_t* __restrict__ keys, int64_t total, int64_t nft, int64_t* __restrict__ off) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k > nft) return;
-    int64_t lo = 0, hi = total;
-    const uint64_t key = (uint64_t)k << 32;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (keys[mid] < key) lo = mid + 1;
-        else hi = mid;
-    }
-    off[k] = lo;
+// A_b from the sorted keys fidx * n + pos: positions, and ab_off[k] = index of failed tid k's first
+// key (every failed tid occurs in at least its own item, so each k < nft starts a run), ab_off[nft] =
+// total.  One thread per key.
+__global__ void k_ab_split(const uint64_t* __restrict__ keys, int64_t total, int64_t n, int64_t nft,
+                           int32_t* __restrict__ pos, int64_t* __restrict__ off) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const uint64_t key = keys[i];
+    const uint64_t k = key / (uint64_t)n;
+    pos[i] = (int32_t)(key - k * (uint64_t)n);
+    if (i == 0 || keys[i - 1] / (uint64_t)n != k) off[k] = i;
+    if (i == total - 1) off[nft] = total;
 }
 
-__global__ void k_low32(const uint64_t* __restrict__ keys, int64_t n, int32_t* __restrict__ out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = (int32_t)(uint32_t)keys[i];
-}
 
 static inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
@@ -805,7 +801,7 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     h->n_ftid = nft;
     BM_TRY(dalloc_t(&keys2, total, st));
     {
-        int eb = 32 + std::max(1, ilog2_u64((uint64_t)nft + 1));
+        const int eb = std::max(1, ilog2_u64((uint64_t)nft * (uint64_t)n));  // keys < nft * n
         size_t tb = 0;
         BM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, (int)total, 0, eb, st));
         BM_TRY(cub_tmp(h, tb, st));
@@ -813,10 +809,8 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
         h->launches += 1;
     }
     BM_TRY(dalloc_t(&h->ab_off_d, (int64_t)nft + 1, st));
-    k_ab_offsets<<<grid_for((int64_t)nft + 1, 256), 256, 0, st>>>(keys2, total, nft, h->ab_off_d);
-    h->launches += 1;
     BM_TRY(dalloc_t(&h->ab_pos_d, total, st));
-    k_low32<<<grid_for(total, 256), 256, 0, st>>>(keys2, total, h->ab_pos_d);
+    k_ab_split<<<grid_for(total, 256), 256, 0, st>>>(keys2, total, n, nft, h->ab_pos_d, h->ab_off_d);
     h->launches += 1;
     return BATMAP_OK;
 }

@@ -37,7 +37,7 @@ struct FailView {
 __global__ void __launch_bounds__(256) k3_correct(const Cand* __restrict__ cand, int64_t n,
                                                   const int32_t* __restrict__ sel2pos,
                                                   const int32_t* __restrict__ sel2orig, FailView fv,
-                                                  uint32_t thr, uint32_t raw, uint64_t* __restrict__ keys,
+                                                  uint32_t thr, uint32_t raw, uint64_t n_ids, uint64_t* __restrict__ keys,
                                                   uint32_t* __restrict__ vals,
                                                   unsigned long long* __restrict__ ctr) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -71,18 +71,24 @@ __global__ void __launch_bounds__(256) k3_correct(const Cand* __restrict__ cand,
         oj = t;
     }
     const unsigned long long at = atomicAdd(ctr, 1ull);
-    keys[at] = ((uint64_t)oi << 32) | oj;
+    keys[at] = (uint64_t)oi * n_ids + oj;  // < n_ids^2: fewer radix passes than (i << 32 | j)
     vals[at] = (uint32_t)supp;
 }
 
+// keys are i * n_ids + j, or (i << 32 | j) when n_ids == 0 (batmap_sort_triples)
 __global__ void k3_emit(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n,
-                        batmap_triple* __restrict__ out) {
+                        uint64_t n_ids, batmap_triple* __restrict__ out) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const uint64_t key = keys[k];
     batmap_triple t;
-    t.i = (uint32_t)(key >> 32);
-    t.j = (uint32_t)key;
+    if (n_ids) {
+        t.i = (uint32_t)(key / n_ids);
+        t.j = (uint32_t)(key - (uint64_t)t.i * n_ids);
+    } else {
+        t.i = (uint32_t)(key >> 32);
+        t.j = (uint32_t)key;
+    }
     t.support = vals[k];
     out[k] = t;
 }
@@ -116,8 +122,8 @@ batmap_status run_finalize(batmap_collection* h, const Selection& sel, int64_t n
     BM_CUDA(cudaMemsetAsync(h->ctr_d + 1, 0, sizeof(unsigned long long), st));
     h->launches += 1;
     k3_correct<<<(unsigned)((n_cand + 255) / 256), 256, 0, st>>>(
-        h->cand_d, n_cand, sel.sel2pos, sel.sel2orig, fv, threshold, (flags & BATMAP_PAIRS_RAW) ? 1u : 0u, k0, v0,
-        h->ctr_d + 1);
+        h->cand_d, n_cand, sel.sel2pos, sel.sel2orig, fv, threshold, (flags & BATMAP_PAIRS_RAW) ? 1u : 0u,
+        (uint64_t)h->n, k0, v0, h->ctr_d + 1);
     BM_CUDA(cudaGetLastError());
     unsigned long long cnt = 0;
     BM_TRY(read_scalar(st, h->ctr_d + 1, &cnt));
@@ -125,20 +131,20 @@ batmap_status run_finalize(batmap_collection* h, const Selection& sel, int64_t n
     *n_res = K;
     BM_TRY(ensure(&h->res_d, &h->res_cap, std::max<int64_t>(K, 1), st));
     if (K == 0) return BATMAP_OK;
-    const int hb = bits_for((uint64_t)h->n);
+    const int kb = bits_for((uint64_t)h->n * (uint64_t)h->n);  // keys i * n + j < n^2
     cub::DoubleBuffer<uint64_t> dk(k0, k1);
     cub::DoubleBuffer<uint32_t> dv(v0, v1);
     size_t tb = 0;
-    BM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)K, 0, 32 + hb, st));
+    BM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)K, 0, kb, st));
     if (!h->cub_tmp || h->cub_tmp_bytes < tb) {
         dfree(h->cub_tmp, st);
         h->cub_tmp = nullptr;
         BM_TRY(dalloc(&h->cub_tmp, tb + tb / 4 + 4096, st));
         h->cub_tmp_bytes = tb + tb / 4 + 4096;
     }
-    BM_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp, tb, dk, dv, (int)K, 0, 32 + hb, st));
+    BM_CUDA(cub::DeviceRadixSort::SortPairs(h->cub_tmp, tb, dk, dv, (int)K, 0, kb, st));
     h->launches += 2;
-    k3_emit<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(dk.Current(), dv.Current(), K, h->res_d);
+    k3_emit<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(dk.Current(), dv.Current(), K, (uint64_t)h->n, h->res_d);
     BM_CUDA(cudaGetLastError());
     return BATMAP_OK;
 }
@@ -169,7 +175,7 @@ batmap_status sort_triples(batmap_triple* t, int64_t n, cudaStream_t st) {
     BM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)n, 0, 64, st));
     BM_TRY(dalloc(&tmp, tb + 16, st));
     BM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)n, 0, 64, st));
-    k3_emit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dk.Current(), dv.Current(), n, t);
+    k3_emit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dk.Current(), dv.Current(), n, 0, t);
     BM_CUDA(cudaGetLastError());
     return BATMAP_OK;
 }
