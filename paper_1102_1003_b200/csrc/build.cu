@@ -619,14 +619,14 @@ __global__ void __launch_bounds__(256) k1_gchunk_cleanup(
 
 // Flat over the CSR entries, 4 per thread per step so that the fidx gathers of a thread are
 // independent (the pass is latency-bound otherwise).  An entry whose tid failed somewhere
-// (fidx >= 0, rare) finds its item by binary search in offsets and emits fidx * n + pos;
-// emits take one cursor atomic per warp.  Writes beyond `cap` are dropped (the caller re-runs
+// (fidx >= 0, rare) emits its CSR index and fidx; emits take one cursor atomic per warp.  The item
+// of each emitted entry is found afterwards (k_ab_keys), off the scan's critical path.  Writes beyond `cap` are dropped (the caller re-runs
 // with the exact count, which the cursor holds either way).
 __global__ void __launch_bounds__(256) k_ab_scan(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
                                                  const int32_t* __restrict__ orig2pos, int64_t n, int64_t nnz,
                                                  const int32_t* __restrict__ fidx, const uint32_t* __restrict__ fbits,
-                                                 uint64_t* __restrict__ keys, unsigned long long* __restrict__ cursor,
-                                                 int64_t cap) {
+                                                 uint64_t* __restrict__ at_k, int32_t* __restrict__ at_f,
+                                                 unsigned long long* __restrict__ cursor, int64_t cap) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
     for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4 - lane * 4 + lane;
@@ -652,16 +652,27 @@ __global__ void __launch_bounds__(256) k_ab_scan(const int64_t* __restrict__ off
             if (lane == __ffs(mask) - 1) at = atomicAdd(cursor, (unsigned long long)__popc(mask));
             at = __shfl_sync(0xFFFFFFFFu, at, __ffs(mask) - 1) + __popc(mask & ((1u << lane) - 1));
             if (hit && (int64_t)at < cap) {
-                int64_t lo = 0, hi = n - 1;  // last item with offsets[item] <= k
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi + 1) >> 1;
-                    if (__ldg(offsets + mid) <= k) lo = mid;
-                    else hi = mid - 1;
-                }
-                keys[at] = (uint64_t)(uint32_t)f[q] * (uint64_t)n + (uint32_t)orig2pos[lo];
+                at_k[at] = (uint64_t)k;
+                at_f[at] = f[q];
             }
         }
     }
+}
+
+// Sort keys fidx * n + pos of the emitted entries: the item of CSR entry k by binary search in
+// offsets (the last item with offsets[item] <= k; empty items are skipped by construction).
+__global__ void k_ab_keys(const int64_t* __restrict__ offsets, const int32_t* __restrict__ orig2pos, int64_t n,
+                          uint64_t* __restrict__ keys, const int32_t* __restrict__ at_f, int64_t total) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const int64_t k = (int64_t)keys[i];
+    int64_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(offsets + mid) <= k) lo = mid;
+        else hi = mid - 1;
+    }
+    keys[i] = (uint64_t)(uint32_t)at_f[i] * (uint64_t)n + (uint32_t)orig2pos[lo];
 }
 
 // A_b from the sorted keys fidx * n + pos: positions, and ab_off[k] = index of failed tid k's first
@@ -721,8 +732,10 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     int32_t *mark = nullptr, *rank = nullptr;
     uint32_t* fbits = nullptr;
     uint64_t *keys = nullptr, *keys2 = nullptr;
+    int32_t* at_f = nullptr;
     unsigned long long* cursor = nullptr;
     Scratch scratch(st);
+    scratch.own(&at_f);
     scratch.own(&sorted);
     scratch.own(&uniq);
     scratch.own(&n_uniq_d);
@@ -784,9 +797,10 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
     int64_t total = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         BM_TRY(dalloc_t(&keys, cap, st));
+        BM_TRY(dalloc_t(&at_f, cap, st));
         BM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
         k_ab_scan<<<scan_grid, 256, 0, st>>>(offsets, tids, h->orig2pos_d, n, nnz, h->fidx_of_tid_d, fbits, keys,
-                                              cursor, cap);
+                                              at_f, cursor, cap);
         h->launches += 1;
         const void* src[3] = {n_uniq_d, rank + m, cursor};
         const size_t bytes[3] = {sizeof(int), sizeof(int32_t), sizeof(int64_t)};
@@ -794,11 +808,15 @@ static batmap_status post_failures(batmap_collection* h, const int64_t* offsets,
         BM_TRY(read_scalars(st, 3, src, bytes, dst));
         if (total <= cap) break;
         dfree(keys, st);
+        dfree(at_f, st);
         keys = nullptr;
+        at_f = nullptr;
         cap = total;
     }
     h->n_fail = n_uniq;
     h->n_ftid = nft;
+    k_ab_keys<<<grid_for(total, 256), 256, 0, st>>>(offsets, h->orig2pos_d, n, keys, at_f, total);
+    h->launches += 1;
     BM_TRY(dalloc_t(&keys2, total, st));
     {
         const int eb = std::max(1, ilog2_u64((uint64_t)nft * (uint64_t)n));  // keys < nft * n
