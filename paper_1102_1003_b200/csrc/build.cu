@@ -236,13 +236,24 @@ __global__ void __launch_bounds__(kConcThreads) k1_conc_small(
         overflow = 0;
     }
     for (uint32_t q = threadIdx.x; q < 3 * r; q += blockDim.x) A[q] = kEmpty;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const uint32_t x = (uint32_t)__ldg(S + e);
+    // four tids per thread loaded ahead of the π evaluations (the loads are independent)
+    for (int e0 = threadIdx.x; e0 < n; e0 += 4 * blockDim.x) {
+        uint32_t xs[4];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-            const uint32_t v = pi_eval(P, t, x);
-            slot[t * maxS + e] = (uint16_t)slot_of(t, v, r, r0, log2r0);
-            code[t * maxS + e] = (uint8_t)(v >> P.s);
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * blockDim.x;
+            xs[u] = e < n ? (uint32_t)__ldg(S + e) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e >= n) break;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const uint32_t v = pi_eval(P, t, xs[u]);
+                slot[t * maxS + e] = (uint16_t)slot_of(t, v, r, r0, log2r0);
+                code[t * maxS + e] = (uint8_t)(v >> P.s);
+            }
         }
     }
     __syncthreads();
