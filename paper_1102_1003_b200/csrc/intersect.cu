@@ -355,13 +355,13 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
         const int2 mt = meta[buf];
         if (mt.y && cur >= 0) {  // a new work item (or the end) begins: finish the previous one
             const Work wk = work[cur];
-            if (wk.tail) {  // a piece of a cut tail tile: partial counts to its slice (thread-major)
-                uint4* dst = reinterpret_cast<uint4*>(tail_buf + (int64_t)(wk.tail - 1) * (kBM * BN)) +
-                             threadIdx.x * 16;
+            if (wk.tail) {  // a piece of a cut tail tile: partial counts to its slice, as 16 uint4
+                            // planes of kThreads (coalesced stores here and loads in k2_tail_threshold)
+                uint4* dst = reinterpret_cast<uint4*>(tail_buf + (int64_t)(wk.tail - 1) * (kBM * BN)) + threadIdx.x;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    dst[2 * i] = make_uint4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-                    dst[2 * i + 1] = make_uint4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+                    dst[(2 * i) * kThreads] = make_uint4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+                    dst[(2 * i + 1) * kThreads] = make_uint4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
                 }
             } else {
                 work_epilogue<BN>(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, lw, thr, use_f, out,
@@ -434,10 +434,10 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads) k2_tail_threshold(const T
         for (int j = 0; j < 8; ++j) acc[i][j] = 0;
     for (int p = 0; p < pieces; ++p) {
         const uint4* src =
-            reinterpret_cast<const uint4*>(tail_buf + (int64_t)(blockIdx.x * pieces + p) * (kBM * BN)) + threadIdx.x * 16;
+            reinterpret_cast<const uint4*>(tail_buf + (int64_t)(blockIdx.x * pieces + p) * (kBM * BN)) + threadIdx.x;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const uint4 a = src[2 * i], b = src[2 * i + 1];
+            const uint4 a = src[(2 * i) * K2Cfg<BN>::kThreads], b = src[(2 * i + 1) * K2Cfg<BN>::kThreads];
             acc[i][0] += a.x;
             acc[i][1] += a.y;
             acc[i][2] += a.z;
