@@ -3,19 +3,22 @@
 
 One step = one pass of the whole hot path over one synthetic instance resident in HBM:
 batmap_build (★K1) + batmap_pair_supports (★K2 intersection + ★K3 corrections/compaction),
-plus, for N > 1, the NCCL gather of the compacted triples and their device merge-sort.
+plus, for N > 1, the sharded build's NCCL all_gather of the BatMaps, the NCCL gather of the
+compacted triples and their device merge-sort.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl batmap|reference] [--config C2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl batmap|reference] [--config C4]
 
-N = 1 runs BASELINE configs[1] (C2: uniform, n = 10,000 items, m = 100,000 transactions,
-density 1 %, s = 20).  N > 1 (torchrun) scales n by sqrt(N) so that every GPU keeps C2's
-number of pair intersections (weak scaling; units = all pairs of the scaled instance).
+Workload: BASELINE configs[3], C4 -- the largest config, the one north_star's scaling target
+names ("near-linear 1->8 GPU scaling on the largest config"): Zipf-skewed (kosarak-shaped)
+tidlists, n = 100,000 items, m = 1,000,000 transactions, threshold s = 100, all C(n, 2) pairs
+intersected (no frequent-item pre-filter).  The instance is the SAME at every N (strong
+scaling): the pair triangle's tiles are dealt over the N ranks.  Extra keys at N = 1: C2
+(BASELINE configs[1]) and C4 with the paper's frequent-item pre-filter.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -29,6 +32,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "item-pair intersections/sec"
 UNIT = "pairs/s"
+DESCR = {
+    "C1": "uniform tidlists, n=1000 items, m=10000 transactions, p=0.01, threshold s=5",
+    "C2": "uniform tidlists, n=10000 items, m=100000 transactions, p=0.01, threshold s=20",
+    "C3": "Quest T40I10D100K-shaped, n=1000 items, m=100000 transactions, threshold s=500",
+    "C4": "Zipf-skewed (kosarak-shaped) tidlists, n=100000 items, m=1000000 transactions, threshold s=100, "
+          "all pairs (no pre-filter)",
+}
 
 
 def _env_int(k, d):
@@ -103,36 +113,24 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
-def _workload(name: str, n_gpus: int, seed: int | None):
+def _workload(name: str, seed: int | None):
     from workloads import make_config
 
-    scale = math.sqrt(n_gpus) if n_gpus > 1 else 1.0
-    return make_config(name, scale_items=scale, seed=seed)
+    return make_config(name, seed=seed)
 
 
-def _cpu_baseline(w, target_s: float = 8.0):
-    """The oracle (sorted merge, P:59 / P:609-611) as it stands, on a bounded row sample."""
-    import oracle
-
-    oracle.set_num_threads(len(os.sched_getaffinity(0)))
-    n = w.n
-    items = np.arange(n, dtype=np.int32)
-    t0 = time.perf_counter()
-    probe = 8
-    oracle.pairs_merge(w.offsets, w.tids, items, threshold=w.threshold, rows=(0, probe))
-    dt = max(time.perf_counter() - t0, 1e-3)
-    rows = int(min(n - 1, max(probe, probe * target_s / dt)))
-    t0 = time.perf_counter()
-    res = oracle.pairs_merge(w.offsets, w.tids, items, threshold=w.threshold, rows=(0, rows))
-    dt = time.perf_counter() - t0
-    pairs = sum(n - 1 - u for u in range(rows))
-    return {"value": pairs / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "cpu_model": _cpu_model(),
-            "sample": f"sorted-merge oracle, first {rows} of {n} items x all later items "
-                      f"({pairs} pair intersections, {len(res)} frequent) of {w.name}, {dt:.1f} s"}
+def _descr(w) -> str:
+    return f"{w.name}: " + DESCR.get(w.name, f"n={w.n} items, m={w.m} transactions, threshold s={w.threshold}")
 
 
 def _cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.strip().startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
     try:
         for ln in open("/proc/cpuinfo"):
             if ln.startswith("model name"):
@@ -142,56 +140,226 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+def _merge_rows_for(w, seconds: float, threads: int) -> int:
+    """Rows of the sorted-merge oracle's row sample that take about `seconds` at `threads`."""
+    import oracle
+
+    oracle.set_num_threads(threads)
+    probe = 8
+    t0 = time.perf_counter()
+    oracle.pairs_merge(w.offsets, w.tids, threshold=w.threshold, rows=(0, probe))
+    dt = max(time.perf_counter() - t0, 1e-4)
+    return int(min(w.n - 1, max(probe, probe * seconds / dt)))
+
+
+def _timed_horizontal(w, threads: int):
+    import oracle
+
+    oracle.set_num_threads(threads)
+    t0 = time.perf_counter()
+    res = oracle.pairs_horizontal(w.offsets, w.tids, w.m, threshold=w.threshold)
+    return time.perf_counter() - t0, int(res.shape[0])
+
+
+def _timed_merge(w, rows: int, threads: int):
+    import oracle
+
+    oracle.set_num_threads(threads)
+    t0 = time.perf_counter()
+    oracle.pairs_merge(w.offsets, w.tids, threshold=w.threshold, rows=(0, rows))
+    return time.perf_counter() - t0
+
+
+def _cpu_baseline(w):
+    """Both CPU oracles as they stand (oracle/pairs.c; never tuned for this), on this box's host
+    cores, single-thread and all threads (SURVEY §8(d) "Oracle timing"):
+
+    * horizontal pair counting over the WHOLE instance -- the faster CPU algorithm on
+      sparse data, as the paper itself notes (P:62-66);
+    * two-finger sorted merge per pair on a row sample (first R items x all
+      later items), the CPU analogue of what the GPU kernel does per pair.
+
+    `value` is the best of them (horizontal, all threads), in the metric's unit: C(n, 2) pairs
+    decided per second."""
+    cores = len(os.sched_getaffinity(0))
+    n = w.n
+    pairs = n * (n - 1) // 2
+    h_all, K = _timed_horizontal(w, cores)
+    h_1t, _ = _timed_horizontal(w, 1)
+    rows_all = _merge_rows_for(w, 4.0, cores)
+    m_all = _timed_merge(w, rows_all, cores)
+    rows_1t = _merge_rows_for(w, 3.0, 1)
+    m_1t = _timed_merge(w, rows_1t, 1)
+
+    def mpairs(rows):
+        return sum(n - 1 - u for u in range(rows))
+
+    hz = {"all": pairs / h_all, "1t": pairs / h_1t, "s_all": h_all, "s_1t": h_1t,
+          "sample": f"whole instance ({pairs} pairs, {K} frequent)"}
+    mg = {"all": mpairs(rows_all) / m_all, "1t": mpairs(rows_1t) / m_1t, "s_all": m_all, "s_1t": m_1t,
+          "sample": f"first {rows_all} (all threads) / {rows_1t} (1 thread) of {n} items x all later items"}
+    return {"value": hz["all"], "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
+            "nproc": os.cpu_count(),
+            "sample": f"horizontal pair-counting oracle over the whole {w.name} instance on {cores} threads "
+                      f"({h_all:.2f} s); merge oracle on a row sample below",
+            "horizontal": hz, "merge": mg, "best": "horizontal"}
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle, timed as it stands on this box's host cores."""
+    """--impl reference: the CPU oracle as it stands on this box's host cores (rank 0 only).
+
+    Each step = the horizontal pair-counting oracle over the whole instance, all host
+    threads -- the best CPU oracle, so the driver's ratio is against the strongest CPU program
+    in the repo.  Falls back to a bounded sorted-merge row sample if horizontal counting would
+    exceed the per-step budget."""
     if rank != 0:
         return 0
     import oracle
 
-    oracle.set_num_threads(len(os.sched_getaffinity(0)))  # torchrun exports OMP_NUM_THREADS=1
-    w = _workload(args.config, world, args.seed)
+    cores = len(os.sched_getaffinity(0))  # torchrun exports OMP_NUM_THREADS=1
+    oracle.set_num_threads(cores)
+    w = _workload(args.config, args.seed)
     n = w.n
-    items = np.arange(n, dtype=np.int32)
-    # each step: a bounded row sample (~2-4 s) of the same workload
-    t0 = time.perf_counter()
-    oracle.pairs_merge(w.offsets, w.tids, items, threshold=w.threshold, rows=(0, 8))
-    dt = max(time.perf_counter() - t0, 1e-3)
-    rows = int(min(n - 1, max(8, 8 * 3.0 / dt)))
-    pairs = sum(n - 1 - u for u in range(rows))
+    pairs = n * (n - 1) // 2
+    toff = np.bincount(w.tids, minlength=w.m).astype(np.float64)
+    horizontal = float((toff * toff).sum()) < 2e10  # Σ|T_b|^2 steps: ~seconds at most
+    if horizontal:
+        def one():
+            return _timed_horizontal(w, cores)[0]
+        sample = f"horizontal pair-counting oracle over the whole instance ({pairs} pairs) per step"
+        step_pairs = pairs
+    else:
+        rows = _merge_rows_for(w, 3.0, cores)
+        step_pairs = sum(n - 1 - u for u in range(rows))
+
+        def one():
+            return _timed_merge(w, rows, cores)
+        sample = f"sorted-merge oracle, first {rows} of {n} items x all later items ({step_pairs} pairs) per step"
     for _ in range(args.warmup):
-        oracle.pairs_merge(w.offsets, w.tids, items, threshold=w.threshold, rows=(0, rows))
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle.pairs_merge(w.offsets, w.tids, items, threshold=w.threshold, rows=(0, rows))
-        times.append(time.perf_counter() - t0)
+        one()
+    times = [one() for _ in range(args.steps)]
     tot = sum(times)
-    value = pairs * args.steps / tot
+    value = step_pairs * args.steps / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{w.name}: uniform tidlists, n={n} items (C2 n x sqrt(N)), m={w.m} transactions, "
-                               f"p={w.meta.get('p')}, threshold s={w.threshold}", "sample_rows": rows},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": _descr(w), "n_items": n, "n_transactions": w.m, "threshold": w.threshold},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                         "sample": f"sorted-merge oracle, first {rows} of {n} items x all later items "
-                                   f"({pairs} pair intersections) per step"},
+                         "cpu_model": _cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def _k2_traffic(name: str):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch on this config, from the
+    committed --set full capture (profiles/k2_traffic.json), or None."""
+    tp = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    try:
+        d = json.load(open(tp))
+    except Exception:
+        return None
+    ent = d.get("per_config", {}).get(name)
+    return int(ent["bytes_per_launch"]) if ent else None
+
+
+def _verify_small_instance(dev, backend, rank, world):
+    """N > 1: before any timing, run the whole N-rank path (sharded build, NCCL all_gather of the
+    BatMaps, dealt tiles, NCCL gather, device merge-sort) on a small Zipf instance and check rank
+    0's triples bit-exactly against the CPU oracle, so a first multi-GPU run cannot silently
+    return wrong results.  Raises on mismatch."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1102_1003_b200 import batmap
+    from paper_1102_1003_b200.dist import build_distributed, gather_triples
+    from workloads import zipf
+
+    m = 20_000
+    off, tids = zipf(3000, m, seed=99, avg=6.0)
+    off_d = torch.as_tensor(off).to(dev)
+    tids_d = torch.as_tensor(tids).to(dev)
+    coll = build_distributed(off_d, tids_d, m, seed=1, max_loop=2)  # small max_loop: exercises corrections
+    res = coll.pair_supports(threshold=2, part=rank, n_parts=world)
+    allp = gather_triples(res if backend == "nccl" else res.cpu())
+    coll.close()
+    ok = torch.ones(1, dtype=torch.int32, device=dev if backend == "nccl" else "cpu")
+    if rank == 0:
+        import oracle
+
+        got = batmap.sort_triples(allp.to(dev)).cpu().numpy().astype(np.uint32).reshape(-1, 3)
+        ref = oracle.pairs_horizontal(off, tids, m, threshold=2)
+        ok[0] = int(got.shape == ref.shape and np.array_equal(got, ref))
+    dist.broadcast(ok, 0)
+    if not int(ok.item()):
+        raise RuntimeError(f"N={world} path differs from the CPU oracle on the verification instance")
+    return True
+
+
+def _single_gpu_extra(name, dev, stream, flush, steps, prefilter=False):
+    """Extra key (N = 1): device-timed step of another config, or C4 with the P:118 pre-filter."""
+    import torch
+
+    from paper_1102_1003_b200 import Collection, frequent_items, select_csr
+
+    w = _workload(name, None)
+    off_d = torch.as_tensor(w.offsets).to(dev)
+    tids_d = torch.as_tensor(w.tids).to(dev)
+
+    def step():
+        if prefilter:
+            keep = frequent_items(off_d, w.threshold)  # batmap_frequent_items (P:118)
+            o, t = select_csr(off_d, tids_d, keep)  # batmap_select_csr
+        else:
+            keep, o, t = None, off_d, tids_d
+        c = Collection(o, t, w.m, seed=1)
+        r = c.pair_supports(threshold=w.threshold)
+        st = c.stats()
+        c.close()
+        return r, st, keep
+
+    for _ in range(3):
+        step()
+    ms, sts = [], []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r, st, keep = step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+        sts.append(st)
+    t = float(np.mean(ms))
+    pairs = w.n * (w.n - 1) // 2
+    k2 = float(np.mean([s["k2_ms"] for s in sts]))
+    peak = 32.0 * torch.cuda.get_device_properties(dev).multi_processor_count * 1.965e9
+    out = {"workload": _descr(w), "ms_per_step": t, "frequent_pairs": int(r.shape[0]),
+           "k2_ms": k2, "k2_frac_R_int": sts[-1]["word_compares"] / (k2 / 1e3) / peak if k2 > 0 else None,
+           "build_ms": float(np.mean([s["build_ms"] for s in sts]))}
+    if prefilter:
+        out["frequent_items"] = int(keep.numel())
+        out["pairs_decided_per_s"] = pairs / (t / 1e3)
+        out["note"] = ("step = batmap_frequent_items + batmap_select_csr + build + pairs over the frequent items "
+                       "(P:118); the output equals the unfiltered run's, since supp(i,j) <= min(|S_i|, |S_j|)")
+    else:
+        out["value"] = pairs / (t / 1e3)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="batmap", choices=["batmap", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -216,9 +384,9 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
         else:
             dist.init_process_group(backend)
-    n_gpus = world
-    w = _workload(args.config, n_gpus, args.seed)
     dev = torch.device("cuda", dev_idx)
+    verified = _verify_small_instance(dev, backend, rank, world) if world > 1 else None
+    w = _workload(args.config, args.seed)
     off_d = torch.as_tensor(w.offsets).to(dev)
     tids_d = torch.as_tensor(w.tids).to(dev)
     stream = torch.cuda.current_stream(dev)
@@ -232,8 +400,7 @@ def main():
         res = coll.pair_supports(threshold=w.threshold, part=rank, n_parts=world)
         if world > 1:
             allp = gather_triples(res if backend == "nccl" else res.cpu())
-            if allp is not None:
-                res = batmap.sort_triples(allp.to(dev))
+            res = batmap.sort_triples(allp.to(dev)) if allp is not None else None
         st = coll.stats()
         coll.close()
         return res, st
@@ -259,52 +426,50 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    tot_ms = float(sum(step_ms))
+    k2_ms = float(np.mean([s["k2_ms"] for s in stats]))
+    wc = int(stats[-1]["word_compares"])
+    launches = int(sum(s["launches_build"] + s["launches_pairs"] for s in stats))
+    # max over ranks of the step time and of K2's time; sums of the work and launches
+    red_dev = dev if backend == "nccl" else "cpu"
+    mx = torch.tensor([float(sum(step_ms)), k2_ms], dtype=torch.float64, device=red_dev)
+    sm = torch.tensor([float(wc), float(launches)], dtype=torch.float64, device=red_dev)
     if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    tot_ms, k2_max = float(mx[0].item()), float(mx[1].item())
+    wc_all, launches_all = int(sm[0].item()), int(sm[1].item())
     n = w.n
     pairs = n * (n - 1) // 2
     value = pairs * args.steps / (tot_ms / 1e3)
     K = int(res.shape[0]) if res is not None else 0
 
-    # ---- dominant kernel roofline: ★K2, plain integer ALU/FMA pipes (DESIGN.md §5)
+    # ---- dominant kernel roofline: ★K2, plain integer ALU/FMA pipes (DESIGN.md §6)
     peaks, src = _peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     clk_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    peak_cmp = 32.0 * sms * clk_max  # R_int word-compares/s at max clock
-    k2_ms = float(np.mean([s["k2_ms"] for s in stats]))
-    wc = int(stats[-1]["word_compares"])
-    achieved = wc / (k2_ms / 1e3)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "k2_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
-        except Exception:
-            traffic = None
+    peak_cmp = 32.0 * sms * clk_max  # R_int word-compares/s per GPU at max clock
+    achieved = wc_all / world / (k2_max / 1e3)  # per GPU, bounded by the slowest rank
     roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_cmp / 1e12, "unit": "Tcmp/s",
-                "frac": achieved / peak_cmp, "traffic": traffic,
+                "frac": achieved / peak_cmp, "traffic": _k2_traffic(w.name) if world == 1 else None,
                 "kernel": "k2_tiled (BatMap pair intersection)",
                 "peak_def": f"R_int = 32 word-compares/clk/SM x {sms} SMs x {clk_max / 1e6:.0f} MHz "
                             f"(sm_max_mhz {src}); 4 integer instructions per 32-bit word compare",
-                "k2_share_of_step": float(np.mean([s["k2_ms"] for s in stats])) / (tot_ms / args.steps),
-                "k2_ms": k2_ms, "word_compares_per_launch": wc,
+                "k2_share_of_step": k2_max / (tot_ms / args.steps),
+                "k2_ms": k2_max, "k2_ms_rank0": k2_ms, "word_compares_per_launch": wc_all // world,
+                "word_compares_all_ranks": wc_all,
                 # executed = the kernel's tiles incl. padding (ragged edges, diagonal lower halves);
-                # tile_frac is the rate of the inner loop itself, frac the algorithmic one
+                # tile_frac is the rate of the inner loop itself, frac the algorithmic one (rank 0)
                 "tile_compares_per_launch": int(stats[-1]["tile_compares"]),
                 "padding_frac": 1.0 - wc / max(int(stats[-1]["tile_compares"]), 1),
                 "tile_frac": int(stats[-1]["tile_compares"]) / (k2_ms / 1e3) / peak_cmp,
-                "logical_GBps": 8.0 * wc / (k2_ms / 1e3) / 1e9}
+                "logical_GBps": 8.0 * achieved / 1e9}
 
     e2e = None
     cpu = None
+    extra = None
     if rank == 0 and world == 1 and not args.no_e2e:
-        import torch as _t
-
-        off_h = _t.from_numpy(np.ascontiguousarray(w.offsets)).pin_memory()
-        tids_h = _t.from_numpy(np.ascontiguousarray(w.tids)).pin_memory()
+        off_h = torch.from_numpy(np.ascontiguousarray(w.offsets)).pin_memory()
+        tids_h = torch.from_numpy(np.ascontiguousarray(w.tids)).pin_memory()
         off_np, tids_np = off_h.numpy(), tids_h.numpy()
         cap = K + 1024
         for _ in range(2):
@@ -324,10 +489,8 @@ def main():
                "h2d_bytes_per_step": int(w.offsets.nbytes + w.tids.nbytes), "d2h_bytes_per_step": int(K * 12),
                "ms_per_step": float(np.mean(e_ms)), "api": "batmap_mine_host (host buffers)"}
     if world > 1 and not args.no_e2e:  # every rank: H2D of the CSR, sharded build, pairs, gather, D2H on rank 0
-        import torch as _t
-
-        off_h = _t.from_numpy(np.ascontiguousarray(w.offsets)).pin_memory()
-        tids_h = _t.from_numpy(np.ascontiguousarray(w.tids)).pin_memory()
+        off_h = torch.from_numpy(np.ascontiguousarray(w.offsets)).pin_memory()
+        tids_h = torch.from_numpy(np.ascontiguousarray(w.tids)).pin_memory()
         for _ in range(2):
             r = mine_distributed(off_h, tids_h, w.m, threshold=w.threshold, device=dev, seed=1)
         e_ms = []
@@ -341,7 +504,7 @@ def main():
             b.record(stream)
             torch.cuda.synchronize()
             e_ms.append(a.elapsed_time(b))
-        t = torch.tensor([float(np.sum(e_ms))], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        t = torch.tensor([float(np.sum(e_ms))], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_tot = float(t.item())
         if rank == 0:
@@ -350,19 +513,25 @@ def main():
                    "h2d_bytes_per_step": int(world * (w.offsets.nbytes + w.tids.nbytes)),
                    "d2h_bytes_per_step": int(K * 12), "ms_per_step": e_tot / len(e_ms),
                    "api": "dist.mine_distributed (host buffers on every rank; max over ranks)"}
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra = {}
+        if w.name != "C2":
+            extra["C2"] = _single_gpu_extra("C2", dev, stream, flush, 10)
+        if w.name == "C4":
+            extra["C4_prefiltered"] = _single_gpu_extra("C4", dev, stream, flush, 10, prefilter=True)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(w)
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{w.name}: uniform tidlists, n={n} items (C2 n x sqrt(N)), m={w.m} "
-                                   f"transactions, p={w.meta.get('p')}, threshold s={w.threshold}",
-                       "n_items": n, "n_transactions": w.m, "nnz": w.nnz, "threshold": w.threshold,
-                       "pairs_per_step": pairs, "frequent_pairs": K, "l2": "flushed (256 MB write) between steps",
-                       "parallelism": f"pair-triangle tiles dealt over {world} GPU(s) + NCCL gather"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": _descr(w), "n_items": n, "n_transactions": w.m, "nnz": w.nnz,
+                       "threshold": w.threshold, "pairs_per_step": pairs, "frequent_pairs": K,
+                       "l2": "flushed (256 MB write) between steps; arena > L2",
+                       "parallelism": f"pair-triangle tiles dealt over {world} GPU(s); sharded build + "
+                                      f"NCCL all_gather of the BatMaps; NCCL gather of the triples"},
             "freq_pairs_per_s": K * args.steps / (tot_ms / 1e3),
             "phases_ms": {"build": float(np.mean([s["build_ms"] for s in stats])),
                           "k1_insert": float(np.mean([s["k1_insert_ms"] for s in stats])),
@@ -372,7 +541,9 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(sum(s["launches_build"] + s["launches_pairs"] for s in stats)),
+            "extra": extra,
+            "verified_vs_oracle_before_timing": verified,
+            "gpu_launches": launches_all,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

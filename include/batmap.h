@@ -285,6 +285,13 @@ batmap_status batmap_merge_pair_supports(const int64_t* offsets, const int32_t* 
 /* ---------------------------------------------------------------- inspection / test hooks */
 
 /*
+ * Determinism of the exported bytes: the default build inserts the elements of an item
+ * concurrently (reading #9b in DESIGN.md), so the entry bytes and the failure set F may differ
+ * from build to build of the same input; the pair supports never do (every layout is exact
+ * after the corrections).  Builds with BATMAP_BUILD_SERIAL follow the paper's
+ * sequential INSERT in ascending tid order and are byte-reproducible for identical
+ * (tidlists, seed, r_min, max_loop).
+ *
  * batmap_export_entries -- the 3 r_i entry bytes of item `item` in entry order
  * e = 0 .. 3 r_i - 1 (superblock layout P:378-379, 4 entries per little-endian word).
  *   out [host] capacity bytes; r_out [host] receives r_i.  E_CAPACITY if capacity < 3 r_i.

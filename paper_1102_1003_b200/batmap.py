@@ -171,8 +171,13 @@ class Collection:
                                       ctypes.byref(h)))
         self._h = h
         self._last_k = 1 << 16
-        # the input CSR is not retained by the library (a shard keeps it until shard_import)
+        # the input CSR is not retained by the library (a shard keeps it until shard_import).  The
+        # build's last kernels may still read it on the library stream after this call returns:
+        # tell the caching allocator, so a converted copy is not reused before they finish.
         if self.n_parts == 1:
+            if stream is not None:
+                for t in (self._offsets, self._tids):
+                    t.record_stream(stream)
             self._offsets = self._tids = None
 
     # ------------------------------------------------------------------ sharded build

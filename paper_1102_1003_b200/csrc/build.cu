@@ -1218,6 +1218,10 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         fails = nullptr;
         fail_cap = 2 * F + 1024;  // the concurrent build is not deterministic: leave headroom
     }
+    if (F > fail_cap || fails == nullptr) {  // every attempt overflowed: never read an undersized list
+        set_error("build: %lld failed insertions exceed the failure buffer after 4 attempts", (long long)F);
+        return BATMAP_E_CAPACITY;
+    }
     h->n_fail = F;
     rec(h, EV_E0, st);
     for (const ClassInfo& cl : h->classes) {

@@ -875,6 +875,15 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         }
         kp = &local;
     }
+    // an item subset's plan buffers (promoted / virtualised copies can be hundreds of MB) are
+    // released on every return path, the BM_CUDA / BM_TRY early returns included
+    struct LocalPlanGuard {
+        K2Prepared* p;
+        cudaStream_t st;
+        ~LocalPlanGuard() {
+            if (p) release_k2(p, st);  // idempotent
+        }
+    } local_guard{kp == &local ? &local : nullptr, st};
     const Plan& pl = kp->pl;
     const int tn = kp->tn;
     const int grid_cap = min_blocks(tn) * h->num_sms;

@@ -270,7 +270,12 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         const int64_t nt = r.diag ? diag_tiles(r.n_rows, TN) : ta * tb;
         total += nt * tile_cost(r);
     }
-    const int64_t target = std::max<int64_t>(1, total / ((int64_t)n_parts * 4 * std::max(grid_cap, 1)));
+    // The split decisions shape the units dealt to the parts, so with n_parts > 1 they use a grid
+    // every rank agrees on (a B200's 2 CTAs x 148 SMs), not the local device's: ranks on devices
+    // with different SM counts (MIG slices, mixed GPUs) must build identical unit lists, or pairs
+    // would be dropped or emitted twice.  grid_cap stays in use for the part-local tail split below.
+    const int split_grid = n_parts > 1 ? kDealGrid : std::max(grid_cap, 1);
+    const int64_t target = std::max<int64_t>(1, total / ((int64_t)n_parts * 4 * split_grid));
     if (allow_split)
         for (Rect& r : P.rects)
             if (tile_cost(r) > 2 * target && r.W / kChunk > 1) r.acc = 1;

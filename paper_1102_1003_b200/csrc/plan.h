@@ -11,6 +11,7 @@ namespace bm {
 
 constexpr int kTile = 128;   // tile rows (items); the tile width (columns) is Plan::tn, 128 or 64
 constexpr int kChunk = 16;   // words per k-chunk (the TMA box height)
+constexpr int kDealGrid = 2 * 148;  // reference grid (B200: 2 K2 CTAs x 148 SMs) for rank-agreed plan decisions
 
 // A rectangle of the pair triangle: the rows are the items of class a (period W_a), the
 // columns those of class b.  A "virtualised" rectangle (R > 1) views each class-b BatMap of

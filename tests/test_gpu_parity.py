@@ -466,6 +466,8 @@ def test_determinism_and_seed_independence():
     np.testing.assert_array_equal(ra, _np(c.pair_supports(threshold=2)))
     d = _coll(w.offsets, w.tids, w.m, seed=1)  # concurrent build: layout may differ, supports may not
     np.testing.assert_array_equal(ra, _np(d.pair_supports(threshold=2)))
+    e = _coll(w.offsets, w.tids, w.m, seed=1)  # a second default build: same supports, bytes unspecified
+    np.testing.assert_array_equal(ra, _np(e.pair_supports(threshold=2)))
 
 
 def test_sort_triples():
