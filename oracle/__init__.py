@@ -14,6 +14,9 @@ Contents
                  byte-level parity of the build and raw-count parity of the intersection.
   fimi.py        NEXT-3: FIMI-repository text -> vertical tidlists (P:56-58, P:556-558,
                  SPEC S:504-512) and the frequent-item pre-filter.
+  triples.c      NEXT-4: supp(i,j,k) = |S_i ∩ S_j ∩ S_k| (P:43-44 for itemsets of size 3, the
+                 extension P:627-631 leaves open) by three-finger merge and by horizontal
+                 triple counting; C + OpenMP.
 
 Parity pins (tests/test_oracle_*.py) tie both to things other than themselves: brute
 force on tiny inputs, the Gram matrix X^T X (numpy int64 matmul), the invariant
@@ -30,17 +33,17 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "pairs.c")
+_SRCS = [os.path.join(_HERE, "pairs.c"), os.path.join(_HERE, "triples.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle/pairs.c -> oracle/liboracle.so (gcc, OpenMP)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    """Compile oracle/pairs.c + oracle/triples.c -> oracle/liboracle.so (gcc, OpenMP)."""
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(s) for s in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-std=c11",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, *_SRCS])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -63,6 +66,12 @@ def _load():
         lib.oracle_pairs_horizontal.argtypes = [P, P, I64, I64, P, I64, U32, ctypes.POINTER(P)]
         lib.oracle_free.argtypes = [P]
         lib.oracle_free.restype = None
+        lib.oracle_triple_count.restype = I64
+        lib.oracle_triple_count.argtypes = [P, I64, P, I64, P, I64]
+        lib.oracle_triples_list.restype = None
+        lib.oracle_triples_list.argtypes = [P, P, P, P, P, I64, P]
+        lib.oracle_triples_horizontal.restype = I64
+        lib.oracle_triples_horizontal.argtypes = [P, P, I64, P, I64, U32, ctypes.POINTER(P)]
         lib.oracle_num_threads.restype = ctypes.c_int
         lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -143,3 +152,39 @@ def pairs_horizontal(offsets, tids, m: int, items=None, threshold: int = 1) -> n
     k = lib.oracle_pairs_horizontal(_ptr(offsets), _ptr(tids), offsets.shape[0] - 1, int(m),
                                     _ptr(items), items.shape[0], int(threshold), ctypes.byref(outp))
     return _take(lib, k, outp)
+
+
+# ----------------------------------------------------------------------------- NEXT-4: triples
+def triple_count(a: np.ndarray, b: np.ndarray, c: np.ndarray) -> int:
+    """|a ∩ b ∩ c| for strictly increasing int arrays (three-finger merge)."""
+    lib = _load()
+    a, b, c = (np.ascontiguousarray(x, dtype=np.int32) for x in (a, b, c))
+    return int(lib.oracle_triple_count(_ptr(a), a.shape[0], _ptr(b), b.shape[0], _ptr(c), c.shape[0]))
+
+
+def triples_list(offsets, tids, ti, tj, tk) -> np.ndarray:
+    """supp(i, j, k) for explicit triples (caller ids) by three-way sorted merge."""
+    lib = _load()
+    offsets, tids, _ = _prep(offsets, tids, None)
+    ti, tj, tk = (np.ascontiguousarray(x, dtype=np.int32) for x in (ti, tj, tk))
+    out = np.zeros(ti.shape[0], dtype=np.uint32)
+    lib.oracle_triples_list(_ptr(offsets), _ptr(tids), _ptr(ti), _ptr(tj), _ptr(tk), ti.shape[0], _ptr(out))
+    return out
+
+
+def triples_horizontal(offsets, tids, m: int, items=None, threshold: int = 1) -> np.ndarray:
+    """Quads (i, j, k, supp), i<j<k, supp >= max(threshold, 1), sorted, by horizontal counting
+    (at most 4096 selected items)."""
+    lib = _load()
+    offsets, tids, items = _prep(offsets, tids, items)
+    outp = ctypes.c_void_p()
+    k = lib.oracle_triples_horizontal(_ptr(offsets), _ptr(tids), int(m), _ptr(items), items.shape[0],
+                                      int(threshold), ctypes.byref(outp))
+    if k == -2:
+        raise ValueError("triples_horizontal: at most 4096 selected items")
+    if k < 0:
+        raise MemoryError("oracle allocation failed")
+    arr = np.ctypeslib.as_array(ctypes.cast(outp, ctypes.POINTER(ctypes.c_uint32)), shape=(max(k, 1) * 4,))
+    res = arr[: 4 * k].copy().reshape(k, 4)
+    lib.oracle_free(outp)
+    return res
