@@ -436,6 +436,93 @@ batmap_status batmap_plan_groups(int32_t n_classes, const int64_t* class_n, cons
 batmap_status batmap_plan_tile(int32_t n_classes, const int64_t* class_n, const int64_t* class_w,
                                int32_t* tile_rows, int32_t* tile_cols);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT-4: supports of item TRIPLES with 3-of-4 BatMaps.
+ *
+ * The paper leaves itemsets of more than two items open and sketches "a
+ * generalization of batmaps that store items in d out of d+1 places", which "would ensure that
+ * itemsets of size up to d would have at least one position witnessing their intersection".
+ * These entry points build that structure for d = 3 and count triples with it.  The counting
+ * rule that makes every common element count exactly once is not in the paper: readings
+ * #26-#32 of DESIGN.md fix it (oracle/batmap3_ref.py follows them step by step):
+ *   - four tables, permutations π_1..π_4 (the mixer of reading #3 with keys for t = 0..3);
+ *   - 6-bit codes π_t(x) >> s3, s3 = min{s : 63 * 2^s >= m}, ⊥ = code 63; table ranges
+ *     r_i = max(2^ceil(log2 2|S_i|), 2^s3, r_min); superblocks of 4 r_0, 4 r_i bytes per item;
+ *   - INSERT over A_1..A_4 cyclically, three times per element; failed insertions are deleted
+ *     and corrected exactly, as for pairs (P:469-474 with set semantics per triple);
+ *   - entry byte = code | B1 << 6 | B2 << 7 encoding which table leaves the element out, and a
+ *     triple is counted at the lowest table all three BatMaps store the element in.
+ * Output = the definition supp(i,j,k) = |S_i ∩ S_j ∩ S_k|, bit-exact.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct batmap3_collection* batmap3_handle; /* library-owned; free with batmap3_destroy */
+
+/* One triple record: i < j < k caller ids; support = |S_i ∩ S_j ∩ S_k|. */
+typedef struct {
+    uint32_t i, j, k, support;
+} batmap_quad;
+
+typedef struct {
+    int32_t s_shift;       /* s3: entries store π_t(x) >> s3                       */
+    int32_t reserved;
+    int64_t r0;            /* min_i r_i (superblocks of 4 r0 entries)             */
+    int64_t n_items;
+    int64_t n_transactions;
+    int64_t arena_bytes;   /* sum_i 4 r_i                                         */
+    int64_t n_failures;    /* |F| of the 3-of-4 build                             */
+    int64_t n_failed_tids;
+    double build_ms;       /* CUDA-event time of batmap3_build                    */
+    double triples_ms;     /* CUDA-event time of the last batmap3_triple_supports */
+} batmap3_info_t;
+
+/*
+ * batmap3_build -- the 3-of-4 BatMap of every item.  Same input contract as batmap_build
+ * (offsets/tids [device] CSR, n_items < 2^21, 1 <= n_transactions < 2^31; opts: seed, r_min,
+ * max_loop (rounds of four swaps), flags BATMAP_CHECK_INPUT | BATMAP_BUILD_SERIAL, pi_table =
+ * [device] 4 x U3 test table, U3 = 63 * 2^s3).  The handle owns the BatMaps (item-major,
+ * 4 r_i bytes each), F, f_i and A_b of failed transactions; the CSR is read during the call
+ * only (the call synchronises `stream` before returning).
+ * Errors: E_INVALID, E_OVERFLOW, E_NOMEM, E_CAPACITY (failure buffer), E_CUDA.
+ */
+batmap_status batmap3_build(const int64_t* offsets, const int32_t* tids, int64_t n_items,
+                            int64_t n_transactions, const batmap_build_opts* opts,
+                            batmap_stream_t stream, batmap3_handle* out);
+
+/*
+ * batmap3_triple_supports -- supports of candidate triples, thresholded.
+ *   triples   [device] int32 [n_triples][3]: caller ids i < j < k (not checked).
+ *   threshold emit iff support >= threshold (0 => every candidate).
+ *   out       [device] batmap_quad[capacity], sorted by (i, j, k); n_out [host] receives the
+ *             count (set also on E_CAPACITY).
+ * One warp per candidate counts over the words of its widest BatMap (the others wrap, reading
+ * #18) with reading #30's rule; candidates with count + f_i + f_j + f_k >= threshold get the
+ * exact correction of reading #31.
+ */
+batmap_status batmap3_triple_supports(batmap3_handle h, const int32_t* triples, int64_t n_triples,
+                                      uint32_t threshold, batmap_quad* out, int64_t capacity,
+                                      int64_t* n_out, batmap_stream_t stream);
+
+/*
+ * batmap_candidate_triples -- Apriori join (reading #32): every i < j < k such that (i, j),
+ * (i, k) and (j, k) all occur in `pairs`.
+ *   pairs  [device] batmap_triple[n_pairs] sorted by (i, j) with i < j < n_items, as
+ *          batmap_pair_supports returns them (the frequent pairs).
+ *   out    [device] int32 [capacity][3], sorted by (i, j, k); n_out [host] (set also on
+ *          E_CAPACITY).
+ * Exact for frequent-triple mining: supp(i,j,k) <= the support of each of its pairs.
+ */
+batmap_status batmap_candidate_triples(const batmap_triple* pairs, int64_t n_pairs, int64_t n_items,
+                                       int32_t* out, int64_t capacity, int64_t* n_out,
+                                       batmap_stream_t stream);
+
+batmap_status batmap3_info(batmap3_handle h, batmap3_info_t* info);
+/* batmap3_export_entries -- item's 4 r_i entry bytes [host] (E_CAPACITY if capacity < 4 r_i). */
+batmap_status batmap3_export_entries(batmap3_handle h, int32_t item, uint8_t* out, int64_t capacity,
+                                     int64_t* r_out);
+/* batmap3_export_failures -- F as (item, tid) [host] sorted by (item, tid). */
+batmap_status batmap3_export_failures(batmap3_handle h, int32_t* items, int32_t* tids,
+                                      int64_t capacity, int64_t* n_out);
+void batmap3_destroy(batmap3_handle h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,6 +6,8 @@ its thin binding (``batmap``), the multi-GPU gather (``dist``) and the build scr
 from .batmap import (  # noqa: F401
     BatMapError,
     Collection,
+    Collection3,
+    candidate_triples,
     dense_pair_supports,
     load_library,
     FimiDB,
@@ -14,6 +16,7 @@ from .batmap import (  # noqa: F401
     mine_fimi,
     parse_fimi,
     mine_host,
+    mine_triples,
     plan_groups,
     plan_tile,
     plan_work,

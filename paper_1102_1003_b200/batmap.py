@@ -56,6 +56,13 @@ class Info(ctypes.Structure):
                 ("arena_bytes", ctypes.c_int64), ("n_failures", ctypes.c_int64), ("n_failed_tids", ctypes.c_int64)]
 
 
+class Info3(ctypes.Structure):
+    _fields_ = [("s_shift", ctypes.c_int32), ("reserved", ctypes.c_int32), ("r0", ctypes.c_int64),
+                ("n_items", ctypes.c_int64), ("n_transactions", ctypes.c_int64), ("arena_bytes", ctypes.c_int64),
+                ("n_failures", ctypes.c_int64), ("n_failed_tids", ctypes.c_int64), ("build_ms", ctypes.c_double),
+                ("triples_ms", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -104,6 +111,13 @@ def load_library():
                                        ctypes.c_int),
         "batmap_merge_pair_supports": ([P, P, I64, I64, P, I64, U32, P, I64, PI64, ctypes.POINTER(ctypes.c_double),
                                         PI64, P], ctypes.c_int),
+        "batmap3_build": ([P, P, I64, I64, ctypes.POINTER(BuildOpts), P, ctypes.POINTER(P)], ctypes.c_int),
+        "batmap3_triple_supports": ([P, P, I64, U32, P, I64, PI64, P], ctypes.c_int),
+        "batmap_candidate_triples": ([P, I64, I64, P, I64, PI64, P], ctypes.c_int),
+        "batmap3_info": ([P, ctypes.POINTER(Info3)], ctypes.c_int),
+        "batmap3_export_entries": ([P, I32, P, I64, PI64], ctypes.c_int),
+        "batmap3_export_failures": ([P, P, P, I64, PI64], ctypes.c_int),
+        "batmap3_destroy": ([P], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -520,3 +534,119 @@ def plan_work(class_n, class_w, part: int = 0, n_parts: int = 1, grid_cap: int =
     _check(lib.batmap_plan_work(*args, items.ctypes.data_as(ctypes.c_void_p), nt.value, ctypes.byref(nt),
                                 ctypes.byref(wc), ctypes.byref(tcmp)))
     return items[: nt.value], int(wc.value), int(tcmp.value)
+
+
+# ----------------------------------------------------------------------------- NEXT-4: triples
+class Collection3:
+    """3-of-4 BatMaps of one instance on the current CUDA device (batmap3_build)."""
+
+    def __init__(self, offsets, tids, n_transactions: int, *, seed: int = 0, r_min: int = 128,
+                 max_loop: int = 0, check: bool = False, pi_table=None, serial: bool = False, stream=None):
+        import torch
+
+        lib = load_library()
+        if not (offsets.is_cuda and tids.is_cuda):
+            raise ValueError("offsets and tids must be CUDA tensors")
+        off = offsets.contiguous().to(torch.int64)
+        td = tids.contiguous().to(torch.int32)
+        pi = pi_table.contiguous().to(torch.int32) if pi_table is not None else None
+        self.n_items = off.numel() - 1
+        self._stream = stream
+        opts = _opts(seed, r_min, max_loop, check, pi, serial)
+        h = ctypes.c_void_p()
+        _check(lib.batmap3_build(_dptr(off), _dptr(td), self.n_items, int(n_transactions), ctypes.byref(opts),
+                                 _stream_ptr(stream), ctypes.byref(h)))  # synchronises the stream
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().batmap3_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def info(self) -> dict:
+        inf = Info3()
+        _check(load_library().batmap3_info(self._h, ctypes.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in Info3._fields_}
+
+    def triple_supports(self, triples, threshold: int = 1, stream=None):
+        """int32 tensor [K, 4] of (i, j, k, support) for the candidate triples (int32 [n, 3], i < j < k,
+        caller ids) with support >= threshold, sorted by (i, j, k)."""
+        import torch
+
+        lib = load_library()
+        t = triples if (hasattr(triples, "is_cuda") and triples.is_cuda) else torch.as_tensor(np.asarray(triples))
+        t = t.to(device="cuda", dtype=torch.int32).contiguous().reshape(-1, 3)
+        n = t.shape[0]
+        st = _stream_ptr(stream if stream is not None else self._stream)
+        n_out = ctypes.c_int64(0)
+        cap = max(1, n)
+        out = torch.empty((cap, 4), dtype=torch.int32, device="cuda")
+        _check(lib.batmap3_triple_supports(self._h, _dptr(t), n, int(threshold), _dptr(out), cap,
+                                           ctypes.byref(n_out), st))
+        return out[: int(n_out.value)]
+
+    def export_entries(self, item: int) -> np.ndarray:
+        lib = load_library()
+        r = ctypes.c_int64(0)
+        rc = lib.batmap3_export_entries(self._h, int(item), None, 0, ctypes.byref(r))
+        _check(rc, ok=(BATMAP_OK, BATMAP_E_CAPACITY))
+        buf = np.empty(4 * r.value, dtype=np.uint8)
+        _check(lib.batmap3_export_entries(self._h, int(item), buf.ctypes.data_as(ctypes.c_void_p), buf.size,
+                                          ctypes.byref(r)))
+        return buf
+
+    def failures(self) -> np.ndarray:
+        lib = load_library()
+        n = ctypes.c_int64(0)
+        rc = lib.batmap3_export_failures(self._h, None, None, 0, ctypes.byref(n))
+        _check(rc, ok=(BATMAP_OK, BATMAP_E_CAPACITY))
+        items = np.empty(max(n.value, 1), np.int32)
+        tids = np.empty(max(n.value, 1), np.int32)
+        _check(lib.batmap3_export_failures(self._h, items.ctypes.data_as(ctypes.c_void_p),
+                                           tids.ctypes.data_as(ctypes.c_void_p), items.size, ctypes.byref(n)))
+        return np.stack([items[: n.value], tids[: n.value]], axis=1)
+
+
+def candidate_triples(pairs, n_items: int, stream=None):
+    """Apriori join (batmap_candidate_triples): int32 [C, 3] of i < j < k whose three pairs all occur
+    in `pairs` ([K, 3] device int32 triples sorted by (i, j), as Collection.pair_supports returns)."""
+    import torch
+
+    lib = load_library()
+    p = pairs.to(device="cuda", dtype=torch.int32).contiguous().reshape(-1, 3)
+    st = _stream_ptr(stream)
+    n_out = ctypes.c_int64(0)
+    rc = lib.batmap_candidate_triples(_dptr(p), p.shape[0], int(n_items), None, 0, ctypes.byref(n_out), st)
+    _check(rc, ok=(BATMAP_OK, BATMAP_E_CAPACITY))
+    cap = int(n_out.value)
+    out = torch.empty((max(cap, 1), 3), dtype=torch.int32, device="cuda")
+    _check(lib.batmap_candidate_triples(_dptr(p), p.shape[0], int(n_items), _dptr(out), cap, ctypes.byref(n_out), st))
+    return out[: int(n_out.value)]
+
+
+def mine_triples(offsets, tids, n_transactions: int, threshold: int, *, seed: int = 0, stream=None):
+    """Frequent triples end to end on the device: frequent pairs (batmap_build + batmap_pair_supports),
+    the Apriori candidates (batmap_candidate_triples), 3-of-4 BatMaps (batmap3_build) and their
+    supports (batmap3_triple_supports).  Returns (int32 [K3, 4] (i, j, k, support) sorted, dict of
+    counts)."""
+    with Collection(offsets, tids, n_transactions, seed=seed, stream=stream) as c2:
+        pairs = c2.pair_supports(threshold=threshold)
+    cand = candidate_triples(pairs, offsets.numel() - 1, stream=stream)
+    with Collection3(offsets, tids, n_transactions, seed=seed, stream=stream) as c3:
+        quads = c3.triple_supports(cand, threshold=threshold)
+        info = c3.info()
+    return quads, {"frequent_pairs": int(pairs.shape[0]), "candidates": int(cand.shape[0]),
+                   "frequent_triples": int(quads.shape[0]), "build3_ms": info["build_ms"],
+                   "triples_ms": info["triples_ms"]}

@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <cstring>
+#include <future>
 
 #include "common.cuh"
 
@@ -466,6 +467,333 @@ __global__ void __launch_bounds__(NT) k1_conc_cluster(
 }
 
 
+// ------------------------------------------------------------------ byte-table tier
+// The working table of an item holds the entry bytes themselves (3r bytes instead of 12r): slot q of
+// table t holds code = π_t(x) >> s of the element x placed there, ⊥ = 0x7F (reading #1).
+// Slot and code determine v = π_t(x) (r >= 2^s: the slot gives v mod r, the code v >> s), so an
+// element evicted by a swap is recovered as x = π_t^-1(v) and continues into table t+1.
+// A table of up to r = 2^16 (192 KB) fits ONE CTA's shared memory, so every swap is a local
+// shared-memory atomic: the uint32 tier needs a cluster of 4 CTAs and remote DSMEM atomics for the
+// same item.  A swap is a byte exchange done as a 32-bit CAS on the word holding the byte (no 8-bit
+// exchange exists).  Larger tables (r <= 2^19) spread over a cluster of CS CTAs as before.
+// The second INSERT of x starts with τ <-> A_1[h_1(x)]; when that slot still holds x this swap
+// exchanges x with itself, so a read replaces it (an atomic fewer per element, same semantics).
+// Encode (Fig. 5): the thread of x reads x's three bytes and sets b = 1 with a plain byte
+// store on the copy whose partner sits in the preceding table -- x's bytes are written by x's thread
+// only, so no atomics are needed -- and the pack pass copies the table words to the arena unchanged.
+constexpr uint32_t kByteSliceMax = 3u * 65536u;  // 192 KB of table bytes per CTA
+constexpr uint32_t kByteMaxR = 1u << 19;          // CS = 8 x 192 KB
+
+__device__ __forceinline__ uint32_t sh_ld_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t sh_cas(uint32_t a, uint32_t cmp, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint32_t sh_ld_u8(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.volatile.shared.u8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t cl_ld_u8(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sh_st_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
+}
+__device__ __forceinline__ void cl_st_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
+}
+
+// One CTA (CS = 1) builds IPC consecutive items of a class, each in its own 3r-byte slice (padded
+// by 16 bytes so the pack's lanes hit distinct banks), or one item is spread over a cluster of CS
+// CTAs (IPC = 1).  The INSERT chains run as persistent lanes: a lane whose chain ends takes its next
+// task (the element's second INSERT, or the next element) at once instead of idling until the
+// warp's slowest chain is done; π's round keys of the table a lane is at come from shared memory.
+// The pack writes word w of the IPC items as IPC consecutive arena columns: whole 32-byte sectors
+// when IPC = 8.
+template <int CS, int IPC, int NT>
+__global__ void __launch_bounds__(NT) k1_byte(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
+    int64_t first, int n_cls, uint32_t r, int log2r, PiParams P, uint32_t r0, int log2r0, uint32_t max_loop_opt,
+    uint32_t* __restrict__ arena_cls, int n_pad, uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr,
+    int64_t fail_cap) {
+    static_assert(CS == 1 || IPC == 1, "an item spread over a cluster is built alone");
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) uint8_t TB[];  // IPC item slices (CS = 1) or this CTA's slice of one item
+    __shared__ uint32_t fl[kConcFailCap];
+    __shared__ uint8_t fl_k[kConcFailCap];
+    __shared__ int nfl, overflow;
+    __shared__ int pre[IPC + 1];
+    __shared__ const int32_t* Sk[IPC];
+    __shared__ __align__(16) uint32_t keys[3][8];  // per table: 4 forward, 4 inverse round keys
+    const uint32_t rank = CS == 1 ? 0u : cg::this_cluster().block_rank();
+    const uint32_t slice = 3u * r / CS;
+    const uint32_t stride_b = IPC == 1 ? slice : slice + 16u;  // item k's slice at TB + k * stride_b
+    const int c0 = (int)(blockIdx.x / CS) * IPC;                // first column of this CTA (cluster)
+    const int n_it = min(IPC, n_cls - c0);
+    if (threadIdx.x <= IPC) {
+        int cnt = 0;
+        for (int k = 0; k < (int)threadIdx.x && k < n_it; ++k) {
+            const int orig = pos2orig[first + c0 + k];
+            cnt += (int)(offsets[orig + 1] - offsets[orig]);
+        }
+        pre[threadIdx.x] = cnt;
+        if ((int)threadIdx.x < n_it) Sk[threadIdx.x] = tids + offsets[pos2orig[first + c0 + threadIdx.x]];
+    }
+    if (threadIdx.x == 32) {  // compile-time indices: the parameter struct stays in constant space
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                keys[t][j] = pi_key(P, t, j);
+                keys[t][4 + j] = pi_kinv(P, t, j);
+            }
+    }
+    const uint32_t T_loc = (uint32_t)__cvta_generic_to_shared(TB);
+    const uint32_t low_s = (1u << P.s) - 1u;
+    // slot q of item k -> shared-window address of its byte (remote for another CTA of the cluster)
+    auto where = [&](int k, uint32_t q, bool* local) -> uint32_t {
+        if (CS == 1) {
+            *local = true;
+            return T_loc + (uint32_t)k * stride_b + q;
+        }
+        const uint32_t o = ((q * CS) >> log2r) / 3u;
+        const uint32_t a = T_loc + (q - o * slice);
+        *local = o == rank;
+        if (*local) return a;
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(o));
+        return ra;
+    };
+    auto read_byte = [&](int k, uint32_t q) -> uint32_t {
+        bool loc;
+        const uint32_t a = where(k, q, &loc);
+        return loc ? sh_ld_u8(a) : cl_ld_u8(a);
+    };
+    // byte exchange (τ <-> A_t[h_t(τ)]): CAS on the word holding the byte; returns the old byte
+    auto xchg = [&](int k, uint32_t q, uint32_t code) -> uint32_t {
+        bool loc;
+        const uint32_t a = where(k, q, &loc);
+        const uint32_t wa = a & ~3u, sh = (a & 3u) * 8u;
+        uint32_t old = loc ? sh_ld_u32(wa) : cl_ld(wa);
+        while (true) {
+            const uint32_t nw = (old & ~(0xFFu << sh)) | (code << sh);
+            const uint32_t prev = loc ? sh_cas(wa, old, nw) : cl_cas(wa, old, nw);
+            if (prev == old) return (old >> sh) & 0xFFu;
+            old = prev;
+        }
+    };
+    // byte -> ⊥ if it still holds `code` (deleting a failed element's remaining copy)
+    auto erase = [&](int k, uint32_t q, uint32_t code) {
+        bool loc;
+        const uint32_t a = where(k, q, &loc);
+        const uint32_t wa = a & ~3u, sh = (a & 3u) * 8u;
+        uint32_t old = loc ? sh_ld_u32(wa) : cl_ld(wa);
+        while (((old >> sh) & 0xFFu) == code) {
+            const uint32_t nw = (old & ~(0xFFu << sh)) | (kNullByte << sh);
+            const uint32_t prev = loc ? sh_cas(wa, old, nw) : cl_cas(wa, old, nw);
+            if (prev == old) return;
+            old = prev;
+        }
+    };
+    for (uint32_t i = threadIdx.x; i < (uint32_t)IPC * stride_b / 16; i += NT)
+        reinterpret_cast<uint4*>(TB)[i] = make_uint4(kNullWord, kNullWord, kNullWord, kNullWord);
+    if (threadIdx.x == 0) {
+        nfl = 0;
+        overflow = 0;
+    }
+    if (CS > 1) cg::this_cluster().sync();
+    else __syncthreads();
+    const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)log2r;
+    const int ntot = pre[n_it];
+    // π_t with table t's round keys from shared memory (t differs between lanes); walk as pi_eval
+    auto pi_fwd = [&](int t, uint32_t v) -> uint32_t {
+        const uint4 kf = *reinterpret_cast<const uint4*>(&keys[t][0]);
+        do {
+            v = (v * kf.x) & P.mask;
+            v ^= v >> P.half;
+            v = (v * kf.y) & P.mask;
+            v ^= v >> P.half;
+            v = (v * kf.z) & P.mask;
+            v ^= v >> P.half;
+            v = (v * kf.w) & P.mask;
+            v ^= v >> P.half;
+        } while (v >= P.U);
+        return v;
+    };
+    auto pi_inv = [&](int t, uint32_t v) -> uint32_t {
+        const uint4 ki = *reinterpret_cast<const uint4*>(&keys[t][4]);
+        do {
+            v ^= v >> P.half;
+            v = (v * ki.w) & P.mask;
+            v ^= v >> P.half;
+            v = (v * ki.z) & P.mask;
+            v ^= v >> P.half;
+            v = (v * ki.y) & P.mask;
+            v ^= v >> P.half;
+            v = (v * ki.x) & P.mask;
+        } while (v >= P.U);
+        return v;
+    };
+    // ---- INSERT chains as persistent lanes (reading #9b)
+    {
+        int g = (int)rank * NT + threadIdx.x;  // next element of this lane (flattened over the IPC items)
+        int k = 0, t = 0, copy = 0;
+        uint32_t x = 0, tau = 0, rounds = 0;
+        bool have = false;
+        auto begin_element = [&]() {
+            have = g < ntot;
+            if (!have) return;
+            k = 0;
+#pragma unroll
+            for (int j = 1; j < IPC; ++j) k += (g >= pre[j]);
+            x = (uint32_t)__ldg(Sk[k] + (g - pre[k]));
+            tau = x;
+            t = 0;
+            rounds = 0;
+            copy = 0;
+        };
+        begin_element();
+        while (__any_sync(0xFFFFFFFFu, have)) {
+            if (!have) continue;
+            const uint32_t v = pi_fwd(t, tau);
+            const uint32_t q = slot_of(t, v, r, r0, log2r0);
+            const uint32_t old = xchg(k, q, v >> P.s);
+            bool end = old == kNullByte;
+            if (!end) {  // the evicted element: v' = π_t(y) from slot and code
+                const uint32_t vr = (((q >> log2r0) / 3u) << log2r0) | (q & (r0 - 1u));
+                tau = pi_inv(t, (old << P.s) | (vr & low_s));
+                if (++t == 3) {
+                    t = 0;
+                    if (++rounds == max_loop) {  // nestless after MaxLoop rounds: a failure
+                        const int j = atomicAdd(&nfl, 1);
+                        if (j < kConcFailCap) {
+                            fl[j] = tau;
+                            fl_k[j] = (uint8_t)k;
+                        } else {
+                            overflow = 1;
+                        }
+                        const unsigned long long idx = atomicAdd(fail_ctr, 1ull);
+                        if ((int64_t)idx < fail_cap) fails[idx] = ((uint64_t)(first + c0 + k) << 32) | tau;
+                        end = true;
+                    }
+                }
+            }
+            if (end) {
+                if (copy == 0) {  // the insert procedure is called twice
+                    copy = 1;
+                    tau = x;
+                    rounds = 0;
+                    // its first swap, τ <-> A_1[h_1(x)], would return x itself if x still sits there
+                    const uint32_t v1 = pi_fwd(0, x);
+                    t = read_byte(k, slot_of(0, v1, r, r0, log2r0)) == (v1 >> P.s) ? 1 : 0;
+                } else {
+                    g += CS * NT;
+                    begin_element();
+                }
+            }
+        }
+    }
+    __syncthreads();
+    int any_overflow;
+    if (CS > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        int* ovf0 = cl.map_shared_rank(&overflow, 0);
+        if (threadIdx.x == 0 && overflow && rank != 0) atomicOr(ovf0, 1);
+        cl.sync();
+        any_overflow = *ovf0;
+    } else {
+        any_overflow = overflow;
+    }
+    if (!any_overflow) {  // delete the remaining copy of every failed element (reading #9b)
+        const int nf = nfl;
+        for (int j = threadIdx.x; j < nf; j += NT) {
+            const uint32_t x = fl[j];
+            const int k = fl_k[j];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const uint32_t v = pi_fwd(t, x);
+                erase(k, slot_of(t, v, r, r0, log2r0), v >> P.s);
+            }
+        }
+    } else {  // rare: any element left with fewer than two copies was recorded
+        for (int g = (int)rank * NT + threadIdx.x; g < ntot; g += CS * NT) {
+            int k = 0;
+#pragma unroll
+            for (int j = 1; j < IPC; ++j) k += (g >= pre[j]);
+            const uint32_t x = (uint32_t)__ldg(Sk[k] + (g - pre[k]));
+            uint32_t q[3], cd[3];
+            int cnt = 0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const uint32_t v = pi_fwd(t, x);
+                q[t] = slot_of(t, v, r, r0, log2r0);
+                cd[t] = v >> P.s;
+                cnt += (read_byte(k, q[t]) == cd[t]);
+            }
+            if (cnt == 1)
+#pragma unroll
+                for (int t = 0; t < 3; ++t) erase(k, q[t], cd[t]);
+        }
+    }
+    if (CS > 1) cg::this_cluster().sync();
+    else __syncthreads();
+    // encode: b = 1 on the copy whose partner sits in the preceding table (Fig. 5, reading #6);
+    // x's bytes are written by x's thread only (plain byte stores)
+    for (int g = (int)rank * NT + threadIdx.x; g < ntot; g += CS * NT) {
+        int k = 0;
+#pragma unroll
+        for (int j = 1; j < IPC; ++j) k += (g >= pre[j]);
+        const uint32_t x = (uint32_t)__ldg(Sk[k] + (g - pre[k]));
+        uint32_t q[3], cd[3];
+        bool in[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const uint32_t v = pi_fwd(t, x);
+            q[t] = slot_of(t, v, r, r0, log2r0);
+            cd[t] = v >> P.s;
+            in[t] = read_byte(k, q[t]) == cd[t];
+        }
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+            if (in[t] && !in[(t + 1) % 3]) {
+                bool loc;
+                const uint32_t a = where(k, q[t], &loc);
+                if (loc) sh_st_u8(a, 0x80u | cd[t]);
+                else cl_st_u8(a, 0x80u | cd[t]);
+            }
+    }
+    if (CS > 1) cg::this_cluster().sync();
+    else __syncthreads();
+    // pack: the table words are the arena words (entry e = byte lane e & 3 of word e >> 2)
+    if (IPC == 1) {
+        const uint32_t w0 = rank * slice / 4;
+        for (uint32_t i = threadIdx.x; i < slice / 16; i += NT) {
+            const uint4 v = reinterpret_cast<const uint4*>(TB)[i];
+            uint32_t* dst = arena_cls + (int64_t)(w0 + 4 * i) * n_pad + c0;
+            dst[0] = v.x;
+            dst[(int64_t)n_pad] = v.y;
+            dst[2 * (int64_t)n_pad] = v.z;
+            dst[3 * (int64_t)n_pad] = v.w;
+        }
+    } else {  // lane -> (word, item): IPC consecutive columns of a word row per store group
+        const uint32_t W = slice / 4;
+        for (uint32_t i = threadIdx.x; i < W * IPC; i += NT) {
+            const uint32_t w = i / IPC, k = i % IPC;
+            if ((int)k < n_it)
+                arena_cls[(int64_t)w * n_pad + c0 + k] = *reinterpret_cast<const uint32_t*>(TB + k * stride_b + 4 * w);
+        }
+    }
+    if (CS > 1) cg::this_cluster().sync();  // no CTA may exit while another still reads its slice
+}
+
 // Encode columns [0, n) of one class block: thread per (word w, column c); writes
 // arena_cls[w * n_pad + c] (padding columns are filled by k_fill_padding).
 __global__ void __launch_bounds__(256) k1_encode(
@@ -892,6 +1220,65 @@ static batmap_status launch_cluster_tier(batmap_collection* h, const ClassInfo& 
     return launch_cluster<8, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
 }
 
+template <int CS, int IPC, int NT>
+static batmap_status launch_byte(const ClassInfo& c, batmap_collection* h, const int64_t* offsets,
+                                 const int32_t* tids, uint64_t* fails, unsigned long long* fail_ctr,
+                                 int64_t fail_cap, cudaStream_t st) {
+    const size_t smem = IPC == 1 ? (size_t)3 * c.r / CS : (size_t)IPC * (3 * c.r + 16);
+    BM_CUDA(cudaFuncSetAttribute(k1_byte<CS, IPC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kByteSliceMax + 256));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((c.n + IPC - 1) / IPC) * CS);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BM_CUDA(cudaLaunchKernelEx(&cfg, k1_byte<CS, IPC, NT>, offsets, tids, (const int32_t*)h->pos2orig_d,
+                               (int64_t)c.first, (int)c.n, (uint32_t)c.r, ilog2_u64((uint64_t)c.r), h->pi,
+                               (uint32_t)h->r0, h->log2r0, h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, fails,
+                               fail_ctr, fail_cap));
+    h->launches += 1;
+    return BATMAP_OK;
+}
+
+// byte tier: the smallest cluster whose CTAs hold <= 192 KB of the item's 3r table bytes, spread over
+// more CTAs when the class has too few items to fill the GPU (BATMAP_K1_SPREAD=0 keeps the smallest);
+// classes of many small tables put IPC = 2..8 items in one CTA (BATMAP_K1_IPC=1 disables it), so the
+// pack stores whole sectors; threads per CTA grow with the table
+static batmap_status launch_byte_tier(batmap_collection* h, const ClassInfo& c, const int64_t* offsets,
+                                      const int32_t* tids, uint64_t* fails, unsigned long long* fail_ctr,
+                                      int64_t fail_cap, cudaStream_t st) {
+    const int64_t bytes = 3ll * c.r;
+    int cs = 1;
+    while (bytes > cs * (int64_t)kByteSliceMax) cs *= 2;
+    const char* sp = getenv("BATMAP_K1_SPREAD");
+    const bool spread = !(sp && sp[0] == '0');
+    while (spread && cs < 8 && (int64_t)c.n * cs * 2 <= h->num_sms) cs *= 2;
+    if (cs == 1) {
+        const char* ie = getenv("BATMAP_K1_IPC");
+        const bool multi = !(ie && ie[0] == '1');
+        int ipc = 1;  // items per CTA while the CTAs still fill every SM
+        while (multi && ipc < 8 && 2 * ipc * (bytes + 16) <= (int64_t)kByteSliceMax + 256 &&
+               (int64_t)c.n >= (int64_t)2 * ipc * h->num_sms)
+            ipc *= 2;
+        if (ipc == 8) return launch_byte<1, 8, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+        if (ipc == 4) return launch_byte<1, 4, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+        if (ipc == 2) return launch_byte<1, 2, 512>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+        if (bytes <= 24576) return launch_byte<1, 1, 256>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+        if (bytes <= 49152) return launch_byte<1, 1, 512>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+        return launch_byte<1, 1, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    }
+    if (cs == 2) return launch_byte<2, 1, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    if (cs == 4) return launch_byte<4, 1, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+    return launch_byte<8, 1, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
+}
+
 batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
                                const batmap_build_opts* o, int part, int n_parts, cudaStream_t st,
                                const int64_t* offsets_host) {
@@ -962,13 +1349,16 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     h->arena_bytes_raw = 0;
     h->classes.clear();
     std::vector<int> class_maxS;
+    std::vector<int64_t> class_sumS;
     int64_t word_off = 0;
     for (int64_t p = 0; p < n;) {
         int64_t q = p;
         int maxS = 0;
+        int64_t sumS = 0;
         while (q < n && lr_pos[q] == lr_pos[p]) {
             const int32_t o2 = h->pos2orig_h[q];
             maxS = std::max<int>(maxS, (int)(off_h[o2 + 1] - off_h[o2]));
+            sumS += off_h[o2 + 1] - off_h[o2];
             ++q;
         }
         ClassInfo c{};
@@ -982,6 +1372,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         h->arena_bytes_raw += 3ll * c.r * c.n;
         h->classes.push_back(c);
         class_maxS.push_back(maxS);
+        class_sumS.push_back(sumS);
         p = q;
     }
     h->arena_words = word_off;
@@ -991,9 +1382,39 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         set_error("arena too large");
         return BATMAP_E_OVERFLOW;
     }
+    // the intersection's host plan (C4: 3e5 work items, milliseconds of host time) is made on a worker
+    // thread while this build's kernels run; prepare_full_k2 uploads it once K1 is launched.  Small
+    // plans are made inline (a thread costs more than they do).
+    struct PlanTask {
+        std::future<K2Prepared*> f;
+        cudaStream_t st;
+        ~PlanTask() {
+            if (f.valid()) destroy_k2(f.get(), st);  // early error return: drop the unused plan
+        }
+    } plan_task{{}, st};
+    if (n >= 16384 && full_k2_plannable(h))
+        plan_task.f = std::async(std::launch::async, new_k2_host_plan, h->classes, h->num_sms, part, n_parts);
     // items of classes with r > glob_min_r (the last positions) use a working table in global memory
     const bool serial = o && (o->flags & BATMAP_BUILD_SERIAL);
-    const int64_t glob_min_r = serial ? kSmallMaxR : kClusterMaxR;
+    // concurrent tiers: the byte-table kernel (k1_byte, r <= 2^19) unless disabled or a test π
+    // table is supplied (the byte tier inverts the hash form of π); else the uint32 cluster kernel
+    // (BATMAP_K1_BYTE=0: never; =all: every class up to 2^19, clusters included -- test hooks).  By
+    // default (measured, profiles/r2_k1_tiers.jsonl): tables of <= 192 KB as bytes (r <= 2^16) that
+    // would need a cluster as uint32 (r >= 2^15), and classes of many nearly empty tables (C4: ~13
+    // elements in r = 8192), whose cost is the pack and which the byte tier packs 8 items at a time;
+    // denser narrow tables stay in the uint32 kernel (fewer instructions per swap); r > 2^16 goes to
+    // the global tier, which spreads a few giant items over many CTAs.
+    const char* bt_env = getenv("BATMAP_K1_BYTE");
+    const int byte_mode = serial || h->pi.table != nullptr || (bt_env && bt_env[0] == '0') ? 0
+                          : (bt_env && bt_env[0] == 'a') ? 2 : 1;
+    auto use_byte = [&](size_t a) {
+        const ClassInfo& c = h->classes[a];
+        if (byte_mode != 1) return byte_mode == 2;
+        if (c.r > 16384) return true;
+        return class_sumS[a] * 16 < (int64_t)c.n * c.r && (int64_t)c.n >= 4ll * h->num_sms;
+    };
+    const int64_t glob_min_r =
+        serial ? kSmallMaxR : byte_mode == 2 ? (int64_t)kByteMaxR : byte_mode == 1 ? 65536 : (int64_t)kClusterMaxR;
     int64_t big_begin = n;
     for (const ClassInfo& c : h->classes)
         if (c.r > glob_min_r) {
@@ -1005,11 +1426,50 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     for (int64_t p = 0; p < n_big; ++p) work_off[p + 1] = work_off[p] + 3ll * (1ll << lr_pos[big_begin + p]);
     const int64_t work_entries = work_off[n_big];
 
-    // this part's share of every class: columns [n*part/n_parts, n*(part+1)/n_parts) (sharded build,
-    // SURVEY §8(e)(ii)); the whole class when n_parts == 1
+    // sharded build: class a is cut into n_parts column chunks; part p builds chunk
+    // (p + rot[a]) mod n_parts.  The rotations deal the chunks by estimated insertion cost, greedily,
+    // most expensive class first, so that parts receiving a giant item get fewer of the cheap ones
+    // (every rank computes the same rotations from the same tidlist sizes).
+    h->shard_rot.assign(h->classes.size(), 0);
+    if (n_parts > 1) {
+        std::vector<std::vector<double>> chunk(h->classes.size(), std::vector<double>(n_parts, 0.0));
+        std::vector<std::pair<double, size_t>> order;
+        for (size_t a = 0; a < h->classes.size(); ++a) {
+            const ClassInfo& c = h->classes[a];
+            for (int j = 0; j < n_parts; ++j) {
+                const int64_t q0 = (int64_t)c.n * j / n_parts, q1 = (int64_t)c.n * (j + 1) / n_parts;
+                for (int64_t q = q0; q < q1; ++q) {
+                    const int32_t o2 = h->pos2orig_h[c.first + q];
+                    // ~ 60 bytes of arena traffic per insertion (profiles/r2_k1_tiers.jsonl)
+                    chunk[a][j] += 120.0 * (double)(off_h[o2 + 1] - off_h[o2]) + 3.0 * c.r;
+                }
+            }
+            order.push_back({*std::max_element(chunk[a].begin(), chunk[a].end()), a});
+        }
+        std::stable_sort(order.begin(), order.end(), [](const std::pair<double, size_t>& x,
+                                                        const std::pair<double, size_t>& y) { return x.first > y.first; });
+        std::vector<double> load(n_parts, 0.0);
+        for (const auto& oa : order) {
+            const size_t a = oa.second;
+            int best = 0;
+            double best_max = 0.0;
+            for (int o = 0; o < n_parts; ++o) {
+                double mx = 0.0;
+                for (int p = 0; p < n_parts; ++p) mx = std::max(mx, load[p] + chunk[a][(p + o) % n_parts]);
+                if (o == 0 || mx < best_max) {
+                    best = o;
+                    best_max = mx;
+                }
+            }
+            h->shard_rot[a] = best;
+            for (int p = 0; p < n_parts; ++p) load[p] += chunk[a][(p + best) % n_parts];
+        }
+    }
+    // this part's share of every class (the whole class when n_parts == 1)
     auto view = [&](const ClassInfo& c) {
         ClassInfo v = c;
-        const int64_t c0 = (int64_t)c.n * part / n_parts, c1 = (int64_t)c.n * (part + 1) / n_parts;
+        int64_t c0, c1;
+        shard_cols(h, (size_t)(&c - h->classes.data()), part, n_parts, &c0, &c1);
         v.first = c.first + c0;
         v.n = (int32_t)(c1 - c0);
         v.word_off = c.word_off + c0;
@@ -1020,7 +1480,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     if (!serial)
         for (const ClassInfo& cl : h->classes) {
             const ClassInfo c = view(cl);
-            if (c.r <= kClusterMaxR) continue;
+            if (c.r <= glob_min_r) continue;
             for (int64_t p = c.first; p < c.first + c.n; ++p) {
                 const int32_t o2 = h->pos2orig_h[p];
                 const int32_t len = (int32_t)(off_h[o2 + 1] - off_h[o2]);
@@ -1138,7 +1598,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
             }
             // r <= cl_min_r: the slot-caching CTA kernel (faster for narrow tables, measured on C2);
             // wider tables: the cluster kernel.  BATMAP_K1_SMALL=legacy|cluster moves the boundary.
-            static const int64_t cl_min_r = [] {
+            const int64_t cl_min_r = [] {  // read per build (tests switch it)
                 const char* v = getenv("BATMAP_K1_SMALL");
                 if (v && v[0] == 'l') return (int64_t)kSmallMaxR;
                 if (v && v[0] == 'c') return (int64_t)0;
@@ -1154,7 +1614,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
             bool any_few = false, any_many = false;
             for (const ClassInfo& cl : h->classes) {
                 const ClassInfo c = view(cl);
-                if (c.n == 0 || c.r > kClusterMaxR) continue;
+                if (c.n == 0 || c.r > glob_min_r) continue;
                 (c.n < h->num_sms ? any_few : any_many) = true;
             }
             const bool use_side = !(se && se[0] == '0') && any_few && any_many && h->device < kMaxDev;
@@ -1185,8 +1645,9 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
             auto sfor = [&](const ClassInfo& c) { return use_side && c.n < h->num_sms ? side : st; };
             for (size_t a = h->classes.size(); a-- > 0;) {  // cluster tier, widest first
                 const ClassInfo c = view(h->classes[a]);
-                if (c.r <= cl_min_r || c.r > kClusterMaxR || c.n == 0) continue;
-                BM_TRY(launch_cluster_tier(h, c, offsets, tids, fails, fail_ctr, fail_cap, sfor(c)));
+                if (c.r <= cl_min_r || c.r > glob_min_r || c.n == 0) continue;
+                if (use_byte(a)) BM_TRY(launch_byte_tier(h, c, offsets, tids, fails, fail_ctr, fail_cap, sfor(c)));
+                else BM_TRY(launch_cluster_tier(h, c, offsets, tids, fails, fail_ctr, fail_cap, sfor(c)));
             }
             for (size_t a = 0; a < h->classes.size(); ++a) {
                 const ClassInfo c = view(h->classes[a]);
@@ -1209,7 +1670,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         rec(h, EV_I1, st);
         BM_CUDA(cudaGetLastError());
         // plan the intersection of the full selection on the host while the build kernels run
-        if (attempt == 0) BM_TRY(prepare_full_k2(h, part, n_parts, st));
+        if (attempt == 0) BM_TRY(prepare_full_k2(h, part, n_parts, st, plan_task.f.valid() ? plan_task.f.get() : nullptr));
         unsigned long long Fh = 0;
         BM_TRY(read_scalar(st, fail_ctr, &Fh));
         F = (int64_t)Fh;
@@ -1253,11 +1714,19 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
 }
 
 // Words of part p's share of the arena (all classes, in class order, each [W][c1 - c0]).
+void shard_cols(const batmap_collection* h, size_t a, int p, int n_parts, int64_t* c0, int64_t* c1) {
+    const int64_t n = h->classes[a].n;
+    const int j = n_parts > 1 && a < h->shard_rot.size() ? (p + h->shard_rot[a]) % n_parts : p;
+    *c0 = n * j / n_parts;
+    *c1 = n * (j + 1) / n_parts;
+}
+
 int64_t shard_words(const batmap_collection* h, int p, int n_parts) {
     int64_t words = 0;
-    for (const ClassInfo& c : h->classes) {
-        const int64_t c0 = (int64_t)c.n * p / n_parts, c1 = (int64_t)c.n * (p + 1) / n_parts;
-        words += (c1 - c0) * c.W;
+    for (size_t a = 0; a < h->classes.size(); ++a) {
+        int64_t c0, c1;
+        shard_cols(h, a, p, n_parts, &c0, &c1);
+        words += (c1 - c0) * h->classes[a].W;
     }
     return words;
 }
@@ -1266,8 +1735,10 @@ int64_t shard_words(const batmap_collection* h, int p, int n_parts) {
 batmap_status shard_copy(batmap_collection* h, int p, int n_parts, uint32_t* packed, bool to_arena,
                          cudaStream_t st) {
     int64_t off = 0;
-    for (const ClassInfo& c : h->classes) {
-        const int64_t c0 = (int64_t)c.n * p / n_parts, c1 = (int64_t)c.n * (p + 1) / n_parts;
+    for (size_t ci = 0; ci < h->classes.size(); ++ci) {
+        const ClassInfo& c = h->classes[ci];
+        int64_t c0, c1;
+        shard_cols(h, ci, p, n_parts, &c0, &c1);
         if (c1 == c0) continue;
         uint32_t* a = h->arena_d + c.word_off + c0;
         uint32_t* b = packed + off;

@@ -41,6 +41,7 @@ struct Status {
 struct PiParams {
     uint32_t s, w, U, mask, half;
     uint32_t key[3][4];
+    uint32_t kinv[3][4];    // key^-1 mod 2^w (the byte-table build inverts π, reading #3)
     const uint32_t* table;  // device [3][U] or nullptr
 };
 
@@ -56,6 +57,29 @@ __host__ __device__ __forceinline__ uint32_t pi_mix(const PiParams& P, int t, ui
         v ^= v >> P.half;
     }
     return v;
+}
+
+__host__ __device__ __forceinline__ uint32_t pi_kinv(const PiParams& P, int t, int r) {
+    return t == 0 ? P.kinv[0][r] : (t == 1 ? P.kinv[1][r] : P.kinv[2][r]);
+}
+
+// mix^-1: the rounds in reverse order; v ^= v >> half is an involution on w bits (half >= w/2)
+__host__ __device__ __forceinline__ uint32_t pi_unmix(const PiParams& P, int t, uint32_t v) {
+#pragma unroll
+    for (int r = 3; r >= 0; --r) {
+        v ^= v >> P.half;
+        v = (v * pi_kinv(P, t, r)) & P.mask;
+    }
+    return v;
+}
+
+// π_t^-1 on [0, U): walk mix^-1 back until the value is in [0, U) again (the cycle-walk's inverse:
+// every value strictly between x and π_t(x) on x's mix orbit is >= U).  Hash form only (P.table
+// == nullptr).
+__device__ __forceinline__ uint32_t pi_inverse(const PiParams& P, int t, uint32_t v) {
+    uint32_t x = pi_unmix(P, t, v);
+    while (x >= P.U) x = pi_unmix(P, t, x);
+    return x;
 }
 
 // t is 0-based (table t+1 of the paper)
@@ -165,6 +189,7 @@ struct batmap_collection {
     // sharded build (batmap_build_shard): this part's failure records until batmap_shard_import
     bool shard_pending = false;
     int shard_part = 0, shard_n_parts = 1;
+    std::vector<int32_t> shard_rot;  // per class: part p builds column chunk (p + shard_rot[a]) mod N
     uint64_t* shard_fails_d = nullptr;
     int64_t shard_n_fail = 0;
     uint32_t* cnt_d = nullptr;
@@ -209,7 +234,9 @@ inline void rec(batmap_collection* h, int idx, cudaStream_t st) {
 // allocation helpers (stream-ordered pool)
 batmap_status dalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
-void* host_staging(size_t bytes);
+// per-thread pinned staging buffers: slot 0 for the build's host tables, slot 1 for the K2 plan
+// upload (both reused by the next call of the thread, after its stream synchronisation)
+void* host_staging(size_t bytes, int slot = 0);
 // k scalar device -> host copies (each <= 8 bytes) then one synchronisation of st
 batmap_status read_scalars(cudaStream_t st, int k, const void* const* src, const size_t* bytes, void* const* dst);
 template <typename T>
@@ -262,6 +289,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
                                const batmap_build_opts* o, int part, int n_parts, cudaStream_t st,
                                const int64_t* offsets_host = nullptr);
 int64_t shard_words(const batmap_collection* h, int p, int n_parts);
+void shard_cols(const batmap_collection* h, size_t a, int p, int n_parts, int64_t* c0, int64_t* c1);
 batmap_status emit_sorted_keys(uint64_t* keys, uint32_t* vals, int64_t K, int64_t cap, batmap_triple* out,
                                cudaStream_t st);
 batmap_status merge_pair_supports(const int64_t* offsets, const int32_t* tids, int64_t n_items, const int32_t* items,
@@ -282,7 +310,10 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
                             int64_t* n_cand);
 batmap_status swar_device(const uint32_t* x, const uint32_t* y, int64_t n, uint32_t* out,
                           cudaStream_t st);
-batmap_status prepare_full_k2(batmap_collection* h, int part, int n_parts, cudaStream_t st);
+batmap_status prepare_full_k2(batmap_collection* h, int part, int n_parts, cudaStream_t st,
+                              K2Prepared* host_plan = nullptr);
+bool full_k2_plannable(const batmap_collection* h);
+K2Prepared* new_k2_host_plan(const std::vector<ClassInfo>& classes, int num_sms, int part, int n_parts);
 void destroy_k2(K2Prepared* kp, cudaStream_t st);
 // finalize.cu
 batmap_status run_finalize(batmap_collection* h, const Selection& sel, int64_t n_cand,

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "plan.h"
@@ -763,24 +764,29 @@ void destroy_k2(K2Prepared* kp, cudaStream_t st) {
 }
 
 // Host planning + device copies of the plan + tensor maps (no dependence on the arena contents).
-batmap_status prepare_k2(batmap_collection* h, const Selection& sel, int part, int n_parts, cudaStream_t st,
-                         K2Prepared* kp) {
-    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
-    if (!enc) {
-        set_error("cuTensorMapEncodeTiled unavailable");
-        return BATMAP_E_CUDA;
-    }
+// Host half of the plan: tile width and work list (pure host computation, no device calls; the build
+// runs it on a worker thread while the K1 kernels execute).
+void plan_k2_host(const std::vector<ClassInfo>& classes, int num_sms, int part, int n_parts, K2Prepared* kp) {
     kp->part = part;
     kp->n_parts = n_parts;
     const bool promote = !env_off("BATMAP_K2_PROMOTE");
     const bool virt = !env_off("BATMAP_K2_VIRTUAL");
     kp->promote = promote;
-    kp->tn = choose_tn(sel.classes, virt, promote);
+    kp->tn = choose_tn(classes, virt, promote);
     kp->tn_env = env_tn();
-    const int grid_cap = min_blocks(kp->tn) * h->num_sms;
-    plan_work(sel.classes, part, n_parts, grid_cap, virt, !env_off("BATMAP_K2_SPLIT"), promote, &kp->pl, kp->tn);
+    const int grid_cap = min_blocks(kp->tn) * num_sms;
+    plan_work(classes, part, n_parts, grid_cap, virt, !env_off("BATMAP_K2_SPLIT"), promote, &kp->pl, kp->tn);
     if ((int)kp->pl.eff.size() > kMaxMaps || (int)(kp->pl.eff.size() + kp->pl.virt.size()) > kMaxMaps)
-        plan_work(sel.classes, part, n_parts, grid_cap, false, true, promote, &kp->pl, kp->tn);
+        plan_work(classes, part, n_parts, grid_cap, false, true, promote, &kp->pl, kp->tn);
+}
+
+// Device half: scratch copies, tensor maps, and the plan's upload.
+static batmap_status materialize_k2(batmap_collection* h, const Selection& sel, cudaStream_t st, K2Prepared* kp) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return BATMAP_E_CUDA;
+    }
     const Plan& pl = kp->pl;
     const int C = (int)pl.eff.size();
     if (pl.work.empty()) return BATMAP_OK;
@@ -811,30 +817,67 @@ batmap_status prepare_k2(batmap_collection* h, const Selection& sel, int part, i
     BM_TRY(dalloc_t(&kp->rects_d, (int64_t)pl.rects.size(), st));
     BM_TRY(dalloc_t(&kp->work_d, (int64_t)pl.work.size(), st));
     BM_TRY(dalloc_t(&kp->units_d, (int64_t)std::max<size_t>(pl.units.size(), 1), st));
-    BM_CUDA(cudaMemcpyAsync(kp->rects_d, pl.rects.data(), pl.rects.size() * sizeof(Rect), cudaMemcpyHostToDevice, st));
-    BM_CUDA(cudaMemcpyAsync(kp->work_d, pl.work.data(), pl.work.size() * sizeof(Work), cudaMemcpyHostToDevice, st));
-    if (!pl.units.empty())
-        BM_CUDA(cudaMemcpyAsync(kp->units_d, pl.units.data(), pl.units.size() * sizeof(AccUnit),
-                                cudaMemcpyHostToDevice, st));
-    if (!pl.tails.empty()) {
-        BM_TRY(dalloc_t(&kp->tails_d, (int64_t)pl.tails.size(), st));
-        BM_CUDA(cudaMemcpyAsync(kp->tails_d, pl.tails.data(), pl.tails.size() * sizeof(TailTile),
-                                cudaMemcpyHostToDevice, st));
+    if (!pl.tails.empty()) BM_TRY(dalloc_t(&kp->tails_d, (int64_t)pl.tails.size(), st));
+    // the plan goes up through pinned staging: a pageable copy would wait for the build's kernels
+    // already queued on the stream (C4: 7.6 MB of work items behind ~2 ms of K1)
+    struct Up {
+        void* dst;
+        const void* src;
+        size_t bytes;
+    };
+    const Up ups[4] = {{kp->rects_d, pl.rects.data(), pl.rects.size() * sizeof(Rect)},
+                       {kp->work_d, pl.work.data(), pl.work.size() * sizeof(Work)},
+                       {kp->units_d, pl.units.data(), pl.units.size() * sizeof(AccUnit)},
+                       {kp->tails_d, pl.tails.data(), pl.tails.size() * sizeof(TailTile)}};
+    size_t total = 0;
+    for (const Up& u : ups) total += (u.bytes + 15) / 16 * 16;
+    char* pin = static_cast<char*>(host_staging(total, 1));
+    size_t at = 0;
+    for (const Up& u : ups) {
+        if (!u.bytes) continue;
+        const void* from = u.src;
+        if (pin) {
+            memcpy(pin + at, u.src, u.bytes);
+            from = pin + at;
+            at += (u.bytes + 15) / 16 * 16;
+        }
+        BM_CUDA(cudaMemcpyAsync(u.dst, from, u.bytes, cudaMemcpyHostToDevice, st));
     }
     return BATMAP_OK;
 }
 
 // Called by batmap_build once the classes are known: plan the full selection for (part, n_parts).
-batmap_status prepare_full_k2(batmap_collection* h, int part, int n_parts, cudaStream_t st) {
-    if (h->n < 2 || (int)h->classes.size() > kMaxMaps) return BATMAP_OK;
+batmap_status prepare_k2(batmap_collection* h, const Selection& sel, int part, int n_parts, cudaStream_t st,
+                         K2Prepared* kp) {
+    plan_k2_host(sel.classes, h->num_sms, part, n_parts, kp);
+    return materialize_k2(h, sel, st, kp);
+}
+
+bool full_k2_plannable(const batmap_collection* h) {
+    if (h->n < 2 || (int)h->classes.size() > kMaxMaps) return false;
     for (const ClassInfo& c : h->classes)
-        if (c.W % kBK != 0 || c.W >= kMaxTiledW || c.W < kBK) return BATMAP_OK;
+        if (c.W % kBK != 0 || c.W >= kMaxTiledW || c.W < kBK) return false;
+    return true;
+}
+
+K2Prepared* new_k2_host_plan(const std::vector<ClassInfo>& classes, int num_sms, int part, int n_parts) {
+    K2Prepared* kp = new K2Prepared();
+    plan_k2_host(classes, num_sms, part, n_parts, kp);
+    return kp;
+}
+
+// The plan of the full selection, from a host plan made beforehand (hp, owned from here on) or now.
+batmap_status prepare_full_k2(batmap_collection* h, int part, int n_parts, cudaStream_t st, K2Prepared* hp) {
+    if (!full_k2_plannable(h)) {
+        if (hp) destroy_k2(hp, st);
+        return BATMAP_OK;
+    }
     Selection sel;
     sel.classes = h->classes;
     sel.arena = h->arena_d;
     sel.n_sel = h->n;
-    K2Prepared* kp = new K2Prepared();
-    batmap_status rc = prepare_k2(h, sel, part, n_parts, st, kp);
+    K2Prepared* kp = hp ? hp : new K2Prepared();
+    batmap_status rc = hp ? materialize_k2(h, sel, st, kp) : prepare_k2(h, sel, part, n_parts, st, kp);
     if (rc != BATMAP_OK) {
         destroy_k2(kp, st);
         return rc;

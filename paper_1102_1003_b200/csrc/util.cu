@@ -18,7 +18,29 @@ void set_error(const char* fmt, ...) {
 
 const char* get_error() { return g_err; }
 
+// The device's default memory pool keeps freed blocks instead of returning them to the driver at
+// every synchronisation (release threshold 0 by default): a bench step builds and frees GBs of
+// BatMaps, and re-mapping them cost ~1 ms per build on C4.  Set once per device per process.
+static void keep_pool(cudaStream_t s) {
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return;
+    }
+    if (done[dev]) return;
+    done[dev] = true;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    (void)s;
+}
+
 batmap_status dalloc(void** p, size_t bytes, cudaStream_t s) {
+    keep_pool(s);
     cudaError_t e = cudaMallocAsync(p, bytes, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -37,21 +59,21 @@ void dfree(void* p, cudaStream_t s) {
 // for the thread's lifetime).  Copies from / to it are asynchronous; every build synchronises its
 // stream (the failure count) before it returns, so the next build of the thread never overwrites
 // bytes still in flight.  Returns nullptr (callers fall back to pageable copies) if pinning fails.
-void* host_staging(size_t bytes) {
-    static thread_local void* buf = nullptr;
-    static thread_local size_t cap = 0;
-    if (bytes <= cap) return buf;
-    if (buf) cudaFreeHost(buf);
-    buf = nullptr;
-    cap = 0;
+void* host_staging(size_t bytes, int slot) {
+    static thread_local void* buf[2] = {nullptr, nullptr};
+    static thread_local size_t cap[2] = {0, 0};
+    if (bytes <= cap[slot]) return buf[slot];
+    if (buf[slot]) cudaFreeHost(buf[slot]);
+    buf[slot] = nullptr;
+    cap[slot] = 0;
     size_t want = bytes + bytes / 2 + 4096;
-    if (cudaHostAlloc(&buf, want, cudaHostAllocPortable) != cudaSuccess) {
+    if (cudaHostAlloc(&buf[slot], want, cudaHostAllocPortable) != cudaSuccess) {
         cudaGetLastError();
-        buf = nullptr;
+        buf[slot] = nullptr;
         return nullptr;
     }
-    cap = want;
-    return buf;
+    cap[slot] = want;
+    return buf[slot];
 }
 
 // Scalar readbacks through a small pinned buffer (one per host thread, allocated once): the
@@ -97,6 +119,9 @@ PiParams make_pi(uint64_t seed, int s, const uint32_t* table) {
         for (int r = 0; r < 4; ++r) {
             uint64_t z = splitmix64(seed + (uint64_t)(4 * t + r) * 0x9E3779B97F4A7C15ull);
             P.key[t][r] = (((uint32_t)z) | 1u) & P.mask;
+            uint32_t inv = P.key[t][r];  // Newton: inv <- inv (2 - k inv), 5 steps reach 32 bits
+            for (int it = 0; it < 5; ++it) inv *= 2u - P.key[t][r] * inv;
+            P.kinv[t][r] = inv & P.mask;
         }
     P.table = table;
     return P;

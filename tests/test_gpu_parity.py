@@ -153,8 +153,15 @@ def _check_layout_invariants(c, off, tids, m, seed, r_min=128):
         assert int((ent != br.NULL).sum()) == int(seen.sum())  # nothing else stored
 
 
+@pytest.mark.parametrize("small", ["default", "cluster", "bytes"])
 @pytest.mark.parametrize("max_loop", [0, 1])
-def test_concurrent_build_invariants(max_loop):
+def test_concurrent_build_invariants(max_loop, small, monkeypatch):
+    # small=cluster: no slot-caching CTA tier (uint32 cluster tier down to the smallest tables);
+    # small=bytes: every table (r = 256 .. 2^16) in the byte tier
+    if small != "default":
+        monkeypatch.setenv("BATMAP_K1_SMALL", "cluster")
+    if small == "bytes":
+        monkeypatch.setenv("BATMAP_K1_BYTE", "all")
     off, tids, m = _mixed(11, n=30)
     c = _coll(off, tids, m, seed=4, max_loop=max_loop)
     _check_layout_invariants(c, off, tids, m, 4)
@@ -163,12 +170,13 @@ def test_concurrent_build_invariants(max_loop):
     np.testing.assert_array_equal(_np(c.pair_supports(threshold=0)), oracle.pairs_merge(off, tids, threshold=0))
 
 
-def _tiers(seed, m=300000):
-    """Items whose table ranges span the cluster tier (r = 2^14 .. 2^17: clusters of 1, 2, 4, 8
-    CTAs) and the global-memory tier (r = 2^18), plus small items, with shared elements."""
+def _tiers(seed, m=300000, huge=False):
+    """Items whose table ranges span the concurrent tiers -- uint32 cluster tier r = 2^14 .. 2^17
+    (clusters of 1, 2, 4, 8 CTAs) and global tier r >= 2^18; byte tier r = 2^12 .. 2^19 (clusters of
+    1 .. 8 CTAs) and global tier r = 2^20 with `huge` -- plus small items, with shared elements."""
     rng = np.random.default_rng(seed)
-    sizes = [5000, 9000, 17000, 40000, 70000, 300, 3000, 8000]
-    base = np.sort(rng.choice(m, size=90000, replace=False))
+    sizes = [5000, 9000, 17000, 40000, 70000, 300, 3000, 8000] + ([150000, 330000] if huge else [])
+    base = np.sort(rng.choice(m, size=150000 if huge else 90000, replace=False))
     rows = []
     for k, size in enumerate(sizes):
         own = rng.choice(m, size=size - size // 3, replace=False)
@@ -179,16 +187,22 @@ def _tiers(seed, m=300000):
     return off, np.concatenate(rows), m
 
 
+@pytest.mark.parametrize("byte", ["0", "1", "all"])
 @pytest.mark.parametrize("spread", ["0", "1"])
 @pytest.mark.parametrize("max_loop", [0, 1])
-def test_cluster_and_global_tiers(max_loop, spread, monkeypatch):
+def test_cluster_and_global_tiers(max_loop, spread, byte, monkeypatch):
     # spread=0: the smallest cluster per table size (1, 2, 4, 8 CTAs); spread=1 (default): these
-    # one-item classes spread over clusters of 8
+    # one-item classes spread over clusters of 8.  byte=1 (default policy): byte-table tier k1_byte
+    # for r = 2^15, 2^16, uint32 cluster tier below, global tier above; byte=all: k1_byte for every
+    # class up to r = 2^19 (clusters of up to 8 CTAs); byte=0: the uint32 cluster tier only
     monkeypatch.setenv("BATMAP_K1_SPREAD", spread)
-    off, tids, m = _tiers(21)
+    monkeypatch.setenv("BATMAP_K1_BYTE", byte)
+    off, tids, m = _tiers(21, m=600000, huge=byte != "0")
     c = _coll(off, tids, m, seed=6, max_loop=max_loop)
     rs = sorted({len(c.export_entries(i)) // 3 for i in range(len(off) - 1)})
     assert {2 ** 14, 2 ** 15, 2 ** 16, 2 ** 17, 2 ** 18} <= set(rs)
+    if byte != "0":
+        assert {2 ** 19, 2 ** 20} <= set(rs)
     _check_layout_invariants(c, off, tids, m, 6)
     if max_loop:
         # some item's failure list overflows its 512-entry shared-memory list (kConcFailCap in
@@ -197,6 +211,30 @@ def test_cluster_and_global_tiers(max_loop, spread, monkeypatch):
         per_item = np.bincount(c.failures()[:, 0], minlength=len(off) - 1)
         assert per_item.max() > 512, per_item
     np.testing.assert_array_equal(_np(c.pair_supports(threshold=0)), oracle.pairs_merge(off, tids, threshold=0))
+
+
+@pytest.mark.parametrize("ipc", ["1", "default"])
+@pytest.mark.parametrize("max_loop", [0, 1])
+def test_byte_tier_many_small_tables(ipc, max_loop, monkeypatch):
+    """A class of 2,500 tiny items in r = 8192 tables (C4's shape): the byte tier builds IPC = 8 items
+    per CTA (ipc=default) or one (ipc=1); overlapping sets from a small pool so pairs are frequent."""
+    if ipc != "default":
+        monkeypatch.setenv("BATMAP_K1_IPC", ipc)
+    rng = np.random.default_rng(17)
+    m, n = 600000, 2500
+    pool = rng.choice(m, size=4000, replace=False)
+    rows = []
+    for i in range(n):
+        size = int(rng.integers(1, 60))
+        mine = np.concatenate([rng.choice(pool, size=size // 2, replace=False), rng.choice(m, size=size - size // 2)])
+        rows.append(np.unique(mine).astype(np.int32))
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    tids = np.concatenate(rows)
+    c = _coll(off, tids, m, seed=9, max_loop=max_loop)
+    assert c.info()["n_classes"] == 1 and c.info()["r0"] == 8192
+    _check_layout_invariants(c, off, tids, m, 9)
+    np.testing.assert_array_equal(_np(c.pair_supports(threshold=2)), oracle.pairs_horizontal(off, tids, m, threshold=2))
 
 
 def _sharded(off, tids, m, n_parts, **kw):

@@ -3,7 +3,7 @@ the library's CUDA events, per K1 variant (environment switches of build.cu, rea
 With --check, one build per variant is also run through the pair kernels and compared with the
 C5 goldens (tests/golden/c5) or the horizontal CPU oracle.  One JSON line per (config, variant).
 
-    python tools/build_bench.py [--reps 5] [--check] [--variants byte=1 byte=0] C2 C5_p0.1 ...
+    python tools/build_bench.py [--reps 5] [--check] [--variants "byte=1;byte=0,small=cluster"] C2 C5_p0.1 ...
 
 Variant keys: byte -> BATMAP_K1_BYTE, small -> BATMAP_K1_SMALL, spread -> BATMAP_K1_SPREAD,
 side -> BATMAP_K1_SIDE.
@@ -23,7 +23,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 from paper_1102_1003_b200 import Collection  # noqa: E402
 from workloads import make_config  # noqa: E402
 
-ENV = {"byte": "BATMAP_K1_BYTE", "small": "BATMAP_K1_SMALL", "spread": "BATMAP_K1_SPREAD", "side": "BATMAP_K1_SIDE"}
+ENV = {"byte": "BATMAP_K1_BYTE", "small": "BATMAP_K1_SMALL", "spread": "BATMAP_K1_SPREAD", "side": "BATMAP_K1_SIDE",
+       "ipc": "BATMAP_K1_IPC"}
 
 
 def _reference(w):
@@ -43,7 +44,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--check", action="store_true")
-    ap.add_argument("--variants", nargs="*", default=["byte=1"])
+    ap.add_argument("--variants", default="byte=1", help="';'-separated variants of ','-separated key=value")
     ap.add_argument("configs", nargs="*", default=["C2", "C3", "C4", "C5_p0.01", "C5_p0.1"])
     a = ap.parse_args()
     for name in a.configs:
@@ -51,7 +52,7 @@ def main():
         off_d = torch.as_tensor(w.offsets).cuda()
         tids_d = torch.as_tensor(w.tids).cuda()
         ref = None
-        for var in a.variants:
+        for var in a.variants.split(";"):
             for k in ENV.values():
                 os.environ.pop(k, None)
             for kv in var.split(","):
