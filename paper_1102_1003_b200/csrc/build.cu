@@ -12,6 +12,8 @@
 
 #include <cstring>
 #include <future>
+#include <chrono>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -1279,9 +1281,29 @@ static batmap_status launch_byte_tier(batmap_collection* h, const ClassInfo& c, 
     return launch_byte<8, 1, 1024>(c, h, offsets, tids, fails, fail_ctr, fail_cap, st);
 }
 
+// BATMAP_TRACE=1: host-side timestamps of the build's phases on stderr (diagnostics)
+struct HostTrace {
+    bool on = false;
+    std::chrono::steady_clock::time_point t0, last;
+    HostTrace() {
+        const char* e = getenv("BATMAP_TRACE");
+        on = e && e[0] == '1';
+        t0 = last = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[batmap trace] %-28s +%8.3f ms  (at %8.3f ms)\n", what,
+                std::chrono::duration<double, std::milli>(now - last).count(),
+                std::chrono::duration<double, std::milli>(now - t0).count());
+        last = now;
+    }
+};
+
 batmap_status build_collection(batmap_collection* h, const int64_t* offsets, const int32_t* tids,
                                const batmap_build_opts* o, int part, int n_parts, cudaStream_t st,
                                const int64_t* offsets_host) {
+    HostTrace tr;
     const int64_t n = h->n, m = h->m;
     const int64_t l0 = h->launches;
     rec(h, EV_B0, st);
@@ -1322,6 +1344,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         int l = ilog2_u64((uint64_t)(2 * sz));  // 2^ceil(log2 2|S|)
         lr_item[i] = (uint8_t)std::max(l, lmin);
     }
+    tr.mark("offsets read, sizes");
     const int64_t nnz = off_h[n];
     h->nnz = nnz;
     h->size_orig_h.resize(n);
@@ -1488,6 +1511,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
                     gchunks.push_back({p, e0, std::min(len, e0 + kGChunk), ilog2_u64((uint64_t)c.r), 0});
             }
         }
+    tr.mark("sort, classes, chunks");
     // ---- device state
     BM_TRY(dalloc_t(&h->pos2orig_d, n, st));
     BM_TRY(dalloc_t(&h->orig2pos_d, n, st));
@@ -1538,6 +1562,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
             BM_CUDA(cudaMemcpyAsync(u.dst, from, u.bytes, cudaMemcpyHostToDevice, st));
         }
     }
+    tr.mark("allocs + uploads");
     if (o && (o->flags & BATMAP_CHECK_INPUT) && n) {
         BM_TRY(dalloc_t(&bad, 1, st));
         BM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
@@ -1669,10 +1694,17 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
         }
         rec(h, EV_I1, st);
         BM_CUDA(cudaGetLastError());
+        tr.mark("K1 launched");
         // plan the intersection of the full selection on the host while the build kernels run
-        if (attempt == 0) BM_TRY(prepare_full_k2(h, part, n_parts, st, plan_task.f.valid() ? plan_task.f.get() : nullptr));
+        if (attempt == 0) {
+            K2Prepared* hp = plan_task.f.valid() ? plan_task.f.get() : nullptr;
+            tr.mark("host plan joined");
+            BM_TRY(prepare_full_k2(h, part, n_parts, st, hp));
+            tr.mark("plan uploaded");
+        }
         unsigned long long Fh = 0;
         BM_TRY(read_scalar(st, fail_ctr, &Fh));
+        tr.mark("K1 done (sync)");
         F = (int64_t)Fh;
         if (F <= fail_cap) break;
         dfree(fails, st);
@@ -1708,6 +1740,7 @@ batmap_status build_collection(batmap_collection* h, const int64_t* offsets, con
     }
     BM_CUDA(cudaGetLastError());
     rec(h, EV_B1, st);  // the scratch buffers are freed on return
+    tr.mark("encode + post queued");
     h->build_timed = true;
     h->stats.launches_build = h->launches - l0;
     return BATMAP_OK;

@@ -316,7 +316,7 @@ __device__ __forceinline__ void work_epilogue(const Rect& r, int ti, int tj, int
 template <int BN>
 __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
     k2_tiled(const __grid_constant__ K2Maps prm, const Rect* __restrict__ rects, const Work* __restrict__ work,
-             int n_work, int* work_ctr, uint32_t* __restrict__ cnt, uint32_t* __restrict__ tail_buf,
+             int n_work, int* work_ctr, uint32_t* __restrict__ cnt, uint32_t* __restrict__ tail_buf, int tail_pieces,
              const int32_t* __restrict__ f, const uint8_t* __restrict__ lw, uint32_t thr, uint32_t use_f,
              Cand* __restrict__ out, unsigned long long* __restrict__ ctr, int64_t cap) {
     using Cfg = K2Cfg<BN>;
@@ -356,14 +356,20 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
         const int2 mt = meta[buf];
         if (mt.y && cur >= 0) {  // a new work item (or the end) begins: finish the previous one
             const Work wk = work[cur];
-            if (wk.tail) {  // a piece of a cut tail tile: partial counts to its slice, as 16 uint4
-                            // planes of kThreads (coalesced stores here and loads in k2_tail_threshold)
-                uint4* dst = reinterpret_cast<uint4*>(tail_buf + (int64_t)(wk.tail - 1) * (kBM * BN)) + threadIdx.x;
+            if (wk.tail) {  // a piece of a cut tail tile: partial counts added (red.global.add, in
+                            // L2) into its tile's one zeroed slice, laid out as 16 uint4 planes of
+                            // kThreads (coalesced loads in k2_tail_threshold); one slice per tile
+                            // instead of one per piece keeps the tail's writes in L2
+                uint32_t* dst = tail_buf + (int64_t)((wk.tail - 1) / tail_pieces) * (kBM * BN) + 4 * threadIdx.x;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    dst[(2 * i) * kThreads] = make_uint4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-                    dst[(2 * i + 1) * kThreads] = make_uint4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
-                }
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (acc[i][j])
+                            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(
+                                             dst + (int64_t)((2 * i + (j >> 2)) * kThreads) * 4 + (j & 3)),
+                                         "r"(acc[i][j])
+                                         : "memory");
             } else {
                 work_epilogue<BN>(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, lw, thr, use_f, out,
                                   ctr, cap);
@@ -972,7 +978,7 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
         h->launches += 1;
     }
     if (pl.cnt_entries) BM_TRY(ensure(&h->cnt_d, &h->cnt_cap, pl.cnt_entries, st));
-    const int64_t tail_words = (int64_t)pl.tails.size() * pl.tail_pieces * kBM * tn;
+    const int64_t tail_words = (int64_t)pl.tails.size() * kBM * tn;  // one slice per cut tail tile
     if (tail_words) BM_TRY(ensure(&h->tail_d, &h->tail_cap, tail_words, st));
     // per device (no process-wide flag)
     if (tn == 128)
@@ -991,25 +997,28 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
     for (int attempt = 0; attempt < 2; ++attempt) {
         BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, 2 * sizeof(unsigned long long), st));  // [1] = work counter
         if (pl.cnt_entries) BM_CUDA(cudaMemsetAsync(h->cnt_d, 0, pl.cnt_entries * sizeof(uint32_t), st));
+        if (tail_words) BM_CUDA(cudaMemsetAsync(h->tail_d, 0, tail_words * sizeof(uint32_t), st));
         rec(h, EV_K20, st);
         if (tn == 128)
             k2_tiled<128><<<grid, K2Cfg<128>::kThreads, K2Cfg<128>::kSmemBytes, st>>>(
-                *prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f,
+                *prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, h->tail_d, std::max(pl.tail_pieces, 1), sel.f,
+                kp->lw_d, threshold, use_f,
                 h->cand_d, h->ctr_d, h->cand_cap);
         else
             k2_tiled<64><<<grid, K2Cfg<64>::kThreads, K2Cfg<64>::kSmemBytes, st>>>(
-                *prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f,
+                *prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, h->tail_d, std::max(pl.tail_pieces, 1), sel.f,
+                kp->lw_d, threshold, use_f,
                 h->cand_d, h->ctr_d, h->cand_cap);
         rec(h, EV_K21, st);
         h->launches += 1;
         if (!pl.tails.empty()) {
             if (tn == 128)
                 k2_tail_threshold<128><<<(unsigned)pl.tails.size(), K2Cfg<128>::kThreads, 0, st>>>(
-                    kp->tails_d, pl.tail_pieces, rects_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
+                    kp->tails_d, 1, rects_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
                     h->ctr_d, h->cand_cap);
             else
                 k2_tail_threshold<64><<<(unsigned)pl.tails.size(), K2Cfg<64>::kThreads, 0, st>>>(
-                    kp->tails_d, pl.tail_pieces, rects_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
+                    kp->tails_d, 1, rects_d, h->tail_d, sel.f, kp->lw_d, threshold, use_f, h->cand_d,
                     h->ctr_d, h->cand_cap);
             h->launches += 1;
         }

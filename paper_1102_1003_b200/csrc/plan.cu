@@ -25,10 +25,13 @@ static void stable_sort_desc(std::vector<T>& v, Cost cost) {
     for (size_t e = 0; e < v.size(); ++e) {
         const int64_t c = cost(v[e]);
         if (c != last) {  // runs of equal cost are the common case
-            auto it = first_seen.emplace(c, (int32_t)keys.size());
-            if (it.second) keys.push_back(c);
+            auto it = first_seen.find(c);  // find first: emplace would allocate a node every time
+            if (it == first_seen.end()) {
+                it = first_seen.emplace(c, (int32_t)keys.size()).first;
+                keys.push_back(c);
+            }
             last = c;
-            last_id = it.first->second;
+            last_id = it->second;
         }
         bucket[e] = last_id;
     }
@@ -316,21 +319,27 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         }
     }
     stable_sort_desc(segs, [](const Seg& x) { return x.cost; });
-    struct WorkC {
+    // Work items are emitted in deal order.  The tiles of ordinary rectangles come out already in
+    // descending cost order (segments are sorted by their tile cost) and go straight into the
+    // reserved list; the k-pieces of accumulated tile rows (few) go to a side list with their deal
+    // position and are merged in from the back -- the stable descending sort of the deal order
+    // without sorting or re-allocating the 3e5 items of C4.
+    struct Side {
         Work w;
-        int64_t cost;
+        int64_t cost, pos;  // pos: main items dealt before it
     };
-    std::vector<WorkC> work;
+    std::vector<Side> side;
+    std::vector<Work>& items = P.work;
     {  // capacity: this part's share of the tiles, split tiles counted per piece
-        int64_t items = 0;
+        int64_t cnt = 0;
         for (const Rect& r : P.rects) {
             const int64_t ta = ceil_div(r.n_rows, kTile), tb = ceil_div(r.n_cols, TN);
             const int64_t nt = r.diag ? diag_tiles(r.n_rows, TN) : ta * tb;
             const int64_t nk = r.W / kChunk;
             const int64_t pieces = (r.acc && tile_cost(r) > 2 * target) ? std::min(nk, ceil_div(tile_cost(r), target)) : 1;
-            items += nt * pieces;
+            cnt += nt * pieces;
         }
-        work.reserve((size_t)(items / n_parts + 1024));
+        items.reserve((size_t)(cnt / n_parts + 8 * 1024));
     }
     // one unit of this part, in deal order: its algorithmic compares and its work items
     auto emit = [&](const Unit& u) {
@@ -338,32 +347,35 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         const int tb = (int)ceil_div(r.n_cols, TN);
         const int64_t rows = std::min<int64_t>(kTile, r.n_rows - (int64_t)u.ti * kTile);
         const int W_real = r.W * r.R;
+        const bool plain_w = P.eff_promo[r.cls_b] < 0;  // every column item has width W_real
         if (r.acc) P.units.push_back({u.rect, u.ti});
         // algorithmic compares of the pairs this unit owns: sum of max(W_i, W_j) = W_j (columns are
         // never narrower than rows: width-sorted positions)
         const int64_t r0 = (int64_t)u.ti * kTile;
         if (r.acc && r.diag) {
-            if (P.eff_promo[r.cls_b] < 0)
-                for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += (int64_t)(r.n_rows - 1 - q) * W_real;
-            else
+            if (plain_w) {
+                const int64_t a = r.n_rows - 1 - r0, b = r.n_rows - r0 - rows;  // sum_{q} (n-1-q), q in [r0, r0+rows)
+                P.word_compares += (a + b) * rows / 2 * W_real;
+            } else {
                 for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += sumW(r.cls_b, q + 1, r.n_rows);
+            }
         } else if (r.acc) {
             P.word_compares += rows * sumW(r.cls_b, 0, r.n_cols_real);
         }
         const int jb = u.tj >= 0 ? u.tj : (r.diag ? u.ti * QD : 0);
         const int je = u.tj >= 0 ? u.tj + 1 : tb;
+        const int nk = r.W / kChunk;
+        int pieces = 1;
+        if (r.acc && tile_cost(r) > 2 * target) pieces = (int)std::min<int64_t>(nk, ceil_div(tile_cost(r), target));
         for (int j = jb; j < je; ++j) {
             if (!r.acc) {
                 const int64_t c0 = (int64_t)j * TN, c1 = std::min<int64_t>(r.n_cols, c0 + TN);
                 if (r.diag && c0 < r0 + rows) {  // the tile straddles the diagonal: pairs q < col only
                     for (int64_t q = r0; q < r0 + rows; ++q) P.word_compares += sumW(r.cls_b, std::max(q + 1, c0), c1);
                 } else {
-                    P.word_compares += rows * sumW(r.cls_b, c0, c1);
+                    P.word_compares += plain_w ? rows * (c1 - c0) * W_real : rows * sumW(r.cls_b, c0, c1);
                 }
             }
-            const int nk = r.W / kChunk;
-            int pieces = 1;
-            if (r.acc && tile_cost(r) > 2 * target) pieces = (int)std::min<int64_t>(nk, ceil_div(tile_cost(r), target));
             for (int p = 0; p < pieces; ++p) {
                 Work w{};
                 w.rect = u.rect;
@@ -372,7 +384,8 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 w.k0 = (int32_t)((int64_t)nk * p / pieces);
                 w.k1 = (int32_t)((int64_t)nk * (p + 1) / pieces);
                 const int64_t c = (int64_t)(w.k1 - w.k0) * kChunk * kTile * TN;
-                work.push_back({w, c});
+                if (r.acc) side.push_back({w, c, (int64_t)items.size()});
+                else items.push_back(w);
                 P.tile_compares += c;
             }
         }
@@ -390,9 +403,14 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 for (int i = 0; i < ta && next < g.count; ++i) {
                     const int j0 = r.diag ? i * QD : 0;
                     const int64_t row_n = tb - j0;
-                    while (next < t + row_n) {  // the row's tiles this part takes
-                        emit(Unit{g.rect, i, (int32_t)(j0 + (next - t)), g.cost});
-                        next += n_parts;
+                    if (n_parts == 1 && next == t) {  // the whole row: one unit of all its tiles
+                        emit(Unit{g.rect, i, -1, g.cost});
+                        next += row_n;
+                    } else {
+                        while (next < t + row_n) {  // the row's tiles this part takes
+                            emit(Unit{g.rect, i, (int32_t)(j0 + (next - t)), g.cost});
+                            next += n_parts;
+                        }
                     }
                     t += row_n;
                 }
@@ -400,20 +418,34 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             at += g.count;
         }
     }
-    // units come in cost order; only split rows (pieces cheaper than their unit) can break it
-    if (!std::is_sorted(work.begin(), work.end(), [](const WorkC& x, const WorkC& y) { return x.cost > y.cost; }))
-        stable_sort_desc(work, [](const WorkC& x) { return x.cost; });
+    auto work_cost = [&](const Work& w) { return (int64_t)(w.k1 - w.k0) * kChunk * kTile * TN; };
+    if (!side.empty()) {  // stable by (cost desc, deal position); main items are sorted by cost
+        std::stable_sort(side.begin(), side.end(), [](const Side& x, const Side& y) { return x.cost > y.cost; });
+        const size_t nm = items.size(), ns = side.size();
+        items.resize(nm + ns);
+        int64_t a = (int64_t)nm - 1, b = (int64_t)ns - 1, o = (int64_t)(nm + ns) - 1;
+        while (b >= 0) {  // from the back: the later of the two tails goes last
+            bool take_main = false;
+            if (a >= 0) {
+                const int64_t ca = work_cost(items[a]);
+                take_main = ca < side[b].cost || (ca == side[b].cost && side[b].pos <= a);
+            }
+            if (take_main) items[o--] = items[a--];
+            else items[o--] = side[b--].w;
+        }
+    }
     // ---- the tail of the schedule: the last grid_cap items (the shortest, claimed last) are whole
     // tiles of ordinary rectangles; cut each into pieces along k so that the CTAs finish within a
     // piece of each other (C2: makespan/mean 1.046 -> 1.005 in the planner's cost model).  The
-    // pieces write partial counts to their own slices; k2_tail_threshold sums and tests them.
-    if (allow_split && grid_cap > 0 && !work.empty()) {
+    // pieces add their partial counts into one slice per tile (red.global.add); k2_tail_threshold tests them.
+    if (allow_split && grid_cap > 0 && !P.work.empty()) {
+        std::vector<Work>& work = P.work;
         const size_t n = work.size();
         const size_t begin = n > (size_t)grid_cap ? n - (size_t)grid_cap : 0;
-        std::vector<WorkC> pieces;
+        std::vector<Work> pieces;
         int pcs = 0;
         for (size_t k = begin; k < n; ++k) {
-            const Work w = work[k].w;
+            const Work w = work[k];
             const Rect& r = P.rects[w.rect];
             const int nk = r.W / kChunk;
             if (pcs == 0) pcs = nk >= 64 ? 8 : (nk >= 16 ? 4 : (nk >= 4 ? 2 : 1));
@@ -425,22 +457,19 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 wp.k0 = (int32_t)((int64_t)nk * p / pcs);
                 wp.k1 = (int32_t)((int64_t)nk * (p + 1) / pcs);
                 wp.tail = 1 + t * pcs + p;
-                const WorkC wc{wp, (int64_t)(wp.k1 - wp.k0) * kChunk * kTile * TN};
-                if (p == 0) work[k] = wc;
-                else pieces.push_back(wc);
+                if (p == 0) work[k] = wp;
+                else pieces.push_back(wp);
             }
         }
         if (!P.tails.empty()) {  // everything before `begin` costs at least as much: re-sort the tail only
             P.tail_pieces = pcs;
-            std::vector<WorkC> tail(work.begin() + (long)begin, work.end());
+            std::vector<Work> tail(work.begin() + (long)begin, work.end());
             tail.insert(tail.end(), pieces.begin(), pieces.end());
-            stable_sort_desc(tail, [](const WorkC& x) { return x.cost; });
+            stable_sort_desc(tail, work_cost);
             work.resize(begin);
             work.insert(work.end(), tail.begin(), tail.end());
         }
     }
-    P.work.reserve(work.size());
-    for (const WorkC& w : work) P.work.push_back(w.w);
 }
 
 }  // namespace bm

@@ -1,4 +1,7 @@
-"""Summarise an ncu report of the K2 kernel: key metrics and the warp-stall breakdown."""
+"""Summarise an ncu report (every kernel in it): key metrics and the warp-stall breakdown.
+
+    python tools/ncu_summary.py report.ncu-rep [more.ncu-rep ...]
+"""
 import csv
 import io
 import subprocess
@@ -14,15 +17,26 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg", "sm__cycles_elapsed.
         "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
         "smsp__inst_executed_op_shared_ld.sum", "launch__grid_size", "launch__block_size",
-        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__inst_executed_op_shared_atom.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+        "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum", "smsp__thread_inst_executed_per_inst_executed.ratio",
+        "lts__t_sectors_op_write.sum", "lts__t_sectors_op_read.sum"]
 
 
 def main(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    d = dict(zip(hdr, vals))
+    hdr, units = rows[0], rows[1]
     u = dict(zip(hdr, units))
+    res = []
+    for vals in rows[2:]:
+        d = dict(zip(hdr, vals))
+        print(f"== {path}: {d.get('Kernel Name', '?')[:100]}")
+        res.append(summ(d, u))
+    return res
+
+
+def summ(d, u):
     out = {}
     for k in KEYS:
         if k in d:
@@ -42,4 +56,5 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    for p in sys.argv[1:]:
+        main(p)
