@@ -110,17 +110,53 @@ struct Ops {
     uint4 xa, xb, ya, yb, ma, mb, na, nb;
 };
 
-template <int BN>
-__device__ __forceinline__ void load_ops(Ops& o, const uint32_t* sA, const uint32_t* sB, const uint32_t* mA,
-                                         const uint32_t* mB, int k, int tr, int tc) {
-    o.xa = *reinterpret_cast<const uint4*>(sA + k * kBM + 4 * tr);
-    o.xb = *reinterpret_cast<const uint4*>(sA + k * kBM + 64 + 4 * tr);
-    o.ya = *reinterpret_cast<const uint4*>(sB + k * BN + 4 * tc);
-    o.yb = *reinterpret_cast<const uint4*>(sB + k * BN + BN / 2 + 4 * tc);
-    o.ma = *reinterpret_cast<const uint4*>(mA + k * kBM + 4 * tr);
-    o.mb = *reinterpret_cast<const uint4*>(mA + k * kBM + 64 + 4 * tr);
-    o.na = *reinterpret_cast<const uint4*>(mB + k * BN + 4 * tc);
-    o.nb = *reinterpret_cast<const uint4*>(mB + k * BN + BN / 2 + 4 * tc);
+// The thread's 8 x 8 micro-tile is four 4 x 4 blocks: bit 0 LL (rows 4tr.., cols 4tc..), bit 1 LH
+// (cols BN/2 + 4tc..), bit 2 HL (rows 64 + 4tr..), bit 3 HH.  INC is the set a warp computes for the
+// current work item; blocks whose pairs are all invalid (below the diagonal of a diagonal tile, or
+// beyond a ragged edge) are skipped, with their operands' loads (block_mask).
+constexpr int kLL = 1, kLH = 2, kHL = 4, kHH = 8, kAll = 15;
+
+template <int BN, int INC = kAll>
+__device__ __forceinline__ void load_ops(Ops& o, const uint32_t* pa, const uint32_t* pb) {
+    // pa = sA + 4 tr + k kBM (row words; masks kStageWords further), pb = sB + 4 tc + k BN
+    constexpr int kM = K2Cfg<BN>::kStageWords;  // offset of the mask plane
+    if (INC & (kLL | kLH)) {
+        o.xa = *reinterpret_cast<const uint4*>(pa);
+        o.ma = *reinterpret_cast<const uint4*>(pa + kM);
+    }
+    if (INC & (kHL | kHH)) {
+        o.xb = *reinterpret_cast<const uint4*>(pa + 64);
+        o.mb = *reinterpret_cast<const uint4*>(pa + kM + 64);
+    }
+    if (INC & (kLL | kHL)) {
+        o.ya = *reinterpret_cast<const uint4*>(pb);
+        o.na = *reinterpret_cast<const uint4*>(pb + kM);
+    }
+    if (INC & (kLH | kHH)) {
+        o.yb = *reinterpret_cast<const uint4*>(pb + BN / 2);
+        o.nb = *reinterpret_cast<const uint4*>(pb + kM + BN / 2);
+    }
+}
+
+// Index i * 8 + j of the q-th pair of the included blocks of INC (blocks in bit order, rows major
+// inside a block); constant-folded in the unrolled loops.
+template <int INC>
+__device__ __forceinline__ constexpr int pair_index(int q) {
+    int b = 0;
+    for (int t = 0, seen = 0; t < 4; ++t)
+        if (INC >> t & 1) {
+            if (seen == (q >> 4)) {
+                b = t;
+                break;
+            }
+            ++seen;
+        }
+    return ((b >> 1) * 4 + ((q >> 2) & 3)) * 8 + (b & 1) * 4 + (q & 3);
+}
+
+template <int INC>
+__device__ __forceinline__ constexpr int n_included() {
+    return 16 * ((INC & 1) + (INC >> 1 & 1) + (INC >> 2 & 1) + (INC >> 3 & 1));
 }
 
 // The 64 compare-and-counts of one k step, written as a software pipeline over the pairs so
@@ -129,27 +165,60 @@ __device__ __forceinline__ void load_ops(Ops& o, const uint32_t* sA, const uint3
 // pipeline steps apart (kD = 2: two independent compares between a producer and its consumer).
 // asm volatile keeps this order.  (tools/swar_ubench.cu: distance 2 runs 1.5 % faster than 1, 3
 // and 4 are slower again; the compiler-scheduled loop is ~4 % slower.)
+template <int INC = kAll>
 __device__ __forceinline__ void compute_ops(const Ops& o, uint32_t (&acc)[8][8]) {
     constexpr int kD = 2;
+    constexpr int N = n_included<INC>();
     const uint32_t x[8] = {o.xa.x, o.xa.y, o.xa.z, o.xa.w, o.xb.x, o.xb.y, o.xb.z, o.xb.w};
     const uint32_t y[8] = {o.ya.x, o.ya.y, o.ya.z, o.ya.w, o.yb.x, o.yb.y, o.yb.z, o.yb.w};
     const uint32_t xm[8] = {o.ma.x, o.ma.y, o.ma.z, o.ma.w, o.mb.x, o.mb.y, o.mb.z, o.mb.w};
     const uint32_t ym[8] = {o.na.x, o.na.y, o.na.z, o.na.w, o.nb.x, o.nb.y, o.nb.z, o.nb.w};
     uint32_t u[64], p[64], v[64];
 #pragma unroll
-    for (int q = 0; q < 64 + 3 * kD; ++q) {
-        if (q < 64)  // u = (x ^ y) | 0x80808080
-            asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[q]) : "r"(x[q >> 3]), "r"(y[q & 7]));
-        if (q >= kD && q - kD < 64)  // p = u - 0x01010101
-            asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - kD]) : "r"(u[q - kD]));
-        if (q >= 2 * kD && q - 2 * kD < 64) {  // v = ~p & (xm | ym)
-            const int e = q - 2 * kD;
+    for (int q = 0; q < N + 3 * kD; ++q) {
+        if (q < N) {  // u = (x ^ y) | 0x80808080
+            const int e = pair_index<INC>(q);
+            asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[e]) : "r"(x[e >> 3]), "r"(y[e & 7]));
+        }
+        if (q >= kD && q - kD < N) {  // p = u - 0x01010101
+            const int e = pair_index<INC>(q - kD);
+            asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[e]) : "r"(u[e]));
+        }
+        if (q >= 2 * kD && q - 2 * kD < N) {  // v = ~p & (xm | ym)
+            const int e = pair_index<INC>(q - 2 * kD);
             asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v[e]) : "r"(p[e]), "r"(xm[e >> 3]), "r"(ym[e & 7]));
         }
         if (q >= 3 * kD) {  // acc += 128 * matches
-            const int e = q - 3 * kD;
+            const int e = pair_index<INC>(q - 3 * kD);
             asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;" : "+r"(acc[e >> 3][e & 7]) : "r"(v[e]));
         }
+    }
+}
+
+// Blocks of the micro-tile that warp `warp` computes on tile (ti, tj) of rectangle r: a block is
+// skipped when all its rows or all its columns lie beyond the rectangle, or -- diagonal
+// rectangles, pairs i < j only -- when its smallest row is >= its largest column.
+template <int BN>
+__device__ __forceinline__ int block_mask(const Rect& r, int ti, int tj, int warp) {
+    int inc = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int r0 = ti * kBM + (t >> 1) * 64 + 32 * (warp & 1);          // rows [r0, r0 + 32)
+        const int c0 = tj * BN + (t & 1) * (BN / 2) + 16 * (warp >> 1);     // cols [c0, c0 + 16)
+        const bool skip = r0 >= r.n_rows || c0 >= r.n_cols || (r.diag && r0 >= c0 + 15);
+        if (!skip) inc |= 1 << t;
+    }
+    return inc;
+}
+
+// One k-chunk of the warp's included blocks; pa / pb: the thread's first row / column words.
+template <int BN, int INC>
+__device__ __forceinline__ void chunk_ops(const uint32_t* pa, const uint32_t* pb, uint32_t (&acc)[8][8]) {
+#pragma unroll 1
+    for (int k = 0; k < kBK; ++k, pa += kBM, pb += BN) {
+        Ops o;
+        load_ops<BN, INC>(o, pa, pb);
+        compute_ops<INC>(o, acc);
     }
 }
 
@@ -349,7 +418,7 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0;
     int cur = -1;
-    bool warp_active = true;
+    int inc = kAll;
     for (uint32_t g = 0;; ++g) {
         const int buf = (int)(g % kStages);
         mbar_wait(&full[buf], (g / kStages) & 1u);
@@ -381,11 +450,10 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
         }
         if (mt.x < 0) break;
         if (mt.y) {
-            // ragged edge tiles: a warp whose rows (from 32 (warp & 1)) or columns (from 16 (warp >> 1))
-            // all lie beyond the rectangle skips the compute, leaving its issue slots to the other CTA
+            // ragged edge and diagonal tiles: blocks of pairs that are all invalid are skipped,
+            // leaving their issue slots to the other CTA
             const Work wk = work[mt.x];
-            const Rect& r = rects[wk.rect];
-            warp_active = 32 * (warp & 1) < r.n_rows - wk.ti * kBM && 16 * (warp >> 1) < r.n_cols - wk.tj * BN;
+            inc = block_mask<BN>(rects[wk.rect], wk.ti, wk.tj, warp);
         }
         cur = mt.x;
         uint32_t* sA = stages + buf * kStageSmem;
@@ -406,15 +474,19 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
         if (threadIdx.x == 0)
             issue_next<BN>(prm, pre, rects, work, n_work, work_ctr, stages, (int)((g + kStages - 1) % kStages),
                            full, meta, end_sent);
-        const uint32_t* sB = sA + kBK * kBM;
-        const uint32_t* mA = sA + kStageWords;
-        const uint32_t* mB = mA + kBK * kBM;
-        if (warp_active) {
-#pragma unroll 1
-            for (int k = 0; k < kBK; ++k) {
-                Ops o;
-                load_ops<BN>(o, sA, sB, mA, mB, k, tr, tc);
-                compute_ops(o, acc);
+        const uint32_t* pa = sA + 4 * tr;
+        const uint32_t* pb = sA + kBK * kBM + 4 * tc;
+        if (inc == kAll) {  // the common case first: one test on the hot path
+            chunk_ops<BN, kAll>(pa, pb, acc);
+        } else {
+            switch (inc) {  // the reachable block sets; any other non-empty set computes all four
+                case 0: break;
+                case kLL | kLH | kHH: chunk_ops<BN, kLL | kLH | kHH>(pa, pb, acc); break;  // diagonal tiles
+                case kLL | kLH: chunk_ops<BN, kLL | kLH>(pa, pb, acc); break;
+                case kLH: chunk_ops<BN, kLH>(pa, pb, acc); break;
+                case kLL | kHL: chunk_ops<BN, kLL | kHL>(pa, pb, acc); break;
+                case kLL: chunk_ops<BN, kLL>(pa, pb, acc); break;
+                default: chunk_ops<BN, kAll>(pa, pb, acc); break;
             }
         }
     }

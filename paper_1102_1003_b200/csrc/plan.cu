@@ -160,6 +160,17 @@ int64_t plan_cost(const std::vector<ClassInfo>& cls, bool allow_virtual, bool al
     return est_cost(n, W, cw, allow_virtual, tn);
 }
 
+// Tile rows per band of the grouped tile order: a band of row tiles of ~32 MB stays in L2 while the
+// columns stream past it.  BATMAP_K2_GROUP=<rows> overrides (1 = row-major).
+static int group_rows(const Rect& r, int ta) {
+    const char* e = getenv("BATMAP_K2_GROUP");  // once per rectangle
+    const int env = e ? atoi(e) : 0;
+    if (env > 0) return std::min(env, std::max(ta, 1));
+    const int64_t row_bytes = (int64_t)kTile * r.W_a * 4;
+    const int64_t g = (int64_t(32) << 20) / std::max<int64_t>(row_bytes, 1);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, std::max(ta, 1)));
+}
+
 void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int grid_cap, bool allow_virtual,
                bool allow_split, bool allow_promote, Plan* out, int tn) {
     Plan& P = *out;
@@ -399,20 +410,50 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             } else if (t0 < g.count) {
                 const Rect& r = P.rects[g.rect];
                 const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, TN);
-                int64_t t = 0, next = t0;  // unit index at the start of row i; next unit of this part
-                for (int i = 0; i < ta && next < g.count; ++i) {
-                    const int j0 = r.diag ? i * QD : 0;
-                    const int64_t row_n = tb - j0;
-                    if (n_parts == 1 && next == t) {  // the whole row: one unit of all its tiles
-                        emit(Unit{g.rect, i, -1, g.cost});
-                        next += row_n;
+                // Tiles in grouped order: bands of G tile rows, column by column inside a band, so
+                // the CTAs running at once share a band of row tiles (kept in L2) and each column
+                // tile is fetched from HBM once per band instead of once per tile row (C4: the
+                // 2.4 GB class would otherwise stream ~780 / 2 times).  G = 1 is row-major.
+                const int G = group_rows(r, ta);
+                if (n_parts == 1) {  // every tile is this part's: closed-form compares, bare items
+                    const bool plain_w = P.eff_promo[r.cls_b] < 0;
+                    if (r.diag) {
+                        const int64_t n = r.n_rows;
+                        if (plain_w) P.word_compares += n * (n - 1) / 2 * r.W;
+                        else
+                            for (int64_t q = 0; q + 1 < n; ++q) P.word_compares += sumW(r.cls_b, q + 1, n);
                     } else {
-                        while (next < t + row_n) {  // the row's tiles this part takes
-                            emit(Unit{g.rect, i, (int32_t)(j0 + (next - t)), g.cost});
-                            next += n_parts;
+                        P.word_compares += (int64_t)r.n_rows * (plain_w ? (int64_t)r.n_cols * r.W : sumW(r.cls_b, 0, r.n_cols));
+                    }
+                    const int nk = r.W / kChunk;
+                    P.tile_compares += g.count * (int64_t)nk * kChunk * kTile * TN;
+                    for (int i0 = 0; i0 < ta; i0 += G) {
+                        const int i1 = std::min(ta, i0 + G);
+                        for (int j = r.diag ? i0 * QD : 0; j < tb; ++j) {
+                            const int ie = r.diag ? std::min(i1, j / QD + 1) : i1;
+                            for (int i = i0; i < ie; ++i) items.push_back(Work{g.rect, i, j, 0, nk, 0});
                         }
                     }
-                    t += row_n;
+                    at += g.count;
+                    continue;
+                }
+                int64_t t = 0, next = t0;  // unit index at the start of band i0; next unit of this part
+                for (int i0 = 0; i0 < ta && next < g.count; i0 += G) {
+                    const int i1 = std::min(ta, i0 + G);
+                    int64_t band_n = 0;
+                    for (int i = i0; i < i1; ++i) band_n += tb - (r.diag ? i * QD : 0);
+                    if (next >= t + band_n) {  // none of this band's tiles is this part's
+                        t += band_n;
+                        continue;
+                    }
+                    for (int j = r.diag ? i0 * QD : 0; j < tb; ++j) {
+                        const int ie = r.diag ? std::min(i1, j / QD + 1) : i1;  // rows with i * QD <= j
+                        for (int i = i0; i < ie; ++i, ++t)
+                            if (t == next) {
+                                emit(Unit{g.rect, i, j, g.cost});
+                                next += n_parts;
+                            }
+                    }
                 }
             }
             at += g.count;

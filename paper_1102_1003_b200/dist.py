@@ -57,6 +57,8 @@ def build_distributed(offsets, tids, n_transactions: int, group=None, **kw):
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     c = Collection(offsets, tids, n_transactions, part=rank, n_parts=world, **kw)
+    if world == 1:  # a one-part build is the whole build: nothing to exchange
+        return c
     stride_w = max(c.shard_sizes(p)[0] for p in range(world))
     nf = torch.tensor([c.shard_sizes(rank)[1]], dtype=torch.int64, device=offsets.device)
     counts = _all_gather_flat(nf, group)

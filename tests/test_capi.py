@@ -237,3 +237,19 @@ def test_cli_builds_and_prints_usage():
     assert r.returncode == 2 and "usage" in r.stderr
     r = subprocess.run([exe, "/nonexistent.dat", "0"], capture_output=True, text=True)
     assert r.returncode == 2  # min_support 0 rejected before any I/O
+
+
+def test_plan_work_grouped_tile_order(monkeypatch):
+    """Tiles of an ordinary rectangle come in bands of G tile rows (column by column inside a band),
+    G = 32 MB / (128 W_a 4 B): the first grid of CTAs shares a band of row tiles, and each column
+    tile streams from HBM once per band.  BATMAP_K2_GROUP=1 is row-major.  Same tiles either way."""
+    cn, cw = [6000], [6144]  # C4's narrow class shape: 3 MB per tile row -> G = 10
+    items = _collect(cn, cw, 1)[0][0]
+    first = items[:296]
+    assert set(first[:, 2].tolist()) == set(range(10))  # ti in the first band
+    assert (np.diff(first[:, 3]) >= 0).all()  # columns ascend inside the band
+    monkeypatch.setenv("BATMAP_K2_GROUP", "1")
+    rows = _collect(cn, cw, 1)[0][0]
+    assert (rows[:40, 2] == 0).all() and (rows[:40, 3] == np.arange(40)).all()
+    # the same tiles (the last grid's worth may be cut into k-pieces differently)
+    assert np.array_equal(np.unique(items[:, :4], axis=0), np.unique(rows[:, :4], axis=0))
