@@ -161,11 +161,16 @@ int64_t plan_cost(const std::vector<ClassInfo>& cls, bool allow_virtual, bool al
 }
 
 // Tile rows per band of the grouped tile order: a band of row tiles of ~32 MB stays in L2 while the
-// columns stream past it.  BATMAP_K2_GROUP=<rows> overrides (1 = row-major).
+// columns stream past it; rectangles whose operands fit in L2 together (<= 96 MB) stay row-major,
+// which re-reads least (measured K2 DRAM reads, profiles/r2_k2_order_dram.json: C4 G = 1 / 2 / 4 /
+// 10 / 20 / 40: 988 / 697 / 432 / 227 / 293 / 684 GB; C2 G = 1 / 4 / 8 / 16 / 42: 130 / 133 / 138 /
+// 146 / 152 MB; K2 time unchanged within 0.1 % in every case).  BATMAP_K2_GROUP=<rows> overrides.
 static int group_rows(const Rect& r, int ta) {
     const char* e = getenv("BATMAP_K2_GROUP");  // once per rectangle
     const int env = e ? atoi(e) : 0;
     if (env > 0) return std::min(env, std::max(ta, 1));
+    const int64_t op_bytes = 4ll * ((int64_t)r.n_rows * r.W_a + (r.diag ? 0 : (int64_t)r.n_cols * r.W));
+    if (op_bytes <= (int64_t(96) << 20)) return 1;
     const int64_t row_bytes = (int64_t)kTile * r.W_a * 4;
     const int64_t g = (int64_t(32) << 20) / std::max<int64_t>(row_bytes, 1);
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, std::max(ta, 1)));
@@ -475,10 +480,12 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             else items[o--] = side[b--].w;
         }
     }
-    // ---- the tail of the schedule: the last grid_cap items (the shortest, claimed last) are whole
-    // tiles of ordinary rectangles; cut each into pieces along k so that the CTAs finish within a
-    // piece of each other (C2: makespan/mean 1.046 -> 1.005 in the planner's cost model).  The
-    // pieces add their partial counts into one slice per tile (red.global.add); k2_tail_threshold tests them.
+    // ---- the tail of the schedule: the last grid_cap items (the shortest, claimed last) are cut
+    // into pieces along k so that the CTAs finish within a piece of each other.  Whole tiles of
+    // ordinary rectangles (C2: makespan/mean 1.046 -> 1.005 in the planner's cost model) add their
+    // pieces' partial counts into one slice per tile (red.global.add), which k2_tail_threshold
+    // tests; k-pieces of accumulated rectangles are cut finer and add into their counters as before
+    // (C3: 2,391 items of 22-24 chunks on 592 CTAs left 23 CTAs a fifth item, makespan/mean 1.22).
     if (allow_split && grid_cap > 0 && !P.work.empty()) {
         std::vector<Work>& work = P.work;
         const size_t n = work.size();
@@ -489,8 +496,20 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             const Work w = work[k];
             const Rect& r = P.rects[w.rect];
             const int nk = r.W / kChunk;
+            if (r.acc) {  // a k-piece of an accumulated rectangle: cut it finer, the counters add up
+                const int len = w.k1 - w.k0;
+                const int ap = len >= 64 ? 8 : (len >= 16 ? 4 : (len >= 4 ? 2 : 1));
+                for (int p = 0; p < ap; ++p) {
+                    Work wp = w;
+                    wp.k0 = w.k0 + (int32_t)((int64_t)len * p / ap);
+                    wp.k1 = w.k0 + (int32_t)((int64_t)len * (p + 1) / ap);
+                    if (p == 0) work[k] = wp;
+                    else pieces.push_back(wp);
+                }
+                continue;
+            }
             if (pcs == 0) pcs = nk >= 64 ? 8 : (nk >= 16 ? 4 : (nk >= 4 ? 2 : 1));
-            if (pcs < 2 || r.acc || w.k0 != 0 || w.k1 != nk || nk < 2 * pcs) continue;
+            if (pcs < 2 || w.k0 != 0 || w.k1 != nk || nk < 2 * pcs) continue;
             const int t = (int)P.tails.size();
             P.tails.push_back({w.rect, w.ti, w.tj, 0});
             for (int p = 0; p < pcs; ++p) {
@@ -502,8 +521,8 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 else pieces.push_back(wp);
             }
         }
-        if (!P.tails.empty()) {  // everything before `begin` costs at least as much: re-sort the tail only
-            P.tail_pieces = pcs;
+        if (!P.tails.empty()) P.tail_pieces = pcs;
+        if (!pieces.empty()) {  // everything before `begin` costs at least as much: re-sort the tail only
             std::vector<Work> tail(work.begin() + (long)begin, work.end());
             tail.insert(tail.end(), pieces.begin(), pieces.end());
             stable_sort_desc(tail, work_cost);
