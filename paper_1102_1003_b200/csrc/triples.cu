@@ -81,18 +81,30 @@ __global__ void __launch_bounds__(256) k3_insert(const Chunk3* __restrict__ chun
     const int32_t* S = tids + offsets[ch.item];
     uint32_t* A = work + woff[ch.item];
     const uint32_t max_loop = max_loop_opt ? max_loop_opt : 16u + 3u * (uint32_t)lr;
-    for (int e = ch.e0 + threadIdx.x; e < ch.e1; e += blockDim.x) {
-        const uint32_t x = (uint32_t)__ldg(S + e);
-        for (int copy = 0; copy < 3; ++copy) {
-            uint32_t tau = x;
-            for (uint32_t l = 0; l < max_loop && tau != kEmpty; ++l)
+    // persistent lanes: one swap per iteration; a lane whose chain ends (placed, or nestless after
+    // MaxLoop rounds) starts its next copy / element at once instead of idling until the warp's
+    // longest chain (a failing one runs 4 MaxLoop swaps) ends
+    // (one round of the four tables per iteration: the table index stays a compile-time constant,
+    // so π's round keys stay kernel-parameter constants)
+    int e = ch.e0 + (int)threadIdx.x, copy = 0;
+    uint32_t l = 0;
+    uint32_t tau = e < ch.e1 ? (uint32_t)__ldg(S + e) : kEmpty;
+    while (e < ch.e1) {
 #pragma unroll
-                for (int t = 0; t < 4 && tau != kEmpty; ++t)
-                    tau = atomicExch(&A[slot4(t, pi4_eval(P, t, tau), r, r0, log2r0)], tau);
-            if (tau != kEmpty) {
-                const unsigned long long idx = atomicAdd(fail_ctr, 1ull);
-                if ((int64_t)idx < fail_cap) fails[idx] = ((uint64_t)ch.item << 32) | tau;
+        for (int t = 0; t < 4; ++t)
+            if (tau != kEmpty) tau = atomicExch(&A[slot4(t, pi4_eval(P, t, tau), r, r0, log2r0)], tau);
+        if (tau != kEmpty && ++l == max_loop) {  // nestless after MaxLoop rounds: a failure
+            const unsigned long long idx = atomicAdd(fail_ctr, 1ull);
+            if ((int64_t)idx < fail_cap) fails[idx] = ((uint64_t)ch.item << 32) | tau;
+            tau = kEmpty;
+        }
+        if (tau == kEmpty) {  // chain done: the next copy, or the next element
+            l = 0;
+            if (++copy == 3) {
+                copy = 0;
+                e += blockDim.x;
             }
+            if (e < ch.e1) tau = (uint32_t)__ldg(S + e);
         }
     }
 }
@@ -172,44 +184,40 @@ __global__ void k3_insert_serial(const int64_t* __restrict__ offsets, const int3
     }
 }
 
-// Encode (reading #29), element by element: one thread per CSR entry of the item range.
-__global__ void __launch_bounds__(256) k3_encode(const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids,
-                                                 const int32_t* __restrict__ item_of_entry_unused, int64_t n,
-                                                 const int64_t* __restrict__ woff, const uint8_t* __restrict__ log2r,
-                                                 Pi4 P, uint32_t r0, int log2r0, const uint32_t* __restrict__ work,
-                                                 uint8_t* __restrict__ arena) {
-    // grid-stride over items x elements: a warp per item keeps the offsets read cheap
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += n_warps) {
-        const uint32_t r = 1u << log2r[i];
-        const uint32_t* A = work + woff[i];
-        uint8_t* B = arena + woff[i];  // 4r bytes per item, same offsets as the working table
-        for (int64_t k = offsets[i] + lane; k < offsets[i + 1]; k += 32) {
-            const uint32_t x = (uint32_t)__ldg(tids + k);
-            uint32_t q[4], cd[4];
-            int have = 0, missing = -1;
+// Encode (reading #29), element by element: one CTA per chunk of an item's elements (the chunks of
+// k3_insert), one thread per element.  (One warp per item took 1.2 ms on C3: 1,000 warps.)
+__global__ void __launch_bounds__(256) k3_encode(const Chunk3* __restrict__ chunks, const int64_t* __restrict__ offsets,
+                                                 const int32_t* __restrict__ tids, const int64_t* __restrict__ woff,
+                                                 const uint8_t* __restrict__ log2r, Pi4 P, uint32_t r0, int log2r0,
+                                                 const uint32_t* __restrict__ work, uint8_t* __restrict__ arena) {
+    const Chunk3 ch = chunks[blockIdx.x];
+    const uint32_t r = 1u << log2r[ch.item];
+    const int32_t* S = tids + offsets[ch.item];
+    const uint32_t* A = work + woff[ch.item];
+    uint8_t* B = arena + woff[ch.item];  // 4r bytes per item, same offsets as the working table
+    for (int e = ch.e0 + threadIdx.x; e < ch.e1; e += blockDim.x) {
+        const uint32_t x = (uint32_t)__ldg(S + e);
+        uint32_t q[4], cd[4];
+        int have = 0, missing = -1;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const uint32_t v = pi4_eval(P, t, x);
-                q[t] = slot4(t, v, r, r0, log2r0);
-                cd[t] = v >> P.s;
-                if (A[q[t]] == x) ++have;
-                else missing = t;
-            }
-            if (have != 3) continue;  // failed element: no copy left
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t v = pi4_eval(P, t, x);
+            q[t] = slot4(t, v, r, r0, log2r0);
+            cd[t] = v >> P.s;
+            if (A[q[t]] == x) ++have;
+            else missing = t;
+        }
+        if (have != 3) continue;  // failed element: no copy left
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                if (t == missing) continue;
-                uint32_t byte = cd[t];
-                if (t == 0) byte |= 0x40u;
-                else {
-                    if (missing == 0) byte |= 0x40u;
-                    if (t >= 2 && missing == 1) byte |= 0x80u;
-                }
-                B[q[t]] = (uint8_t)byte;
+        for (int t = 0; t < 4; ++t) {
+            if (t == missing) continue;
+            uint32_t byte = cd[t];
+            if (t == 0) byte |= 0x40u;
+            else {
+                if (missing == 0) byte |= 0x40u;
+                if (t >= 2 && missing == 1) byte |= 0x80u;
             }
+            B[q[t]] = (uint8_t)byte;
         }
     }
 }
@@ -287,6 +295,152 @@ __global__ void __launch_bounds__(256) k3_triples(const int32_t* __restrict__ ca
     }
 }
 
+// Grouped variant (r_0 >= 16, so the 4 words of a 16-byte load share a table): one CTA per kG3
+// consecutive candidates.  Candidates come sorted by (i, j, k) from the Apriori join, so runs of
+// them share (i, j); in a run, B_i's and B_j's words (and the parts of reading #30 that depend on
+// them only) are loaded once per 4 words and reused for every k, and only B_k is read per
+// candidate: ~1 instead of 3 L2 loads per word-triple on C3 (4.5 candidates per frequent pair).
+constexpr int kG3 = 8;
+constexpr int kG3Threads = 128;
+
+// Reading #30 with the (a, b) half of a word hoisted out of the loop over k: every value below
+// keeps only bit 6 of each byte lane.  With p = ((a ^ c) | 0xC0C0C0C0) - 0x01010101 (bit 6 of ~p:
+// the codes of a and c are equal; no borrow crosses a lane) and c1 = c >> 1 (B2 moved to bit 6):
+//   t = 0: e0 & a & ~p                   (codes equal, B1 of a)
+//   t = 1: e0 & ~p & (o1 | c)            (any B1)
+//   t = 2: ... & (o2 | c1)               (and any B2)
+//   t = 3: ... & (n | ~(c | c1))         (and some member holding neither)
+// and acc += dp4a(f, 0x01010101) adds 64 per counted entry.
+struct PairWord {
+    uint32_t a, e0, o1, o2, n;
+};
+
+template <int T>
+__device__ __forceinline__ PairWord pair_word(uint32_t a, uint32_t b) {  // only what table T needs
+    constexpr uint32_t M6 = 0x40404040u;
+    PairWord p;
+    p.a = a;
+    p.e0 = ~(((a ^ b) | 0xC0C0C0C0u) - 0x01010101u) & M6;  // codes of a and b equal
+    if (T >= 1) p.o1 = (a | b) & M6;
+    if (T >= 2) p.o2 = ((a | b) >> 1) & M6;
+    if (T == 3) p.n = (~(a | (a >> 1)) | ~(b | (b >> 1))) & M6;
+    return p;
+}
+
+template <int T>
+__device__ __forceinline__ uint32_t triple_word_acc(const PairWord& q, uint32_t c, uint32_t acc) {
+    const uint32_t p = ((q.a ^ c) | 0xC0C0C0C0u) - 0x01010101u;
+    uint32_t f;
+    if (T == 0) {
+        f = q.e0 & q.a & ~p;
+    } else {
+        f = q.e0 & ~p & (q.o1 | c);
+        if (T >= 2) {
+            const uint32_t c1 = c >> 1;
+            f &= q.o2 | c1;
+            if (T == 3) f &= q.n | ~(c | c1);
+        }
+    }
+    uint32_t r;
+    asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(f), "n"(0x01010101), "r"(acc));
+    return r;
+}
+
+// The run loop of one 4-word step for table T: B_i, B_j loaded once per run of candidates sharing
+// (i, j); B_k per candidate.
+template <int T>
+__device__ __forceinline__ void triples_step(uint32_t w, int nc, const int (&snew)[kG3], const uint32_t (&sW)[kG3],
+                                             const int64_t (&soff)[kG3][3], const uint32_t (&swm)[kG3][3],
+                                             const uint8_t* __restrict__ arena, uint32_t (&cnt)[kG3]) {
+    PairWord p[4];
+    bool have = false;
+#pragma unroll
+    for (int g = 0; g < kG3; ++g) {
+        if (g >= nc) break;
+        if (snew[g]) have = false;
+        if (w >= sW[g]) continue;
+        if (!have) {  // B_i, B_j words of this run (wrapped, reading #18)
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(arena + soff[g][0]) + ((w & swm[g][0]) >> 2));
+            const uint4 b = __ldg(reinterpret_cast<const uint4*>(arena + soff[g][1]) + ((w & swm[g][1]) >> 2));
+            p[0] = pair_word<T>(a.x, b.x);
+            p[1] = pair_word<T>(a.y, b.y);
+            p[2] = pair_word<T>(a.z, b.z);
+            p[3] = pair_word<T>(a.w, b.w);
+            have = true;
+        }
+        const uint4 c = __ldg(reinterpret_cast<const uint4*>(arena + soff[g][2]) + ((w & swm[g][2]) >> 2));
+        uint32_t acc = cnt[g];
+        acc = triple_word_acc<T>(p[0], c.x, acc);
+        acc = triple_word_acc<T>(p[1], c.y, acc);
+        acc = triple_word_acc<T>(p[2], c.z, acc);
+        cnt[g] = triple_word_acc<T>(p[3], c.w, acc);
+    }
+}
+
+__global__ void __launch_bounds__(kG3Threads) k3_triples_grouped(const int32_t* __restrict__ cand, int64_t n_cand,
+                                                                 const int64_t* __restrict__ woff,
+                                                                 const uint8_t* __restrict__ log2r,
+                                                                 const uint8_t* __restrict__ arena, int log2r0,
+                                                                 const int32_t* __restrict__ f, uint32_t threshold,
+                                                                 uint32_t use_f, Cand3* __restrict__ out,
+                                                                 unsigned long long* __restrict__ ctr, int64_t cap) {
+    __shared__ int32_t sit[kG3][3];
+    __shared__ int64_t soff[kG3][3];
+    __shared__ uint32_t swm[kG3][3], sW[kG3];
+    __shared__ int snew[kG3];
+    __shared__ uint32_t sred[kG3][kG3Threads / 32];
+    const int64_t z0 = (int64_t)blockIdx.x * kG3;
+    const int nc = (int)(n_cand - z0 < kG3 ? n_cand - z0 : kG3);
+    if (threadIdx.x < 3 * nc) {
+        const int g = threadIdx.x / 3, u = threadIdx.x % 3;
+        const int32_t it = cand[3 * z0 + threadIdx.x];
+        sit[g][u] = it;
+        soff[g][u] = woff[it];
+        swm[g][u] = (1u << log2r[it]) - 1u;  // words = 4r / 4 = r
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+        const int g = threadIdx.x;
+        sW[g] = max(max(swm[g][0], swm[g][1]), swm[g][2]) + 1u;
+        snew[g] = g == 0 || sit[g][0] != sit[g - 1][0] || sit[g][1] != sit[g - 1][1];
+    }
+    __syncthreads();
+    uint32_t Wmax = 0;
+    for (int g = 0; g < nc; ++g) Wmax = max(Wmax, sW[g]);
+    uint32_t cnt[kG3];
+#pragma unroll
+    for (int g = 0; g < kG3; ++g) cnt[g] = 0;
+    for (uint32_t w = 4 * threadIdx.x; w < Wmax; w += 4 * kG3Threads) {
+        switch ((w >> (log2r0 - 2)) & 3u) {  // the table of these 4 words (r_0 >= 16)
+            case 0: triples_step<0>(w, nc, snew, sW, soff, swm, arena, cnt); break;
+            case 1: triples_step<1>(w, nc, snew, sW, soff, swm, arena, cnt); break;
+            case 2: triples_step<2>(w, nc, snew, sW, soff, swm, arena, cnt); break;
+            default: triples_step<3>(w, nc, snew, sW, soff, swm, arena, cnt); break;
+        }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int g = 0; g < kG3; ++g) {
+        uint32_t v = cnt[g];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (lane == 0) sred[g][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+        const int g = threadIdx.x;
+        uint32_t c = 0;
+#pragma unroll
+        for (int q = 0; q < kG3Threads / 32; ++q) c += sred[g][q] >> 6;  // 64 per counted entry
+        const uint32_t slack = use_f ? (uint32_t)(f[sit[g][0]] + f[sit[g][1]] + f[sit[g][2]]) : 0u;
+        if (c + slack >= threshold) {
+            const unsigned long long at = atomicAdd(ctr, 1ull);
+            if ((int64_t)at < cap)
+                out[at] = Cand3{(uint32_t)sit[g][0], (uint32_t)sit[g][1], (uint32_t)sit[g][2], c};
+        }
+    }
+}
+
 __device__ __forceinline__ bool bsearch_i32(const int32_t* a, int64_t n, int32_t v) {
     int64_t lo = 0, hi = n;
     while (lo < hi) {
@@ -299,38 +453,45 @@ __device__ __forceinline__ bool bsearch_i32(const int32_t* a, int64_t n, int32_t
 
 // Exact corrections (reading #31): b counts once if it failed in i, j or k and all three hold b
 // (membership in A_b, the sorted items of failed transaction b).  Then re-threshold and emit
-// (i, j, k, support) with a 64-bit sort key (i n + j) n + k.
-__global__ void k3_correct(const Cand3* __restrict__ cand, int64_t n_cand, const int64_t* __restrict__ fail_off,
-                           const int32_t* __restrict__ fail_tid, const int32_t* __restrict__ fidx_of_tid,
-                           const int64_t* __restrict__ ab_off, const int32_t* __restrict__ ab_item, uint32_t threshold,
-                           int64_t n_items, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                           unsigned long long* __restrict__ ctr) {
-    const int64_t z = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (z >= n_cand) return;
+// (i, j, k, support) with a 64-bit sort key (i n + j) n + k.  One warp per candidate: the lanes
+// share the failures of its three items (dependent binary searches, latency-bound per thread).
+__global__ void __launch_bounds__(256) k3_correct(const Cand3* __restrict__ cand, int64_t n_cand,
+                                                  const int64_t* __restrict__ fail_off,
+                                                  const int32_t* __restrict__ fail_tid,
+                                                  const int32_t* __restrict__ fidx_of_tid,
+                                                  const int64_t* __restrict__ ab_off, const int32_t* __restrict__ ab_item,
+                                                  uint32_t threshold, int64_t n_items, uint64_t* __restrict__ keys,
+                                                  uint32_t* __restrict__ vals, unsigned long long* __restrict__ ctr) {
+    const int64_t z = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (z >= n_cand) return;  // warp-uniform
     const Cand3 c = cand[z];
     const uint32_t it[3] = {c.i, c.j, c.k};
     uint32_t corr = 0;
     if (fail_off) {
+        int64_t f0[3], nf[3];
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
-            const int32_t* Fu = fail_tid + fail_off[it[u]];
-            const int64_t nu = fail_off[it[u] + 1] - fail_off[it[u]];
-            for (int64_t q = 0; q < nu; ++q) {
-                const int32_t b = Fu[q];
-                bool seen = false;  // counted already through an earlier member's failure list
-                for (int v = 0; v < u; ++v)
-                    seen |= bsearch_i32(fail_tid + fail_off[it[v]], fail_off[it[v] + 1] - fail_off[it[v]], b);
-                if (seen) continue;
-                const int32_t k = fidx_of_tid[b];
-                const int32_t* Ab = ab_item + ab_off[k];
-                const int64_t na = ab_off[k + 1] - ab_off[k];
-                corr += (bsearch_i32(Ab, na, (int32_t)it[0]) && bsearch_i32(Ab, na, (int32_t)it[1]) &&
-                         bsearch_i32(Ab, na, (int32_t)it[2]));
-            }
+            f0[u] = fail_off[it[u]];
+            nf[u] = fail_off[it[u] + 1] - f0[u];
         }
+        for (int64_t q = lane; q < nf[0] + nf[1] + nf[2]; q += 32) {
+            const int u = q < nf[0] ? 0 : (q < nf[0] + nf[1] ? 1 : 2);
+            const int32_t b = fail_tid[f0[u] + q - (u > 0 ? nf[0] : 0) - (u > 1 ? nf[1] : 0)];
+            bool seen = false;  // counted already through an earlier member's failure list
+            for (int v = 0; v < u; ++v) seen |= bsearch_i32(fail_tid + f0[v], nf[v], b);
+            if (seen) continue;
+            const int32_t k = fidx_of_tid[b];
+            const int32_t* Ab = ab_item + ab_off[k];
+            const int64_t na = ab_off[k + 1] - ab_off[k];
+            corr += (bsearch_i32(Ab, na, (int32_t)it[0]) && bsearch_i32(Ab, na, (int32_t)it[1]) &&
+                     bsearch_i32(Ab, na, (int32_t)it[2]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) corr += __shfl_xor_sync(0xFFFFFFFFu, corr, o);
     }
     const uint32_t s = c.c + corr;
-    if (s >= threshold) {
+    if (lane == 0 && s >= threshold) {
         const unsigned long long at = atomicAdd(ctr, 1ull);
         keys[at] = ((uint64_t)c.i * (uint64_t)n_items + c.j) * (uint64_t)n_items + c.k;
         vals[at] = s;
@@ -489,25 +650,22 @@ struct batmap3_collection {
     double build_ms = 0, triples_ms = 0;
     int64_t word_triples = 0;
     cudaEvent_t ev[4] = {};
+    cudaStream_t stream = nullptr;  // the build's stream: the handle's buffers are allocated on it
 };
 
-static void free3(batmap3_collection* h) {
+static void free3(batmap3_collection* h, cudaStream_t st) {
     void* ps[] = {h->log2r_d, h->woff_d, h->arena_d, h->f_d, h->fail_off_d, h->fail_tid_d, h->fidx_d, h->ab_off_d,
                   h->ab_item_d};
-    for (void* p : ps)
-        if (p) cudaFree(p);
+    for (void* p : ps) dfree(p, st);  // stream-ordered, into the device pool
     for (cudaEvent_t e : h->ev)
         if (e) cudaEventDestroy(e);
 }
 
+// The handle's buffers come from the device pool on the build stream (a plain cudaMalloc of C3's
+// 46 MB arena and 184 MB working table took 0.73 ms of host time per build).
 template <typename T>
-static batmap_status alloc3(T** p, int64_t count) {
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), (size_t)std::max<int64_t>(count, 1) * sizeof(T));
-    if (e != cudaSuccess) {
-        set_error("cudaMalloc(%lld bytes): %s", (long long)(count * sizeof(T)), cudaGetErrorString(e));
-        return e == cudaErrorMemoryAllocation ? BATMAP_E_NOMEM : BATMAP_E_CUDA;
-    }
-    return BATMAP_OK;
+static batmap_status alloc3(batmap3_collection* h, T** p, int64_t count) {
+    return dalloc_t(p, count, h->stream);
 }
 
 static uint64_t splitmix64_h(uint64_t x) {
@@ -518,6 +676,12 @@ static uint64_t splitmix64_h(uint64_t x) {
 }
 
 static int ceil_log2(uint64_t v) { return v <= 1 ? 0 : 64 - __builtin_clzll(v - 1); }
+
+// BATMAP_K3_GROUPED=0: the one-warp-per-candidate triple kernel (test hook)
+static bool env_flag_off(const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] == '0';
+}
 
 static batmap_status build3(batmap3_collection* h, const int64_t* offsets, const int32_t* tids,
                             const batmap_build_opts* o, cudaStream_t st) {
@@ -552,7 +716,8 @@ static batmap_status build3(batmap3_collection* h, const int64_t* offsets, const
     const int lmin = std::max(s3, ceil_log2(r_min));
     std::vector<int64_t> woff(n + 1, 0);
     int lr0 = 62;
-    std::vector<Chunk3> chunks;
+    const bool serial = o && (o->flags & BATMAP_BUILD_SERIAL);
+    std::vector<Chunk3> chunks;  // items in chunks of elements (k3_insert, k3_cleanup, k3_encode)
     for (int64_t i = 0; i < n; ++i) {
         const int64_t sz = off_h[i + 1] - off_h[i];
         if (sz < 0 || sz > m) {
@@ -570,10 +735,10 @@ static batmap_status build3(batmap3_collection* h, const int64_t* offsets, const
     h->r0 = n ? (1ll << lr0) : (1ll << lmin);
     h->log2r0 = ceil_log2((uint64_t)h->r0);
     h->arena_bytes = woff[n];
-    BM_TRY(alloc3(&h->log2r_d, n));
-    BM_TRY(alloc3(&h->woff_d, n + 1));
-    BM_TRY(alloc3(&h->arena_d, h->arena_bytes));
-    BM_TRY(alloc3(&h->f_d, n));
+    BM_TRY(alloc3(h, &h->log2r_d, n));
+    BM_TRY(alloc3(h, &h->woff_d, n + 1));
+    BM_TRY(alloc3(h, &h->arena_d, h->arena_bytes));
+    BM_TRY(alloc3(h, &h->f_d, n));
     BM_CUDA(cudaMemcpyAsync(h->log2r_d, h->lr_h.data(), (size_t)n, cudaMemcpyHostToDevice, st));
     BM_CUDA(cudaMemcpyAsync(h->woff_d, woff.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     uint32_t* work = nullptr;
@@ -604,7 +769,6 @@ static batmap_status build3(batmap3_collection* h, const int64_t* offsets, const
             return BATMAP_E_INVALID;
         }
     }
-    const bool serial = o && (o->flags & BATMAP_BUILD_SERIAL);
     int64_t fail_cap = std::max<int64_t>(1 << 16, h->nnz / 8), F = 0;
     for (int attempt = 0; attempt < 4; ++attempt) {
         BM_TRY(dalloc_t(&fails, fail_cap, st));
@@ -636,8 +800,9 @@ static batmap_status build3(batmap3_collection* h, const int64_t* offsets, const
     // the byte arena: ⊥ everywhere, then every stored element's three entries
     k3_fill_u32<<<gridn(h->arena_bytes / 4, 256), 256, 0, st>>>(reinterpret_cast<uint32_t*>(h->arena_d),
                                                                h->arena_bytes / 4, kNull3Word);
-    k3_encode<<<std::max<unsigned>(1, (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 64)), 256, 0, st>>>(
-        offsets, tids, nullptr, n, h->woff_d, h->log2r_d, P, (uint32_t)h->r0, h->log2r0, work, h->arena_d);
+    if (!chunks.empty())
+        k3_encode<<<(unsigned)chunks.size(), 256, 0, st>>>(chunks_d, offsets, tids, h->woff_d, h->log2r_d, P,
+                                                           (uint32_t)h->r0, h->log2r0, work, h->arena_d);
     BM_CUDA(cudaGetLastError());
     // F: sort, deduplicate (a concurrent build may record an element once per failed copy), then
     // per-item failure lists Fail(i), f_i, the failed tids and their item lists A_b
@@ -669,15 +834,15 @@ static batmap_status build3(batmap3_collection* h, const int64_t* offsets, const
         const uint64_t* uf = sorted + F;  // unique (item << 32 | tid), sorted
         F = Fu;
         h->n_fail = F;
-        BM_TRY(alloc3(&h->fail_off_d, n + 1));
-        BM_TRY(alloc3(&h->fail_tid_d, F));
+        BM_TRY(alloc3(h, &h->fail_off_d, n + 1));
+        BM_TRY(alloc3(h, &h->fail_tid_d, F));
         k3_fail_split<<<gridn(F + 1, 256), 256, 0, st>>>(uf, F, n, h->fail_off_d, h->fail_tid_d);
         k3_fail_counts<<<gridn(n, 256), 256, 0, st>>>(h->fail_off_d, n, h->f_d);
         // failed tids: mark, exclusive scan -> index of each failed tid; total = n_ftid
         BM_TRY(dalloc_t(&mark, m + 1, st));
         BM_CUDA(cudaMemsetAsync(mark, 0, (m + 1) * sizeof(int32_t), st));
         k3_mark_failed<<<gridn(F, 256), 256, 0, st>>>(uf, F, mark);
-        BM_TRY(alloc3(&h->fidx_d, m + 1));
+        BM_TRY(alloc3(h, &h->fidx_d, m + 1));
         cub::DeviceScan::ExclusiveSum(tmp, b3, mark, h->fidx_d, m + 1, st);
         int32_t nft = 0;
         BM_TRY(read_scalar(st, h->fidx_d + m, &nft));
@@ -704,8 +869,8 @@ static batmap_status build3(batmap3_collection* h, const int64_t* offsets, const
         scratch.own(&tmp2);
         BM_TRY(dalloc(&tmp2, b4, st));
         cub::DeviceRadixSort::SortKeys(tmp2, b4, abk, abk + total, total, 0, 64, st);
-        BM_TRY(alloc3(&h->ab_off_d, h->n_ftid + 1));
-        BM_TRY(alloc3(&h->ab_item_d, total));
+        BM_TRY(alloc3(h, &h->ab_off_d, h->n_ftid + 1));
+        BM_TRY(alloc3(h, &h->ab_item_d, total));
         k3_ab_split<<<gridn(total + 1, 256), 256, 0, st>>>(abk + total, total, n, h->n_ftid, h->ab_item_d, h->ab_off_d);
     }
     BM_CUDA(cudaGetLastError());
@@ -729,6 +894,7 @@ batmap_status batmap3_build(const int64_t* offsets, const int32_t* tids, int64_t
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     auto* h = new batmap3_collection();
+    h->stream = st;
     h->n = n_items;
     h->m = n_transactions;
     for (cudaEvent_t& e : h->ev) cudaEventCreate(&e);
@@ -736,7 +902,7 @@ batmap_status batmap3_build(const int64_t* offsets, const int32_t* tids, int64_t
     const batmap_status rc = build3(h, offsets, tids, opts, st);
     if (rc != BATMAP_OK) {
         cudaStreamSynchronize(st);
-        free3(h);
+        free3(h, st);
         delete h;
         return rc;
     }
@@ -773,8 +939,16 @@ batmap_status batmap3_triple_supports(batmap3_handle h, const int32_t* triples, 
     BM_TRY(dalloc_t(&cand, n_triples, st));
     BM_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), st));
     cudaEventRecord(h->ev[2], st);
+    // grouped when the narrowest BatMap has >= 1024 words (C3: r_0 = 2048; measured 2.26 -> 2.09 ms);
+    // C1's 256-word BatMaps leave a CTA of 8 candidates one half-occupied step (2.6 -> 4.2 ms)
+    const bool grouped = h->log2r0 >= 10 && !env_flag_off("BATMAP_K3_GROUPED");
+    if (grouped)
+        k3_triples_grouped<<<(unsigned)((n_triples + kG3 - 1) / kG3), kG3Threads, 0, st>>>(
+            triples, n_triples, h->woff_d, h->log2r_d, h->arena_d, h->log2r0, h->f_d, threshold, 1u, cand, ctr,
+            n_triples);
     const unsigned grid = (unsigned)std::min<int64_t>((n_triples + 7) / 8, 148 * 64);
-    k3_triples<<<grid, 256, 0, st>>>(triples, n_triples, h->woff_d, h->log2r_d, h->arena_d, h->log2r0, h->f_d,
+    if (!grouped)
+        k3_triples<<<grid, 256, 0, st>>>(triples, n_triples, h->woff_d, h->log2r_d, h->arena_d, h->log2r0, h->f_d,
                                       threshold, 1u, cand, ctr, n_triples);
     BM_CUDA(cudaGetLastError());
     unsigned long long nc = 0;
@@ -784,7 +958,7 @@ batmap_status batmap3_triple_supports(batmap3_handle h, const int32_t* triples, 
     BM_TRY(dalloc_t(&vals, 2 * std::max<int64_t>(NC, 1), st));
     BM_CUDA(cudaMemsetAsync(ctr + 1, 0, sizeof(unsigned long long), st));
     if (NC)
-        k3_correct<<<gridn(NC, 256), 256, 0, st>>>(cand, NC, h->n_fail ? h->fail_off_d : nullptr, h->fail_tid_d,
+        k3_correct<<<gridn(NC * 32, 256), 256, 0, st>>>(cand, NC, h->n_fail ? h->fail_off_d : nullptr, h->fail_tid_d,
                                                     h->fidx_d, h->ab_off_d, h->ab_item_d, threshold, h->n, keys, vals,
                                                     ctr + 1);
     unsigned long long K = 0;
@@ -905,7 +1079,8 @@ batmap_status batmap3_export_failures(batmap3_handle h, int32_t* items, int32_t*
 void batmap3_destroy(batmap3_handle h) {
     if (!h) return;
     cudaDeviceSynchronize();
-    free3(h);
+    free3(h, 0);  // after the device synchronisation: the caller's stream may be gone
+    cudaStreamSynchronize(0);
     delete h;
 }
 

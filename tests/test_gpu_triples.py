@@ -148,6 +148,7 @@ def test_big_tables_and_wide_width_mix():
     tids = np.concatenate(rows)
     for max_loop in (0, 1):
         c = _c3(off, tids, m, seed=2, max_loop=max_loop)
+        _check_layout(c, off, tids, m, 2)
         tri = _all_triples(len(rows))
         got = c.triple_supports(tri, threshold=0).cpu().numpy().astype(np.uint32)
         np.testing.assert_array_equal(got[:, 3], oracle.triples_list(off, tids, tri[:, 0], tri[:, 1], tri[:, 2]))
@@ -208,3 +209,22 @@ def test_mine_triples_planted():
     ref = oracle.triples_horizontal(off, tids, m, threshold=20)
     assert ref.shape[0] >= 25
     np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("grouped", ["", "0"])  # "" = the pair-grouped kernel (r_0 >= 1024); "0" = warp per candidate
+def test_triple_kernels_any_candidate_order(grouped, monkeypatch):
+    """k3_triples_grouped reuses B_i and B_j across a run of candidates sharing (i, j); it must be
+    exact for any candidate order (runs split anywhere), with and without failures, and agree with
+    the one-warp-per-candidate kernel."""
+    if grouped:
+        monkeypatch.setenv("BATMAP_K3_GROUPED", grouped)
+    off, tids, m = _instance(21, n=14)
+    rng = np.random.default_rng(5)
+    tri = _all_triples(len(off) - 1)
+    for max_loop in (0, 1):
+        c = _c3(off, tids, m, seed=6, max_loop=max_loop, r_min=1024)  # r_0 >= 1024: the grouped kernel's range
+        ref = oracle.triples_list(off, tids, tri[:, 0], tri[:, 1], tri[:, 2])
+        for order in (np.arange(len(tri)), rng.permutation(len(tri))):
+            got = c.triple_supports(np.ascontiguousarray(tri[order]), threshold=0).cpu().numpy().astype(np.uint32)
+            np.testing.assert_array_equal(got[:, :3], tri.astype(np.uint32))
+            np.testing.assert_array_equal(got[:, 3], ref)
