@@ -2,8 +2,11 @@
 // symmetry cut p <= q, virtualised skinny rectangles, split-K for long tiles, and
 // the deal of work to the parts of a multi-GPU run, and promotion of small narrow classes.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <functional>
+#include <mutex>
+#include <new>
 #include <unordered_map>
 
 #include "plan.h"
@@ -12,11 +15,61 @@ namespace bm {
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+namespace {
+struct PoolBlock {
+    void* p;
+    size_t bytes;
+    bool busy;
+};
+std::mutex g_pool_mu;
+std::vector<PoolBlock> g_pool;
+constexpr size_t kPoolMinBytes = size_t(1) << 20;
+constexpr size_t kPoolMaxBlocks = 8;
+}  // namespace
+
+void* plan_pool_alloc(size_t bytes) {
+    if (bytes < kPoolMinBytes) return ::operator new(bytes);
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    PoolBlock* best = nullptr;  // the smallest idle block that fits without hogging a much larger one
+    for (PoolBlock& b : g_pool)
+        if (!b.busy && b.bytes >= bytes && b.bytes <= 4 * bytes && (!best || b.bytes < best->bytes)) best = &b;
+    if (best) {
+        best->busy = true;
+        return best->p;
+    }
+    const size_t want = (bytes + kPoolMinBytes - 1) / kPoolMinBytes * kPoolMinBytes;
+    void* p = ::operator new(want);
+    if (g_pool.size() >= kPoolMaxBlocks) {  // replace the smallest idle block, else do not pool this one
+        PoolBlock* victim = nullptr;
+        for (PoolBlock& b : g_pool)
+            if (!b.busy && (!victim || b.bytes < victim->bytes)) victim = &b;
+        if (!victim) return p;  // freed by plan_pool_free's fallback
+        ::operator delete(victim->p);
+        *victim = PoolBlock{p, want, true};
+        return p;
+    }
+    g_pool.push_back(PoolBlock{p, want, true});
+    return p;
+}
+
+void plan_pool_free(void* p) {
+    if (!p) return;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (PoolBlock& b : g_pool)
+            if (b.p == p) {
+                b.busy = false;
+                return;
+            }
+    }
+    ::operator delete(p);
+}
+
 // Stable sort by descending cost.  Work lists have few distinct costs (one per rectangle, per
 // accumulated tile row or per k-piece length), so this buckets in O(T) instead of comparing
 // (C4: 3e5 tiles; the plan is built on the host while the build kernels run).
-template <typename T, typename Cost>
-static void stable_sort_desc(std::vector<T>& v, Cost cost) {
+template <typename V, typename Cost>
+static void stable_sort_desc(V& v, Cost cost) {
     std::unordered_map<int64_t, int32_t> first_seen;  // cost -> id in order of first appearance
     std::vector<int64_t> keys;
     std::vector<int32_t> bucket(v.size());
@@ -42,7 +95,7 @@ static void stable_sort_desc(std::vector<T>& v, Cost cost) {
     std::vector<int64_t> at(keys.size() + 1, 0);
     for (size_t e = 0; e < v.size(); ++e) ++at[rank[bucket[e]] + 1];
     for (size_t k = 1; k < at.size(); ++k) at[k] += at[k - 1];
-    std::vector<T> out(v.size());
+    V out(v.size());
     for (size_t e = 0; e < v.size(); ++e) out[at[rank[bucket[e]]]++] = v[e];
     v.swap(out);
 }
@@ -337,15 +390,17 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
     stable_sort_desc(segs, [](const Seg& x) { return x.cost; });
     // Work items are emitted in deal order.  The tiles of ordinary rectangles come out already in
     // descending cost order (segments are sorted by their tile cost) and go straight into the
-    // reserved list; the k-pieces of accumulated tile rows (few) go to a side list with their deal
-    // position and are merged in from the back -- the stable descending sort of the deal order
-    // without sorting or re-allocating the 3e5 items of C4.
+    // reserved list; the k-pieces of accumulated tile rows (few) are generated first, into a side
+    // list with their deal position, stably sorted by cost and merged in as the main items are
+    // emitted -- the stable descending sort of the deal order without sorting or moving the 3e5
+    // items of C4 (a merge from the back afterwards moved every item: 1.5 ms of C4's plan).
     struct Side {
         Work w;
         int64_t cost, pos;  // pos: main items dealt before it
     };
     std::vector<Side> side;
-    std::vector<Work>& items = P.work;
+    side.reserve(4096);
+    WorkList& items = P.work;
     {  // capacity: this part's share of the tiles, split tiles counted per piece
         int64_t cnt = 0;
         for (const Rect& r : P.rects) {
@@ -357,6 +412,16 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         }
         items.reserve((size_t)(cnt / n_parts + 8 * 1024));
     }
+    // main items go through put(): side items that sort before it (higher cost, or equal cost and
+    // dealt no later) are placed first
+    size_t si = 0;
+    int64_t main_count = 0, main_before = 0;  // main_before: the side pre-pass's deal position
+    auto put = [&](const Work& w, int64_t c) {
+        while (si < side.size() && (side[si].cost > c || (side[si].cost == c && side[si].pos <= main_count)))
+            items.push_back(side[si++].w);
+        items.push_back(w);
+        ++main_count;
+    };
     // one unit of this part, in deal order: its algorithmic compares and its work items
     auto emit = [&](const Unit& u) {
         const Rect& r = P.rects[u.rect];
@@ -400,18 +465,31 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                 w.k0 = (int32_t)((int64_t)nk * p / pieces);
                 w.k1 = (int32_t)((int64_t)nk * (p + 1) / pieces);
                 const int64_t c = (int64_t)(w.k1 - w.k0) * kChunk * kTile * TN;
-                if (r.acc) side.push_back({w, c, (int64_t)items.size()});
-                else items.push_back(w);
+                if (r.acc) side.push_back({w, c, main_before});
+                else put(w, c);
                 P.tile_compares += c;
             }
         }
     };
+    {  // pre-pass: the accumulated tile rows of this part (their k-pieces form the side list)
+        int64_t at = 0;
+        for (const Seg& g : segs) {
+            const int64_t t0 = (((int64_t)part - at) % n_parts + n_parts) % n_parts;
+            if (g.ti >= 0) {
+                if (t0 == 0) emit(Unit{g.rect, g.ti, -1, g.cost});
+            } else if (t0 < g.count) {
+                main_before += (g.count - t0 + n_parts - 1) / n_parts;
+            }
+            at += g.count;
+        }
+        std::stable_sort(side.begin(), side.end(), [](const Side& x, const Side& y) { return x.cost > y.cost; });
+    }
     {
         int64_t at = 0;  // global index of the segment's first unit
         for (const Seg& g : segs) {
             const int64_t t0 = (((int64_t)part - at) % n_parts + n_parts) % n_parts;
             if (g.ti >= 0) {
-                if (t0 == 0) emit(Unit{g.rect, g.ti, -1, g.cost});
+                // emitted by the pre-pass
             } else if (t0 < g.count) {
                 const Rect& r = P.rects[g.rect];
                 const int ta = (int)ceil_div(r.n_rows, kTile), tb = (int)ceil_div(r.n_cols, TN);
@@ -431,12 +509,32 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                         P.word_compares += (int64_t)r.n_rows * (plain_w ? (int64_t)r.n_cols * r.W : sumW(r.cls_b, 0, r.n_cols));
                     }
                     const int nk = r.W / kChunk;
-                    P.tile_compares += g.count * (int64_t)nk * kChunk * kTile * TN;
+                    const int64_t c = (int64_t)nk * kChunk * kTile * TN;
+                    P.tile_compares += g.count * c;
+                    while (si < side.size() && side[si].cost > c) items.push_back(side[si++].w);
+                    // side items of equal cost land inside the segment, before the main item
+                    // whose index reaches their deal position; the rest is one contiguous run
+                    size_t ties = 0;
+                    while (si + ties < side.size() && side[si + ties].cost == c &&
+                           side[si + ties].pos < main_count + g.count)
+                        ++ties;
+                    const size_t base = items.size();
+                    items.resize(base + (size_t)g.count + ties);
+                    Work* o = items.data() + base;
+                    const size_t tie_end = si + ties;
+                    int64_t next_tie = si < tie_end ? side[si].pos : INT64_MAX;
                     for (int i0 = 0; i0 < ta; i0 += G) {
                         const int i1 = std::min(ta, i0 + G);
                         for (int j = r.diag ? i0 * QD : 0; j < tb; ++j) {
                             const int ie = r.diag ? std::min(i1, j / QD + 1) : i1;
-                            for (int i = i0; i < ie; ++i) items.push_back(Work{g.rect, i, j, 0, nk, 0});
+                            for (int i = i0; i < ie; ++i) {
+                                while (main_count >= next_tie) {
+                                    *o++ = side[si++].w;
+                                    next_tie = si < tie_end ? side[si].pos : INT64_MAX;
+                                }
+                                *o++ = Work{g.rect, i, j, 0, nk, 0};
+                                ++main_count;
+                            }
                         }
                     }
                     at += g.count;
@@ -464,22 +562,8 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             at += g.count;
         }
     }
+    while (si < side.size()) items.push_back(side[si++].w);  // the side items after the last main one
     auto work_cost = [&](const Work& w) { return (int64_t)(w.k1 - w.k0) * kChunk * kTile * TN; };
-    if (!side.empty()) {  // stable by (cost desc, deal position); main items are sorted by cost
-        std::stable_sort(side.begin(), side.end(), [](const Side& x, const Side& y) { return x.cost > y.cost; });
-        const size_t nm = items.size(), ns = side.size();
-        items.resize(nm + ns);
-        int64_t a = (int64_t)nm - 1, b = (int64_t)ns - 1, o = (int64_t)(nm + ns) - 1;
-        while (b >= 0) {  // from the back: the later of the two tails goes last
-            bool take_main = false;
-            if (a >= 0) {
-                const int64_t ca = work_cost(items[a]);
-                take_main = ca < side[b].cost || (ca == side[b].cost && side[b].pos <= a);
-            }
-            if (take_main) items[o--] = items[a--];
-            else items[o--] = side[b--].w;
-        }
-    }
     // ---- the tail of the schedule: the last grid_cap items (the shortest, claimed last) are cut
     // into pieces along k so that the CTAs finish within a piece of each other.  Whole tiles of
     // ordinary rectangles (C2: makespan/mean 1.046 -> 1.005 in the planner's cost model) add their
@@ -487,7 +571,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
     // tests; k-pieces of accumulated rectangles are cut finer and add into their counters as before
     // (C3: 2,391 items of 22-24 chunks on 592 CTAs left 23 CTAs a fifth item, makespan/mean 1.22).
     if (allow_split && grid_cap > 0 && !P.work.empty()) {
-        std::vector<Work>& work = P.work;
+        WorkList& work = P.work;
         const size_t n = work.size();
         const size_t begin = n > (size_t)grid_cap ? n - (size_t)grid_cap : 0;
         std::vector<Work> pieces;
@@ -523,7 +607,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
         }
         if (!P.tails.empty()) P.tail_pieces = pcs;
         if (!pieces.empty()) {  // everything before `begin` costs at least as much: re-sort the tail only
-            std::vector<Work> tail(work.begin() + (long)begin, work.end());
+            WorkList tail(work.begin() + (long)begin, work.end());
             tail.insert(tail.end(), pieces.begin(), pieces.end());
             stable_sort_desc(tail, work_cost);
             work.resize(begin);
