@@ -549,13 +549,11 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
                         t += band_n;
                         continue;
                     }
-                    for (int j = r.diag ? i0 * QD : 0; j < tb; ++j) {
+                    for (int j = r.diag ? i0 * QD : 0; j < tb && next < g.count; ++j) {
                         const int ie = r.diag ? std::min(i1, j / QD + 1) : i1;  // rows with i * QD <= j
-                        for (int i = i0; i < ie; ++i, ++t)
-                            if (t == next) {
-                                emit(Unit{g.rect, i, j, g.cost});
-                                next += n_parts;
-                            }
+                        const int64_t cnt = ie - i0;  // the column's tiles: units [t, t + cnt)
+                        for (; next < t + cnt; next += n_parts) emit(Unit{g.rect, i0 + (int)(next - t), j, g.cost});
+                        t += cnt;
                     }
                 }
             }

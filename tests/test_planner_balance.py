@@ -52,3 +52,31 @@ def test_parts_balanced_within_one_percent(classes, name, N):
     wcs, tcs = np.array(wcs, float), np.array(tcs, float)
     assert wcs.max() / wcs.mean() <= 1.01, wcs
     assert tcs.max() / tcs.mean() <= 1.01, tcs
+
+
+def test_plan_repeatable_across_threads(classes):
+    """The work lists live in a pooled allocator shared by every host thread (plan.cu): plans made
+    concurrently from several threads, and again afterwards, are identical."""
+    import threading
+
+    from paper_1102_1003_b200 import plan_work
+
+    cn, cw = classes["C4"]
+    ref = {N: plan_work(cn, cw, N - 1, N) for N in (1, 3, 8)}
+    out, errs = {}, []
+
+    def run(t):
+        try:
+            for N in (1, 3, 8):
+                out[(t, N)] = plan_work(cn, cw, N - 1, N)
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(t,)) for t in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs
+    for (t, N), (items, wc, tc) in out.items():
+        assert np.array_equal(items, ref[N][0]) and wc == ref[N][1] and tc == ref[N][2]

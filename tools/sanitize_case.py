@@ -2,7 +2,8 @@
 every build tier (CTA, cluster of 1/2/4 CTAs over DSMEM, the chunked global tier), serial and
 concurrent builds with forced failures, item subsets, a sharded build exchanged in-process, the
 cut tail tiles of K2, both K2 tile widths with class promotion, the frequent-item selection, the
-GPU merge path, FIMI parsing + filtering + CSR selection, and (not under initcheck, whose reads of
+GPU merge path, FIMI parsing + filtering + CSR selection, the byte-table K1 tier and the NEXT-4
+triples path (candidates, 3-of-4 builds, triple supports), and (not under initcheck, whose reads of
 cuBLASLt's output are false positives) the dense path."""
 import os
 import sys
@@ -97,4 +98,20 @@ kd = frequent_items(torch.as_tensor(zo).cuda(), 3)
 so, st_ = select_csr(torch.as_tensor(zo).cuda(), torch.as_tensor(zt).cuda(), kd)
 eo, et = filter_csr(zo, zt, kd.cpu().numpy())
 assert np.array_equal(so.cpu().numpy(), eo) and np.array_equal(st_.cpu().numpy(), et)
-print("sanitize case ok", len(ref))
+# round 2: the byte-table K1 tier on every class (BATMAP_K1_BYTE=all), serial and concurrent
+os.environ["BATMAP_K1_BYTE"] = "all"
+for serial in (False, True):
+    c = Collection(o, t, m, seed=7, max_loop=2, serial=serial)
+    assert np.array_equal(c.pair_supports(threshold=2).cpu().numpy().astype(np.uint32), ref)
+    c.close()
+os.environ.pop("BATMAP_K1_BYTE")
+# NEXT-4: Apriori candidates, 3-of-4 BatMaps (concurrent with forced failures, and serial), triple supports
+from paper_1102_1003_b200 import Collection3, candidate_triples  # noqa: E402
+
+tri_ref = oracle.triples_horizontal(off, tids, m, threshold=1)
+cand = candidate_triples(torch.as_tensor(ref[ref[:, 2] >= 1].astype(np.int32)).cuda(), n)
+for serial, ml in ((False, 2), (True, 0)):
+    with Collection3(o, t, m, seed=8, max_loop=ml, serial=serial) as c3:
+        q = c3.triple_supports(cand, threshold=1).cpu().numpy().astype(np.uint32)
+    assert np.array_equal(q, tri_ref), (q.shape, tri_ref.shape)
+print("sanitize case ok", len(ref), len(tri_ref))
