@@ -402,6 +402,7 @@ def main():
             allp = gather_triples(res if backend == "nccl" else res.cpu())
             res = batmap.sort_triples(allp.to(dev)) if allp is not None else None
         st = coll.stats()
+        st["arena_bytes"] = coll.info()["arena_bytes"]  # host-side field read (compulsory K2 bytes)
         coll.close()
         return res, st
 
@@ -451,6 +452,9 @@ def main():
     achieved = wc_all / world / (k2_max / 1e3)  # per GPU, bounded by the slowest rank
     roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_cmp / 1e12, "unit": "Tcmp/s",
                 "frac": achieved / peak_cmp, "traffic": _k2_traffic(w.name) if world == 1 else None,
+                "traffic_src": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch of this "
+                               "workload (profiles/k2_traffic.json; not measurable inside the timed run)",
+                "compulsory_bytes": int(stats[-1]["arena_bytes"]),
                 "kernel": "k2_tiled (BatMap pair intersection)",
                 "peak_def": f"R_int = 32 word-compares/clk/SM x {sms} SMs x {clk_max / 1e6:.0f} MHz "
                             f"(sm_max_mhz {src}); 4 integer instructions per 32-bit word compare",

@@ -3,6 +3,7 @@
 mkdir -p gpurun_out
 TAG=${TAG:-r2u}
 timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_$TAG.txt 2>&1; tail -2 gpurun_out/pytest_gpu_$TAG.txt
+timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -c 300 gpurun_out/bench_$TAG.json
 timeout 600 python tools/build_bench.py --reps 7 C2 C3 C4 C5_p0.01 C5_p0.1 > gpurun_out/build_$TAG.jsonl 2> gpurun_out/build_$TAG.err; cut -c1-200 gpurun_out/build_$TAG.jsonl
 BATMAP_TRACE=1 timeout 300 python tools/run_one.py C4 3 > gpurun_out/trace_c4_$TAG.txt 2>&1; tail -9 gpurun_out/trace_c4_$TAG.txt
 timeout 1200 python tools/part_balance.py C4 C5_p0.1 C2 > gpurun_out/part_balance_$TAG.jsonl 2> gpurun_out/part_balance_$TAG.err; cut -c1-300 gpurun_out/part_balance_$TAG.jsonl
