@@ -13,10 +13,20 @@ def fmt_ms(x):
 
 
 def main(path):
+    import os
+
     rows = [json.loads(l) for l in open(path) if l.strip().startswith("{")]
+    mp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "c5", "manifest.json")
+    man = json.load(open(mp)) if os.path.exists(mp) else {}
     print("| Config | step ms (build + pairs) | pair-intersections/s | frequent pairs | K2 ms | K2 % R_int "
-          "| K1 insertions/s | parity | CPU horizontal oracle s (16 thr) | dense XᵀX ms | GPU merge ms |")
+          "| K1 insertions/s | parity | CPU horizontal oracle s | dense XᵀX ms | GPU merge ms |")
     print("|---|---|---|---|---|---|---|---|---|---|---|")
+    def cpu_s(r):
+        if "golden" in r.get("parity", "") and r["config"] in man:
+            e = man[r["config"]]
+            return f"{e['horizontal_s']} ({e['threads']} thr, golden)"
+        return r.get("oracle_s", "—")
+
     for r in rows:
         d = r.get("dense_xtx")
         m = r.get("merge")
@@ -33,7 +43,7 @@ def main(path):
         print(f"| {r['config']} n={r['n']:,} m={r['m']:,} s={r['threshold']} "
               f"| {fmt_ms(r['step_ms'])} ({fmt_ms(r['build_ms'])} + {fmt_ms(r['pairs_ms'])}) "
               f"| {r['pairs_per_s']:.2e} | {r['K']:,} | {fmt_ms(r['k2_ms'])} | {100 * (r['k2_frac_R_int'] or 0):.0f} % "
-              f"| {ins:.1e} | {par} | {r.get('oracle_s', '—')} "
+              f"| {ins:.1e} | {par} | {cpu_s(r)} "
               f"| {fmt_ms(d['total_ms']) if d else 'n/a'} | {fmt_ms(m['kernel_ms']) if m else '—'} |")
     pf = [r for r in rows if r.get("prefiltered")]
     for r in pf:
