@@ -45,6 +45,8 @@ def test_bench_line_contract():
     r = d["roofline"]
     assert r["bound"] == "alu" and r["unit"] == "Tcmp/s" and 0.3 < r["frac"] < 1.0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    # traffic: the committed ncu figure of this workload's K2 launch, against the arena it must read
+    assert r["compulsory_bytes"] == 2_487_803_904 and r["traffic"] >= r["compulsory_bytes"] and r["traffic_src"]
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"] and c["cpu_model"]
     for alg in ("horizontal", "merge"):  # both oracles, 1 thread and all threads
