@@ -346,34 +346,47 @@ __device__ __forceinline__ uint32_t triple_word_acc(const PairWord& q, uint32_t 
     return r;
 }
 
-// The run loop of one 4-word step for table T: B_i, B_j loaded once per run of candidates sharing
-// (i, j); B_k per candidate.
+// One 4-word step for table T.  The B_k words of all kG3 candidates (and the B_i, B_j words of the
+// first run) are loaded first, as predicated loads with no branch between them, so a thread keeps
+// up to kG3 + 2 L2 requests in flight (one at a time when each load sat behind its candidate's
+// branch: ncu showed the kernel latency-bound, long_scoreboard the top stall, ALU pipe 59 %).  Then
+// the runs are computed in order; a run after the first loads its B_i, B_j words when it starts.
 template <int T>
 __device__ __forceinline__ void triples_step(uint32_t w, int nc, const int (&snew)[kG3], const uint32_t (&sW)[kG3],
                                              const int64_t (&soff)[kG3][3], const uint32_t (&swm)[kG3][3],
                                              const uint8_t* __restrict__ arena, uint32_t (&cnt)[kG3]) {
+    uint4 cv[kG3];
+#pragma unroll
+    for (int g = 0; g < kG3; ++g) {
+        const bool act = g < nc && w < sW[g];
+        const uint4* pc = reinterpret_cast<const uint4*>(arena + soff[g][2]) + ((w & swm[g][2]) >> 2);
+        cv[g] = act ? __ldg(pc) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    // B_i, B_j words of the first run (wrapped, reading #18); every word index is valid after the wrap
+    uint4 a = __ldg(reinterpret_cast<const uint4*>(arena + soff[0][0]) + ((w & swm[0][0]) >> 2));
+    uint4 b = __ldg(reinterpret_cast<const uint4*>(arena + soff[0][1]) + ((w & swm[0][1]) >> 2));
     PairWord p[4];
-    bool have = false;
+    p[0] = pair_word<T>(a.x, b.x);
+    p[1] = pair_word<T>(a.y, b.y);
+    p[2] = pair_word<T>(a.z, b.z);
+    p[3] = pair_word<T>(a.w, b.w);
 #pragma unroll
     for (int g = 0; g < kG3; ++g) {
         if (g >= nc) break;
-        if (snew[g]) have = false;
-        if (w >= sW[g]) continue;
-        if (!have) {  // B_i, B_j words of this run (wrapped, reading #18)
-            const uint4 a = __ldg(reinterpret_cast<const uint4*>(arena + soff[g][0]) + ((w & swm[g][0]) >> 2));
-            const uint4 b = __ldg(reinterpret_cast<const uint4*>(arena + soff[g][1]) + ((w & swm[g][1]) >> 2));
+        if (g > 0 && snew[g]) {  // a later run: its own B_i, B_j words
+            a = __ldg(reinterpret_cast<const uint4*>(arena + soff[g][0]) + ((w & swm[g][0]) >> 2));
+            b = __ldg(reinterpret_cast<const uint4*>(arena + soff[g][1]) + ((w & swm[g][1]) >> 2));
             p[0] = pair_word<T>(a.x, b.x);
             p[1] = pair_word<T>(a.y, b.y);
             p[2] = pair_word<T>(a.z, b.z);
             p[3] = pair_word<T>(a.w, b.w);
-            have = true;
         }
-        const uint4 c = __ldg(reinterpret_cast<const uint4*>(arena + soff[g][2]) + ((w & swm[g][2]) >> 2));
+        if (w >= sW[g]) continue;
         uint32_t acc = cnt[g];
-        acc = triple_word_acc<T>(p[0], c.x, acc);
-        acc = triple_word_acc<T>(p[1], c.y, acc);
-        acc = triple_word_acc<T>(p[2], c.z, acc);
-        cnt[g] = triple_word_acc<T>(p[3], c.w, acc);
+        acc = triple_word_acc<T>(p[0], cv[g].x, acc);
+        acc = triple_word_acc<T>(p[1], cv[g].y, acc);
+        acc = triple_word_acc<T>(p[2], cv[g].z, acc);
+        cnt[g] = triple_word_acc<T>(p[3], cv[g].w, acc);
     }
 }
 
