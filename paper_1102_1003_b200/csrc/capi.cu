@@ -76,13 +76,21 @@ static batmap_status build_impl(const int64_t* offsets, const int32_t* tids, int
         return BATMAP_E_INVALID;
     }
     *out = nullptr;
-    if (!offsets || (!tids && n_items > 0)) {
-        set_error("offsets/tids is NULL");
+    if (!offsets) {
+        set_error("offsets is NULL");
         return BATMAP_E_INVALID;
     }
     if (n_items < 0 || n_transactions < 1) {
         set_error("need n_items >= 0 and n_transactions >= 1");
         return BATMAP_E_INVALID;
+    }
+    if (offsets_host) {
+        if (!tids && n_items > 0 && offsets_host[n_items] != 0) {
+            set_error("tids is NULL but offsets[n_items] = %lld", (long long)offsets_host[n_items]);
+            return BATMAP_E_INVALID;
+        }
+    } else {
+        BM_TRY(check_tids_device(offsets, tids, n_items, reinterpret_cast<cudaStream_t>(stream)));
     }
     if (n_items >= (1ll << 31) || n_transactions >= (1ll << 31)) {
         set_error("n_items and n_transactions must be < 2^31");
@@ -346,7 +354,7 @@ batmap_status batmap_dense_pair_supports(const int64_t* offsets, const int32_t* 
                                          int64_t n_transactions, const int32_t* items, int64_t n_sel,
                                          uint32_t threshold, batmap_triple* out, int64_t capacity, int64_t* n_out,
                                          double* gemm_ms, batmap_stream_t stream) {
-    if (!offsets || (!tids && n_items > 0) || !n_out || (!out && capacity > 0) || n_items < 0 ||
+    if (!offsets || !n_out || (!out && capacity > 0) || n_items < 0 ||
         n_transactions < 1 || (items && n_sel < 0)) {
         set_error("bad arguments");
         return BATMAP_E_INVALID;
@@ -357,6 +365,7 @@ batmap_status batmap_dense_pair_supports(const int64_t* offsets, const int32_t* 
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     init_pool();
+    BM_TRY(check_tids_device(offsets, tids, n_items, st));
     if (items && n_sel) {  // validate the selection on the host
         std::vector<int32_t> it(n_sel);
         BM_CUDA(cudaMemcpyAsync(it.data(), items, n_sel * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -376,7 +385,7 @@ batmap_status batmap_merge_pair_supports(const int64_t* offsets, const int32_t* 
                                          int64_t n_transactions, const int32_t* items, int64_t n_sel,
                                          uint32_t threshold, batmap_triple* out, int64_t capacity, int64_t* n_out,
                                          double* kernel_ms, int64_t* merge_steps, batmap_stream_t stream) {
-    if (!offsets || (!tids && n_items > 0) || !n_out || (!out && capacity > 0) || n_items < 0 ||
+    if (!offsets || !n_out || (!out && capacity > 0) || n_items < 0 ||
         n_transactions < 1 || (items && n_sel < 0)) {
         set_error("bad arguments");
         return BATMAP_E_INVALID;
@@ -387,6 +396,7 @@ batmap_status batmap_merge_pair_supports(const int64_t* offsets, const int32_t* 
     }
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     init_pool();
+    BM_TRY(check_tids_device(offsets, tids, n_items, st));
     if (items && n_sel) {  // validate the selection on the host
         std::vector<int32_t> it(n_sel);
         BM_CUDA(cudaMemcpyAsync(it.data(), items, n_sel * sizeof(int32_t), cudaMemcpyDeviceToHost, st));

@@ -237,6 +237,9 @@ void dfree(void* p, cudaStream_t s);
 // per-thread pinned staging buffers: slot 0 for the build's host tables, slot 1 for the K2 plan
 // upload (both reused by the next call of the thread, after its stream synchronisation)
 void* host_staging(size_t bytes, int slot = 0);
+// tids may be NULL exactly when the tidlists are all empty (a zero-length int32[offsets[n]]): reads
+// offsets[n_items] (device) when tids is NULL and n_items > 0; E_INVALID if it is not 0.
+batmap_status check_tids_device(const int64_t* offsets, const int32_t* tids, int64_t n_items, cudaStream_t st);
 // k scalar device -> host copies (each <= 8 bytes) then one synchronisation of st
 batmap_status read_scalars(cudaStream_t st, int k, const void* const* src, const size_t* bytes, void* const* dst);
 template <typename T>

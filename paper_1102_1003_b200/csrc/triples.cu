@@ -896,11 +896,12 @@ extern "C" {
 
 batmap_status batmap3_build(const int64_t* offsets, const int32_t* tids, int64_t n_items, int64_t n_transactions,
                             const batmap_build_opts* opts, batmap_stream_t stream, batmap3_handle* out) {
-    if (!out || !offsets || (n_items > 0 && !tids) || n_items < 0 || n_transactions < 1) {
+    if (!out || !offsets || n_items < 0 || n_transactions < 1) {
         set_error("batmap3_build: invalid arguments");
         return BATMAP_E_INVALID;
     }
     *out = nullptr;
+    BM_TRY(check_tids_device(offsets, tids, n_items, reinterpret_cast<cudaStream_t>(stream)));
     if (n_transactions >= (1ll << 31) || n_items >= (1ll << 21)) {
         set_error("batmap3_build: n_transactions must be < 2^31 and n_items < 2^21");
         return BATMAP_E_OVERFLOW;

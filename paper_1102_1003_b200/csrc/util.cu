@@ -59,6 +59,21 @@ void dfree(void* p, cudaStream_t s) {
 // for the thread's lifetime).  Copies from / to it are asynchronous; every build synchronises its
 // stream (the failure count) before it returns, so the next build of the thread never overwrites
 // bytes still in flight.  Returns nullptr (callers fall back to pageable copies) if pinning fails.
+batmap_status check_tids_device(const int64_t* offsets, const int32_t* tids, int64_t n_items, cudaStream_t st) {
+    if (tids || n_items <= 0) return BATMAP_OK;
+    int64_t nnz = 0;
+    if (cudaMemcpyAsync(&nnz, offsets + n_items, sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+        set_error("reading offsets[n_items]: %s", cudaGetErrorString(cudaGetLastError()));
+        return BATMAP_E_CUDA;
+    }
+    if (nnz != 0) {
+        set_error("tids is NULL but offsets[n_items] = %lld", (long long)nnz);
+        return BATMAP_E_INVALID;
+    }
+    return BATMAP_OK;
+}
+
 void* host_staging(size_t bytes, int slot) {
     static thread_local void* buf[2] = {nullptr, nullptr};
     static thread_local size_t cap[2] = {0, 0};

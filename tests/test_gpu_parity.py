@@ -449,6 +449,18 @@ def test_edge_cases():
     assert c.pair_supports(threshold=0).shape == (0, 3)
     c = _coll(np.array([0, 3], np.int64), np.array([1, 2, 3], np.int32), 10)
     assert c.pair_supports(threshold=0).shape == (0, 3)
+    # items whose tidlists are ALL empty (nnz = 0: the zero-length tids array arrives as NULL)
+    off0 = np.zeros(4, np.int64)
+    c = _coll(off0, np.zeros(0, np.int32), 10)
+    assert c.pair_supports(threshold=0).cpu().numpy().tolist() == [[0, 1, 0], [0, 2, 0], [1, 2, 0]]
+    assert c.pair_supports(threshold=1).shape[0] == 0
+    from paper_1102_1003_b200 import Collection3, dense_pair_supports, merge_pair_supports
+
+    o0, t0 = torch.as_tensor(off0).cuda(), torch.zeros(0, dtype=torch.int32, device="cuda")
+    assert merge_pair_supports(o0, t0, 10, threshold=1)[0].shape[0] == 0
+    assert dense_pair_supports(o0, t0, 10, threshold=1)[0].shape[0] == 0
+    with Collection3(o0, t0, 10) as c3:
+        assert c3.triple_supports(torch.tensor([[0, 1, 2]], dtype=torch.int32), threshold=1).shape[0] == 0
     off = np.array([0, 0, 0, 2], np.int64)
     c, got = _check_exact(off, np.array([0, 5], np.int32), 10, 0)
     assert got.tolist() == [[0, 1, 0], [0, 2, 0], [1, 2, 0]]
