@@ -222,6 +222,135 @@ __device__ __forceinline__ void chunk_ops(const uint32_t* pa, const uint32_t* pb
     }
 }
 
+// ---- balanced mode for accumulated work items (ragged / diagonal tiles of split-K and virtual
+// rectangles).  In the default mapping warp w owns four fixed 32-row x 16-column blocks of the tile
+// and skips those with no valid pair; in a ragged tile some warps then own 2 valid blocks and
+// others 1 or 0, and the CTA waits for the slowest at every chunk's barrier (C3: 15 % of the warp
+// samples).  Accumulated items add partial counts with atomics anyway, so the valid blocks' k-steps
+// can be dealt evenly instead: the sequence (valid block, k-step) is cut into one contiguous range
+// per warp, i.e. at most 4 units (block, k range) per warp, each held in one of the four 4 x 4
+// accumulator slots of the thread's micro-tile.  Slot s covers rows 32 rb + 4 (lane & 7) + i and
+// columns 16 cb + 4 (lane >> 3) + j of the tile in acc[(s >> 1) 4 + i][(s & 1) 4 + j].
+__device__ __forceinline__ uint32_t bal_unit(int rb, int cb, int klo, int khi) {
+    return 0x80000000u | ((uint32_t)rb << 24) | ((uint32_t)cb << 16) | ((uint32_t)klo << 8) | (uint32_t)khi;
+}
+
+__device__ __forceinline__ bool block_valid(const Rect& r, int ti, int tj, int tn, int rb, int cb) {
+    return k2_block_valid(r.n_rows, r.n_cols, r.diag, ti, tj, tn, rb, cb);
+}
+
+// CTA-uniform decision (k2_balance_pays, plan.h); on true, writes this warp's units to slots[0..3]
+// (0 = empty).
+template <int BN>
+__device__ __forceinline__ bool plan_balance(const Rect& r, int ti, int tj, int warp, int lane,
+                                             uint32_t* __restrict__ slots) {
+    constexpr int NW = BN / 16, NCB = BN / 16;  // warps per CTA; 16-column groups per tile
+    if (!k2_balance_pays(r.n_rows, r.n_cols, r.diag, ti, tj, BN)) return false;
+    int B = 0;
+#pragma unroll 1
+    for (int rb = 0; rb < 4; ++rb)
+#pragma unroll 1
+        for (int cb = 0; cb < NCB; ++cb) B += block_valid(r, ti, tj, BN, rb, cb);
+    const int total = 16 * B;
+    const int lo = warp * total / NW, hi = (warp + 1) * total / NW;
+    int n = 0, bi = 0;
+    __syncwarp();  // every lane has read the previous item's slots (its epilogue ran before)
+#pragma unroll 1
+    for (int rb = 0; rb < 4; ++rb)
+#pragma unroll 1
+        for (int cb = 0; cb < NCB; ++cb) {
+            if (!block_valid(r, ti, tj, BN, rb, cb)) continue;
+            const int blo = 16 * bi, klo = max(lo, blo) - blo, khi = min(hi, blo + 16) - blo;
+            if (khi > klo && n < 4) {
+                if (lane == 0) slots[n] = bal_unit(rb, cb, klo, khi);
+                ++n;
+            }
+            ++bi;
+        }
+    if (lane == 0)
+        for (int q = n; q < 4; ++q) slots[q] = 0u;
+    __syncwarp();
+    return true;
+}
+
+// 16 compare-and-counts of one 4 x 4 block into accumulator slot S (same pipeline as compute_ops).
+template <int S>
+__device__ __forceinline__ void compute_block(const uint4& xv, const uint4& xmv, const uint4& yv, const uint4& ymv,
+                                              uint32_t (&acc)[8][8]) {
+    constexpr int kD = 2, N = 16;
+    const uint32_t x[4] = {xv.x, xv.y, xv.z, xv.w}, y[4] = {yv.x, yv.y, yv.z, yv.w};
+    const uint32_t xm[4] = {xmv.x, xmv.y, xmv.z, xmv.w}, ym[4] = {ymv.x, ymv.y, ymv.z, ymv.w};
+    uint32_t u[16], p[16], v[16];
+#pragma unroll
+    for (int q = 0; q < N + 3 * kD; ++q) {
+        if (q < N) asm volatile("lop3.b32 %0, %1, %2, 0x80808080, 0xBE;" : "=r"(u[q]) : "r"(x[q >> 2]), "r"(y[q & 3]));
+        if (q >= kD && q - kD < N) asm volatile("sub.u32 %0, %1, 0x01010101;" : "=r"(p[q - kD]) : "r"(u[q - kD]));
+        if (q >= 2 * kD && q - 2 * kD < N) {
+            const int e = q - 2 * kD;
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x0E;" : "=r"(v[e]) : "r"(p[e]), "r"(xm[e >> 2]), "r"(ym[e & 3]));
+        }
+        if (q >= 3 * kD) {
+            const int e = q - 3 * kD;
+            asm volatile("dp4a.u32.u32 %0, %1, 0x01010101, %0;"
+                         : "+r"(acc[(S >> 1) * 4 + (e >> 2)][(S & 1) * 4 + (e & 3)])
+                         : "r"(v[e]));
+        }
+    }
+}
+
+// One k-chunk in balanced mode: each of the warp's units runs its k range on its block.
+template <int BN, int S>
+__device__ __forceinline__ void chunk_unit(const uint32_t* sA, const uint32_t* sB, uint32_t unit, int lane,
+                                           uint32_t (&acc)[8][8]) {
+    constexpr int kM = K2Cfg<BN>::kStageWords;
+    if (!unit) return;
+    const int rb = (unit >> 24) & 3, cb = (unit >> 16) & 15, klo = (unit >> 8) & 31, khi = unit & 31;
+    const uint32_t* pa = sA + 32 * rb + 4 * (lane & 7) + klo * kBM;
+    const uint32_t* pb = sB + 16 * cb + 4 * (lane >> 3) + klo * BN;
+#pragma unroll 1
+    for (int k = klo; k < khi; ++k, pa += kBM, pb += BN) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(pa), xmv = *reinterpret_cast<const uint4*>(pa + kM);
+        const uint4 yv = *reinterpret_cast<const uint4*>(pb), ymv = *reinterpret_cast<const uint4*>(pb + kM);
+        compute_block<S>(xv, xmv, yv, ymv, acc);
+    }
+}
+
+// End of a balanced item: add every slot's partial counts to the rectangle's counters (the
+// accumulated epilogue of work_epilogue with per-slot rows and columns).
+template <int BN>
+__device__ __forceinline__ void bal_epilogue(const Rect& r, int ti, int tj, int lane, const uint32_t* slots,
+                                             const uint32_t (&acc)[8][8], uint32_t* __restrict__ cnt) {
+    uint32_t* base = cnt + r.cnt_off;
+    const int lgR = __ffs(r.R) - 1;  // R is a power of two (widths 3r/4)
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+        const uint32_t unit = slots[sl];
+        if (!unit) continue;
+        const int rb = (unit >> 24) & 3, cb = (unit >> 16) & 15;
+        const int row0 = ti * kBM + 32 * rb + 4 * (lane & 7), col0 = tj * BN + 16 * cb + 4 * (lane >> 3);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int row = row0 + i;
+            if (row >= r.n_rows) continue;
+            uint32_t* rowp = base + (int64_t)row * r.n_cols_real;
+            const uint32_t* a = acc[(sl >> 1) * 4 + i] + (sl & 1) * 4;
+            if (r.R >= 4) {  // the 4 columns are 4 virtual columns of one item
+                if (col0 >= r.n_cols) continue;
+                const uint32_t sum = (a[0] >> 7) + (a[1] >> 7) + (a[2] >> 7) + (a[3] >> 7);
+                if (sum) atomicAdd(rowp + (col0 >> lgR), sum);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int col = col0 + j;
+                    if (col >= r.n_cols || (r.diag && row >= col)) continue;
+                    const uint32_t v = a[j] >> 7;
+                    if (v) atomicAdd(rowp + (col >> lgR), v);
+                }
+            }
+        }
+    }
+}
+
 // Per-CTA stream of k-chunks.  Work items (longest first) are claimed from a global counter by
 // thread 0 -- longest-processing-time order, so the CTAs finish within about one short item of
 // each other.  The narrow operand's chunk coordinate wraps mod W_a (reading #18).
@@ -387,7 +516,7 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
     k2_tiled(const __grid_constant__ K2Maps prm, const Rect* __restrict__ rects, const Work* __restrict__ work,
              int n_work, int* work_ctr, uint32_t* __restrict__ cnt, uint32_t* __restrict__ tail_buf, int tail_pieces,
              const int32_t* __restrict__ f, const uint8_t* __restrict__ lw, uint32_t thr, uint32_t use_f,
-             Cand* __restrict__ out, unsigned long long* __restrict__ ctr, int64_t cap) {
+             Cand* __restrict__ out, unsigned long long* __restrict__ ctr, int64_t cap, int bal_enabled) {
     using Cfg = K2Cfg<BN>;
     constexpr int kStages = Cfg::kStages, kStageSmem = Cfg::kStageSmem, kStageWords = Cfg::kStageWords;
     constexpr int kThreads = Cfg::kThreads;
@@ -395,6 +524,7 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
     uint32_t* stages = smem_raw;  // keep the shared address space visible to the compiler (LDS, not LD)
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + kStages * kStageSmem);
     __shared__ int2 meta[kStages];
+    __shared__ uint32_t bal_slots[kThreads / 32][4];  // balanced-mode units of each warp
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -419,13 +549,38 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
         for (int j = 0; j < 8; ++j) acc[i][j] = 0;
     int cur = -1;
     int inc = kAll;
+    bool bal = false;  // the current item runs in balanced mode (CTA-uniform)
+    uint32_t* my_slots = bal_slots[warp];
+    const bool bal_on = bal_enabled;
     for (uint32_t g = 0;; ++g) {
         const int buf = (int)(g % kStages);
         mbar_wait(&full[buf], (g / kStages) & 1u);
         const int2 mt = meta[buf];
         if (mt.y && cur >= 0) {  // a new work item (or the end) begins: finish the previous one
             const Work wk = work[cur];
-            if (wk.tail) {  // a piece of a cut tail tile: partial counts added (red.global.add, in
+            if (wk.tail && bal) {  // a balanced ordinary tile: each slot's counts go where the
+                                   // default mapping keeps that pair (thread 32 w' + lane, block (h, hc))
+                uint32_t* slice = tail_buf + (int64_t)((wk.tail - 1) / tail_pieces) * (kBM * BN);
+#pragma unroll
+                for (int sl = 0; sl < 4; ++sl) {
+                    const uint32_t unit = my_slots[sl];
+                    if (!unit) continue;
+                    const int rb = (unit >> 24) & 3, cb = (unit >> 16) & 15;
+                    const int w2 = (rb & 1) | ((cb % (BN / 32)) << 1), h = rb >> 1, hc = cb / (BN / 32);
+                    uint32_t* dst = slice + 4 * (32 * w2 + lane);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t v = acc[(sl >> 1) * 4 + i][(sl & 1) * 4 + j];
+                            if (v)
+                                asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(
+                                                 dst + (int64_t)((2 * (4 * h + i) + hc) * kThreads) * 4 + j),
+                                             "r"(v)
+                                             : "memory");
+                        }
+                }
+            } else if (wk.tail) {  // a piece of a cut tail tile: partial counts added (red.global.add, in
                             // L2) into its tile's one zeroed slice, laid out as 16 uint4 planes of
                             // kThreads (coalesced loads in k2_tail_threshold); one slice per tile
                             // instead of one per piece keeps the tail's writes in L2
@@ -439,6 +594,8 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
                                              dst + (int64_t)((2 * i + (j >> 2)) * kThreads) * 4 + (j & 3)),
                                          "r"(acc[i][j])
                                          : "memory");
+            } else if (bal) {
+                bal_epilogue<BN>(rects[wk.rect], wk.ti, wk.tj, lane, my_slots, acc, cnt);
             } else {
                 work_epilogue<BN>(rects[wk.rect], wk.ti, wk.tj, tr, tc, lane, acc, cnt, f, lw, thr, use_f, out,
                                   ctr, cap);
@@ -453,7 +610,9 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
             // ragged edge and diagonal tiles: blocks of pairs that are all invalid are skipped,
             // leaving their issue slots to the other CTA
             const Work wk = work[mt.x];
-            inc = block_mask<BN>(rects[wk.rect], wk.ti, wk.tj, warp);
+            const Rect& rr = rects[wk.rect];
+            inc = block_mask<BN>(rr, wk.ti, wk.tj, warp);
+            bal = bal_on && (rr.acc || wk.tail) && plan_balance<BN>(rr, wk.ti, wk.tj, warp, lane, my_slots);
         }
         cur = mt.x;
         uint32_t* sA = stages + buf * kStageSmem;
@@ -476,8 +635,14 @@ __global__ void __launch_bounds__(K2Cfg<BN>::kThreads, K2Cfg<BN>::kMinBlocks)
                            full, meta, end_sent);
         const uint32_t* pa = sA + 4 * tr;
         const uint32_t* pb = sA + kBK * kBM + 4 * tc;
-        if (inc == kAll) {  // the common case first: one test on the hot path
+        if (inc == kAll && !bal) {  // the common case first: one test on the hot path
             chunk_ops<BN, kAll>(pa, pb, acc);
+        } else if (bal) {
+            const uint32_t* sB = sA + kBK * kBM;
+            chunk_unit<BN, 0>(sA, sB, my_slots[0], lane, acc);
+            chunk_unit<BN, 1>(sA, sB, my_slots[1], lane, acc);
+            chunk_unit<BN, 2>(sA, sB, my_slots[2], lane, acc);
+            chunk_unit<BN, 3>(sA, sB, my_slots[3], lane, acc);
         } else {
             switch (inc) {  // the reachable block sets; any other non-empty set computes all four
                 case 0: break;
@@ -1066,6 +1231,7 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
     batmap_status rc = BATMAP_OK;
     int* work_ctr = reinterpret_cast<int*>(h->ctr_d + 1);
     const int grid = (int)std::min<int64_t>(n_work, grid_cap);
+    const int bal_on = env_off("BATMAP_K2_BALANCE") ? 0 : 1;  // balanced accumulated items (test switch)
     for (int attempt = 0; attempt < 2; ++attempt) {
         BM_CUDA(cudaMemsetAsync(h->ctr_d, 0, 2 * sizeof(unsigned long long), st));  // [1] = work counter
         if (pl.cnt_entries) BM_CUDA(cudaMemsetAsync(h->cnt_d, 0, pl.cnt_entries * sizeof(uint32_t), st));
@@ -1075,12 +1241,12 @@ batmap_status run_intersect(batmap_collection* h, const Selection& sel, uint32_t
             k2_tiled<128><<<grid, K2Cfg<128>::kThreads, K2Cfg<128>::kSmemBytes, st>>>(
                 *prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, h->tail_d, std::max(pl.tail_pieces, 1), sel.f,
                 kp->lw_d, threshold, use_f,
-                h->cand_d, h->ctr_d, h->cand_cap);
+                h->cand_d, h->ctr_d, h->cand_cap, bal_on);
         else
             k2_tiled<64><<<grid, K2Cfg<64>::kThreads, K2Cfg<64>::kSmemBytes, st>>>(
                 *prm, rects_d, work_d, (int)n_work, work_ctr, h->cnt_d, h->tail_d, std::max(pl.tail_pieces, 1), sel.f,
                 kp->lw_d, threshold, use_f,
-                h->cand_d, h->ctr_d, h->cand_cap);
+                h->cand_d, h->ctr_d, h->cand_cap, bal_on);
         rec(h, EV_K21, st);
         h->launches += 1;
         if (!pl.tails.empty()) {

@@ -612,6 +612,27 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             work.insert(work.end(), tail.begin(), tail.end());
         }
     }
+    // ---- ordinary tiles that K2 will run in balanced mode (ragged or diagonal tiles whose warps hold
+    // unequal numbers of valid blocks; k2_balance_pays, plan.h): they add their partial counts into a
+    // tail slice like the cut tail tiles, and k2_tail_threshold tests them.  Scanned only for plans of
+    // moderate size (C2: 5,312 items, 1.5 % of its K2 time in such tiles); in C4's 3e5 items they
+    // weigh 0.2 % and the scan would lengthen the build.
+    const char* be = getenv("BATMAP_K2_BALANCE");
+    if (allow_split && !(be && be[0] == '0') && P.work.size() <= 65536) {
+        const int pcs = P.tail_pieces > 0 ? P.tail_pieces : 1;
+        for (Work& w : P.work) {
+            if (w.tail) continue;
+            const Rect& r = P.rects[w.rect];
+            if (r.acc) continue;
+            const bool ragged = (int64_t)(w.ti + 1) * kTile > r.n_rows || (int64_t)(w.tj + 1) * TN > r.n_cols ||
+                                (r.diag && (int64_t)w.tj * TN < (int64_t)(w.ti + 1) * kTile);
+            if (!ragged || !k2_balance_pays(r.n_rows, r.n_cols, r.diag, w.ti, w.tj, TN)) continue;
+            const int t = (int)P.tails.size();
+            P.tails.push_back({w.rect, w.ti, w.tj, 0});
+            w.tail = 1 + t * pcs;
+        }
+        if (!P.tails.empty()) P.tail_pieces = pcs;
+    }
 }
 
 }  // namespace bm

@@ -57,6 +57,36 @@ struct PoolAlloc {
 };
 using WorkList = std::vector<Work, PoolAlloc<Work>>;
 
+// K2's balanced mode (intersect.cu): in a ragged or diagonal tile the warps' fixed 32 x 16 blocks
+// hold unequal numbers of valid pairs; dealing the valid blocks' k-steps evenly over the warps pays
+// when the busiest warp would otherwise run at least 1/16 longer than the even share, and each warp's
+// contiguous share then touches at most 4 blocks.  Evaluated identically on the host (which gives
+// ordinary tiles that will run balanced a slice of the tail buffer) and in the kernel.
+__host__ __device__ inline bool k2_block_valid(int n_rows, int n_cols, int diag, int ti, int tj, int tn, int rb,
+                                               int cb) {
+    const int r0 = ti * kTile + 32 * rb, c0 = tj * tn + 16 * cb;
+    return r0 < n_rows && c0 < n_cols && !(diag && r0 >= c0 + 15);
+}
+__host__ __device__ inline bool k2_balance_pays(int n_rows, int n_cols, int diag, int ti, int tj, int tn) {
+    const int nw = tn / 16, ncb = tn / 16;  // warps per CTA; 16-column groups per tile
+    int B = 0, dmax = 0;
+    for (int rb = 0; rb < 4; ++rb)
+        for (int cb = 0; cb < ncb; ++cb) B += k2_block_valid(n_rows, n_cols, diag, ti, tj, tn, rb, cb);
+    for (int w = 0; w < nw; ++w) {  // default: warp w owns row groups (w & 1) + {0, 2}, columns (w >> 1) + {0, ncb / 2}
+        int c = 0;
+        for (int t = 0; t < 4; ++t)
+            c += k2_block_valid(n_rows, n_cols, diag, ti, tj, tn, (w & 1) + 2 * (t >> 1), (w >> 1) + (ncb / 2) * (t & 1));
+        dmax = dmax > c ? dmax : c;
+    }
+    const int total = 16 * B, bmax = (total + nw - 1) / nw;
+    if (B == 0 || bmax + bmax / 16 >= 16 * dmax) return false;  // a unit loads 2x the operands per compare
+    for (int w = 0; w < nw; ++w) {
+        const int lo = w * total / nw, hi = (w + 1) * total / nw;
+        if (hi > lo && (hi - 1) / 16 - lo / 16 + 1 > 4) return false;
+    }
+    return true;
+}
+
 struct TailTile {  // a whole tile of an ordinary rectangle, cut into pieces at the end of the schedule
     int32_t rect, ti, tj, pad;
 };
