@@ -347,7 +347,9 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
     // with different SM counts (MIG slices, mixed GPUs) must build identical unit lists, or pairs
     // would be dropped or emitted twice.  grid_cap stays in use for the part-local tail split below.
     const int split_grid = n_parts > 1 ? kDealGrid : std::max(grid_cap, 1);
-    const int64_t target = std::max<int64_t>(1, total / ((int64_t)n_parts * 4 * split_grid));
+    const char* fe = getenv("BATMAP_K2_SPLITF");  // split granularity f (measured: 4; test hook)
+    const int64_t split_f = fe && atoi(fe) > 0 ? atoi(fe) : 4;
+    const int64_t target = std::max<int64_t>(1, total / ((int64_t)n_parts * split_f * split_grid));
     if (allow_split)
         for (Rect& r : P.rects)
             if (tile_cost(r) > 2 * target && r.W / kChunk > 1) r.acc = 1;
@@ -568,6 +570,8 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
     // pieces' partial counts into one slice per tile (red.global.add), which k2_tail_threshold
     // tests; k-pieces of accumulated rectangles are cut finer and add into their counters as before
     // (C3: 2,391 items of 22-24 chunks on 592 CTAs left 23 CTAs a fifth item, makespan/mean 1.22).
+    const char* ate = getenv("BATMAP_K2_ACCTAIL");  // 0: no finer cut of accumulated tail pieces (test hook)
+    const bool acc_tail_off = ate && ate[0] == '0';
     if (allow_split && grid_cap > 0 && !P.work.empty()) {
         WorkList& work = P.work;
         const size_t n = work.size();
@@ -580,7 +584,7 @@ void plan_work(const std::vector<ClassInfo>& orig, int part, int n_parts, int gr
             const int nk = r.W / kChunk;
             if (r.acc) {  // a k-piece of an accumulated rectangle: cut it finer, the counters add up
                 const int len = w.k1 - w.k0;
-                const int ap = len >= 64 ? 8 : (len >= 16 ? 4 : (len >= 4 ? 2 : 1));
+                const int ap = acc_tail_off ? 1 : len >= 64 ? 8 : (len >= 16 ? 4 : (len >= 4 ? 2 : 1));
                 for (int p = 0; p < ap; ++p) {
                     Work wp = w;
                     wp.k0 = w.k0 + (int32_t)((int64_t)len * p / ap);
