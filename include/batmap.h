@@ -46,6 +46,20 @@ typedef enum {
 typedef struct CUstream_st* batmap_stream_t;   /* == cudaStream_t */
 typedef struct batmap_collection* batmap_handle; /* library-owned; free with batmap_destroy */
 
+/*
+ * Environment switches (diagnostics and test hooks; read per call; every setting is exact, only the
+ * speed differs):
+ *   BATMAP_K1_BYTE=0|all      byte-table K1 tier never / for every class (default: measured policy)
+ *   BATMAP_K1_SMALL, BATMAP_K1_SPREAD, BATMAP_K1_SIDE, BATMAP_K1_IPC   other K1 tier policies
+ *   BATMAP_K2_TN=64|128       K2 tile width (default: the planner's cost model)
+ *   BATMAP_K2_PROMOTE=0, BATMAP_K2_VIRTUAL=0, BATMAP_K2_SPLIT=0        planner features off
+ *   BATMAP_K2_SPLITF=f        split-K granularity (default 4); BATMAP_K2_ACCTAIL=0: no finer tail cut
+ *   BATMAP_K2_GROUP=g         tile rows per band of large rectangles (default: ~32 MB bands)
+ *   BATMAP_K2_BALANCE=0       K2's balanced mode for ragged / diagonal tiles off
+ *   BATMAP_K3_GROUPED=0       the one-warp-per-candidate triple kernel instead of the grouped one
+ *   BATMAP_AB_CAP=n           force the A_b re-run path;  BATMAP_TRACE=1: host phase timestamps (stderr)
+ */
+
 /* Build flags */
 #define BATMAP_CHECK_INPUT 0x1u   /* validate on device: every tidlist strictly increasing, 0 <= tid < m */
 #define BATMAP_BUILD_SERIAL 0x2u  /* one thread runs each item's INSERTs in ascending tid order:
@@ -102,7 +116,10 @@ typedef struct {
  *   offsets   [device] int64[n_items+1], offsets[0] = 0, non-decreasing: item i's tidlist
  *             is tids[offsets[i] .. offsets[i+1]).
  *   tids      [device] int32[offsets[n_items]]: each tidlist strictly increasing,
- *             0 <= tid < n_transactions (validated only with BATMAP_CHECK_INPUT).
+ *             0 <= tid < n_transactions (validated only with BATMAP_CHECK_INPUT).  May be NULL
+ *             when offsets[n_items] == 0 (every tidlist empty; a zero-length array); the same
+ *             holds for the tids of batmap3_build, batmap_dense_pair_supports and
+ *             batmap_merge_pair_supports.
  *   n_items, n_transactions   n and m; 1 <= m < 2^31, 0 <= n < 2^31.
  *   opts      [host] may be NULL (defaults).
  *   out       [host] receives the handle.
