@@ -23,6 +23,7 @@
 // k3_triples (one warp per candidate, SWAR over the 4 byte lanes of a word), k3_correct,
 // k_cand_count / k_cand_emit (Apriori join of the sorted frequent pairs).
 #include <algorithm>
+#include <type_traits>
 #include <cub/cub.cuh>
 #include <cstring>
 #include <vector>
@@ -434,6 +435,112 @@ __global__ void __launch_bounds__(kG3Threads) k3_triples_grouped(const int32_t* 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int g = 0; g < kG3; ++g) {
+        uint32_t v = cnt[g];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (lane == 0) sred[g][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+        const int g = threadIdx.x;
+        uint32_t c = 0;
+#pragma unroll
+        for (int q = 0; q < kG3Threads / 32; ++q) c += sred[g][q] >> 6;  // 64 per counted entry
+        const uint32_t slack = use_f ? (uint32_t)(f[sit[g][0]] + f[sit[g][1]] + f[sit[g][2]]) : 0u;
+        if (c + slack >= threshold) {
+            const unsigned long long at = atomicAdd(ctr, 1ull);
+            if ((int64_t)at < cap)
+                out[at] = Cand3{(uint32_t)sit[g][0], (uint32_t)sit[g][1], (uint32_t)sit[g][2], c};
+        }
+    }
+}
+
+// Variant of the grouped kernel with the CTA's per-candidate parameters hoisted into registers
+// before the loop over words (no shared-memory reads and no 64-bit address arithmetic per step), and
+// G candidates per CTA (BATMAP_K3_HOIST=4|8 selects it; A/B against k3_triples_grouped).
+template <int T, int G>
+__device__ __forceinline__ void triples_step_h(uint32_t w, int nc, uint32_t newmask, const uint4* const (&cb)[G],
+                                               const uint32_t (&cm)[G], const uint32_t (&cw)[G],
+                                               const uint4* const (&ab)[G][2], const uint32_t (&abm)[G][2],
+                                               uint32_t (&cnt)[G]) {
+    const uint32_t w4 = w >> 2;
+    uint4 cv[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) cv[g] = w < cw[g] ? __ldg(cb[g] + (w4 & cm[g])) : make_uint4(0u, 0u, 0u, 0u);
+    PairWord p[4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        if (g >= nc) break;
+        if (g == 0 || (newmask >> g & 1u)) {  // a run starts: its B_i, B_j words (wrapped, reading #18)
+            const uint4 a = __ldg(ab[g][0] + (w4 & abm[g][0]));
+            const uint4 b = __ldg(ab[g][1] + (w4 & abm[g][1]));
+            p[0] = pair_word<T>(a.x, b.x);
+            p[1] = pair_word<T>(a.y, b.y);
+            p[2] = pair_word<T>(a.z, b.z);
+            p[3] = pair_word<T>(a.w, b.w);
+        }
+        if (w >= cw[g]) continue;
+        uint32_t acc = cnt[g];
+        acc = triple_word_acc<T>(p[0], cv[g].x, acc);
+        acc = triple_word_acc<T>(p[1], cv[g].y, acc);
+        acc = triple_word_acc<T>(p[2], cv[g].z, acc);
+        cnt[g] = triple_word_acc<T>(p[3], cv[g].w, acc);
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kG3Threads) k3_triples_hoisted(const int32_t* __restrict__ cand, int64_t n_cand,
+                                                                 const int64_t* __restrict__ woff,
+                                                                 const uint8_t* __restrict__ log2r,
+                                                                 const uint8_t* __restrict__ arena, int log2r0,
+                                                                 const int32_t* __restrict__ f, uint32_t threshold,
+                                                                 uint32_t use_f, Cand3* __restrict__ out,
+                                                                 unsigned long long* __restrict__ ctr, int64_t cap) {
+    __shared__ int32_t sit[G][3];
+    __shared__ int64_t soff[G][3];
+    __shared__ uint32_t swm[G][3];
+    __shared__ uint32_t sred[G][kG3Threads / 32];
+    const int64_t z0 = (int64_t)blockIdx.x * G;
+    const int nc = (int)(n_cand - z0 < G ? n_cand - z0 : G);
+    if (threadIdx.x < 3 * nc) {
+        const int g = threadIdx.x / 3, u = threadIdx.x % 3;
+        const int32_t it = cand[3 * z0 + threadIdx.x];
+        sit[g][u] = it;
+        soff[g][u] = woff[it];
+        swm[g][u] = (1u << log2r[it]) - 1u;  // words = 4r / 4 = r
+    }
+    __syncthreads();
+    const uint4* cb[G];
+    const uint4* ab[G][2];
+    uint32_t cm[G], cw[G], abm[G][2];
+    uint32_t newmask = 0, Wmax = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const bool on = g < nc;
+        cb[g] = reinterpret_cast<const uint4*>(arena + (on ? soff[g][2] : 0));
+        ab[g][0] = reinterpret_cast<const uint4*>(arena + (on ? soff[g][0] : 0));
+        ab[g][1] = reinterpret_cast<const uint4*>(arena + (on ? soff[g][1] : 0));
+        cm[g] = on ? swm[g][2] >> 2 : 0u;
+        abm[g][0] = on ? swm[g][0] >> 2 : 0u;
+        abm[g][1] = on ? swm[g][1] >> 2 : 0u;
+        cw[g] = on ? max(max(swm[g][0], swm[g][1]), swm[g][2]) + 1u : 0u;
+        Wmax = max(Wmax, cw[g]);
+        if (on && g > 0 && (sit[g][0] != sit[g - 1][0] || sit[g][1] != sit[g - 1][1])) newmask |= 1u << g;
+    }
+    uint32_t cnt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) cnt[g] = 0;
+    for (uint32_t w = 4 * threadIdx.x; w < Wmax; w += 4 * kG3Threads) {
+        switch ((w >> (log2r0 - 2)) & 3u) {  // the table of these 4 words (r_0 >= 16)
+            case 0: triples_step_h<0, G>(w, nc, newmask, cb, cm, cw, ab, abm, cnt); break;
+            case 1: triples_step_h<1, G>(w, nc, newmask, cb, cm, cw, ab, abm, cnt); break;
+            case 2: triples_step_h<2, G>(w, nc, newmask, cb, cm, cw, ab, abm, cnt); break;
+            default: triples_step_h<3, G>(w, nc, newmask, cb, cm, cw, ab, abm, cnt); break;
+        }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
         uint32_t v = cnt[g];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
@@ -955,8 +1062,23 @@ batmap_status batmap3_triple_supports(batmap3_handle h, const int32_t* triples, 
     cudaEventRecord(h->ev[2], st);
     // grouped when the narrowest BatMap has >= 1024 words (C3: r_0 = 2048; measured 2.26 -> 2.09 ms);
     // C1's 256-word BatMaps leave a CTA of 8 candidates one half-occupied step (2.6 -> 4.2 ms)
-    const bool grouped = h->log2r0 >= 10 && !env_flag_off("BATMAP_K3_GROUPED");
-    if (grouped)
+    const char* ge = getenv("BATMAP_K3_GROUPED");  // 0: never; 1: also below 1024 words (A/B hook)
+    const bool grouped = (h->log2r0 >= 10 || (ge && ge[0] == '1' && h->log2r0 >= 4)) && !env_flag_off("BATMAP_K3_GROUPED");
+    // candidates per CTA of the hoisted kernel: 4 (measured on C3: 1.56 ms vs 1.81 with 8 and 1.86
+    // for the shared-memory-parameter kernel, BATMAP_K3_HOIST=0); 2, 6, 8 are A/B hooks
+    const char* he = getenv("BATMAP_K3_HOIST");
+    const int hoist = he ? atoi(he) : 4;
+    auto launch_h = [&](auto gtag) {
+        constexpr int G = decltype(gtag)::value;
+        k3_triples_hoisted<G><<<(unsigned)((n_triples + G - 1) / G), kG3Threads, 0, st>>>(
+            triples, n_triples, h->woff_d, h->log2r_d, h->arena_d, h->log2r0, h->f_d, threshold, 1u, cand, ctr,
+            n_triples);
+    };
+    if (grouped && hoist == 2) launch_h(std::integral_constant<int, 2>());
+    else if (grouped && hoist == 4) launch_h(std::integral_constant<int, 4>());
+    else if (grouped && hoist == 6) launch_h(std::integral_constant<int, 6>());
+    else if (grouped && hoist == 8) launch_h(std::integral_constant<int, 8>());
+    else if (grouped)
         k3_triples_grouped<<<(unsigned)((n_triples + kG3 - 1) / kG3), kG3Threads, 0, st>>>(
             triples, n_triples, h->woff_d, h->log2r_d, h->arena_d, h->log2r0, h->f_d, threshold, 1u, cand, ctr,
             n_triples);
