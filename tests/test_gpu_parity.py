@@ -408,6 +408,30 @@ def test_tile_widths_exact(max_loop, monkeypatch):
     c.close()
 
 
+@pytest.mark.parametrize("tn", ["128", "64"])
+def test_balanced_mode_exact(tn, monkeypatch):
+    """K2's balanced mode (ragged / diagonal tiles deal their valid blocks' k-steps evenly over the
+    warps; ordinary tiles then go through a tail slice) against the default mapping and the oracle,
+    on a shape with ragged edges in every class, with and without forced failures, whole and in a
+    3-way part split."""
+    monkeypatch.setenv("BATMAP_K2_TN", tn)
+    off, tids, m = _quest_widths(11)
+    ref0 = oracle.pairs_merge(off, tids, threshold=0)
+    for max_loop in (0, 1):
+        c = _coll(off, tids, m, seed=9, max_loop=max_loop)
+        outs = []
+        for bal in ("1", "0"):
+            monkeypatch.setenv("BATMAP_K2_BALANCE", bal)
+            got = _np(c.pair_supports(threshold=0))
+            np.testing.assert_array_equal(got, ref0)
+            outs.append(_np(c.pair_supports(threshold=0, raw=True)))
+            parts = np.concatenate([_np(c.pair_supports(threshold=2, part=p, n_parts=3)) for p in range(3)])
+            parts = parts[np.lexsort((parts[:, 1], parts[:, 0]))]
+            np.testing.assert_array_equal(parts, ref0[ref0[:, 2] >= 2])
+        np.testing.assert_array_equal(outs[0], outs[1])
+        c.close()
+
+
 def test_frequent_only_same_output():
     """BATMAP_PAIRS_FREQUENT intersects only items with |S_i| >= threshold and returns exactly
     the same triples: full selection, a subset, parts, with forced failures; ignored at threshold 0."""

@@ -211,12 +211,17 @@ def test_mine_triples_planted():
     np.testing.assert_array_equal(got, ref)
 
 
-@pytest.mark.parametrize("grouped", ["", "0"])  # "" = the pair-grouped kernel (r_0 >= 1024); "0" = warp per candidate
+# "" = the default grouped kernel (hoisted parameters, 4 candidates per CTA; r_0 >= 1024); "0" = warp
+# per candidate; "h0" = the grouped kernel with shared-memory parameters; "h2" / "h6" / "h8" = other
+# candidates-per-CTA counts of the hoisted kernel
+@pytest.mark.parametrize("grouped", ["", "0", "h0", "h2", "h6", "h8"])
 def test_triple_kernels_any_candidate_order(grouped, monkeypatch):
-    """k3_triples_grouped reuses B_i and B_j across a run of candidates sharing (i, j); it must be
-    exact for any candidate order (runs split anywhere), with and without failures, and agree with
-    the one-warp-per-candidate kernel."""
-    if grouped:
+    """The grouped kernels reuse B_i and B_j across a run of candidates sharing (i, j); they must be
+    exact for any candidate order (runs split anywhere, CTAs of any size), with and without
+    failures, and agree with the one-warp-per-candidate kernel."""
+    if grouped.startswith("h"):
+        monkeypatch.setenv("BATMAP_K3_HOIST", grouped[1:])
+    elif grouped:
         monkeypatch.setenv("BATMAP_K3_GROUPED", grouped)
     off, tids, m = _instance(21, n=14)
     rng = np.random.default_rng(5)
