@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(NT) k1_byte(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
     int64_t first, int n_cls, uint32_t r, int log2r, PiParams P, uint32_t r0, int log2r0, uint32_t max_loop_opt,
     uint32_t* __restrict__ arena_cls, int n_pad, uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr,
-    int64_t fail_cap) {
+    int64_t fail_cap, uint32_t* __restrict__ stage) {
     static_assert(CS == 1 || IPC == 1, "an item spread over a cluster is built alone");
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) uint8_t TB[];  // IPC item slices (CS = 1) or this CTA's slice of one item
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(NT) k1_byte(
     const uint32_t slice = 3u * r / CS;
     const uint32_t stride_b = IPC == 1 ? slice : slice + 16u;  // item k's slice at TB + k * stride_b
     const int c0 = (int)(blockIdx.x / CS) * IPC;                // first column of this CTA (cluster)
-    const int n_it = min(IPC, n_cls - c0);
+    const int n_it = max(0, min(IPC, n_cls - c0));
     if (threadIdx.x <= IPC) {
         int cnt = 0;
         for (int k = 0; k < (int)threadIdx.x && k < n_it; ++k) {
@@ -775,7 +775,16 @@ __global__ void __launch_bounds__(NT) k1_byte(
     if (CS > 1) cg::this_cluster().sync();
     else __syncthreads();
     // pack: the table words are the arena words (entry e = byte lane e & 3 of word e >> 2)
-    if (IPC == 1) {
+    if (CS == 1 && stage) {  // each table as one contiguous row of the staging block
+        // (k_pack_transpose then writes the arena in 128-byte row segments): one store instruction
+        // here moves 512 bytes instead of 32 single words (IPC = 1) or pairs (IPC = 2) n_pad apart
+        const uint32_t n16 = slice / 16;
+        for (uint32_t i = threadIdx.x; i < (uint32_t)n_it * n16; i += NT) {
+            const uint32_t k = i / n16, j = i - k * n16;
+            reinterpret_cast<uint4*>(stage + (int64_t)(c0 + k) * (slice / 4))[j] =
+                reinterpret_cast<const uint4*>(TB + k * stride_b)[j];
+        }
+    } else if (IPC == 1) {
         const uint32_t w0 = rank * slice / 4;
         for (uint32_t i = threadIdx.x; i < slice / 16; i += NT) {
             const uint4 v = reinterpret_cast<const uint4*>(TB)[i];
@@ -794,6 +803,28 @@ __global__ void __launch_bounds__(NT) k1_byte(
         }
     }
     if (CS > 1) cg::this_cluster().sync();  // no CTA may exit while another still reads its slice
+}
+
+// Staged pack of the byte tier: stage holds the class's tables item-major ([item][word], W words
+// each); the arena block is word-major ([word][n_pad items], the layout K2's TMA boxes read).  A
+// 32-item x 32-word tile goes through shared memory: reads of 128 bytes along the words of an item,
+// writes of 128 bytes along the items of a word row.
+__global__ void __launch_bounds__(256) k_pack_transpose(const uint32_t* __restrict__ stage, int n, uint32_t W,
+                                                        uint32_t* __restrict__ arena_cls, int n_pad) {
+    __shared__ uint32_t tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32, w0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t i = i0 + ty + 8 * q, w = w0 + tx;
+        if (i < n && w < W) tile[ty + 8 * q][tx] = stage[i * W + w];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t w = w0 + ty + 8 * q, i = i0 + tx;
+        if (i < n && w < W) arena_cls[w * n_pad + i] = tile[tx][ty + 8 * q];
+    }
 }
 
 // Encode columns [0, n) of one class block: thread per (word w, column c); writes
@@ -1241,12 +1272,34 @@ static batmap_status launch_byte(const ClassInfo& c, batmap_collection* h, const
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    BM_CUDA(cudaLaunchKernelEx(&cfg, k1_byte<CS, IPC, NT>, offsets, tids, (const int32_t*)h->pos2orig_d,
-                               (int64_t)c.first, (int)c.n, (uint32_t)c.r, ilog2_u64((uint64_t)c.r), h->pi,
-                               (uint32_t)h->r0, h->log2r0, h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, fails,
-                               fail_ctr, fail_cap));
-    h->launches += 1;
-    return BATMAP_OK;
+    // one or two items per CTA: stage the tables item-major and transpose into the arena (the direct
+    // pack's single-word stores n_pad apart cost ~25 % of k1_byte on C5 p = 10 %: build 16.6 -> 12.4
+    // ms with staging); BATMAP_K1_STAGE=0: direct
+    uint32_t* stage = nullptr;
+    const char* se = getenv("BATMAP_K1_STAGE");
+    // (IPC = 8 already stores whole 32-byte sectors; BATMAP_K1_STAGE=4 also stages IPC = 4)
+    const int stage_max_ipc = se && se[0] == '4' ? 4 : 2;
+    if (CS == 1 && IPC <= stage_max_ipc && !(se && se[0] == '0') && c.n >= 64 &&
+        dalloc_t(&stage, (int64_t)c.n * c.W, st) != BATMAP_OK) {
+        stage = nullptr;  // no room for the staging block: pack directly
+        cudaGetLastError();
+    }
+    const batmap_status rc = [&]() -> batmap_status {
+        BM_CUDA(cudaLaunchKernelEx(&cfg, k1_byte<CS, IPC, NT>, offsets, tids, (const int32_t*)h->pos2orig_d,
+                                   (int64_t)c.first, (int)c.n, (uint32_t)c.r, ilog2_u64((uint64_t)c.r), h->pi,
+                                   (uint32_t)h->r0, h->log2r0, h->max_loop_opt, h->arena_d + c.word_off, c.n_pad,
+                                   fails, fail_ctr, fail_cap, stage));
+        h->launches += 1;
+        if (stage) {
+            const dim3 grid((unsigned)((c.n + 31) / 32), (unsigned)((c.W + 31) / 32));  // x: items, y: words
+            k_pack_transpose<<<grid, 256, 0, st>>>(stage, (int)c.n, (uint32_t)c.W, h->arena_d + c.word_off, c.n_pad);
+            BM_CUDA(cudaGetLastError());
+            h->launches += 1;
+        }
+        return BATMAP_OK;
+    }();
+    if (stage) dfree(stage, st);
+    return rc;
 }
 
 // byte tier: the smallest cluster whose CTAs hold <= 192 KB of the item's 3r table bytes, spread over

@@ -24,7 +24,7 @@ from paper_1102_1003_b200 import Collection  # noqa: E402
 from workloads import make_config  # noqa: E402
 
 ENV = {"byte": "BATMAP_K1_BYTE", "small": "BATMAP_K1_SMALL", "spread": "BATMAP_K1_SPREAD", "side": "BATMAP_K1_SIDE",
-       "ipc": "BATMAP_K1_IPC"}
+       "ipc": "BATMAP_K1_IPC", "stage": "BATMAP_K1_STAGE"}
 
 
 def _reference(w):
