@@ -1,7 +1,7 @@
 """Randomized exactness stress of the whole path against the oracle, for a fixed wall-clock budget:
 random shapes (uniform or Zipf tidlists, a few long items to reach the cluster and global build
 tiers), forced insertion failures, item subsets, both K1 cluster policies, the byte-table K1 tier
-(never / default / every class), both K2 tile widths, K2's balanced mode on and off, and -- where horizontal triple counting is
+(never / default / every class), both K2 tile widths, K2's balanced mode on and off, the byte tier's staged pack, and -- where horizontal triple counting is
 cheap -- the NEXT-4 triples path (candidates from the frequent pairs, 3-of-4 BatMaps, supports).
 The concurrent build is timing-dependent (reading #9b), so rare interleavings only show up over
 many runs; every run must be bit-exact.  (K1 side stream on/off too.)
@@ -54,6 +54,7 @@ def main():
         os.environ["BATMAP_K2_TN"] = str(int(rng.choice([64, 128])))
         os.environ["BATMAP_K1_SIDE"] = str(int(rng.integers(0, 2)))
         os.environ["BATMAP_K2_BALANCE"] = str(int(rng.integers(0, 2)))
+        os.environ["BATMAP_K1_STAGE"] = str(rng.choice(["0", "1", "4"]))  # byte-tier staged pack
         byte = str(rng.choice(["", "0", "all"]))
         if byte:
             os.environ["BATMAP_K1_BYTE"] = byte
