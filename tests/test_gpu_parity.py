@@ -237,6 +237,39 @@ def test_byte_tier_many_small_tables(ipc, max_loop, monkeypatch):
     np.testing.assert_array_equal(_np(c.pair_supports(threshold=2)), oracle.pairs_horizontal(off, tids, m, threshold=2))
 
 
+@pytest.mark.parametrize("max_loop", [0, 1])
+def test_byte_tier_staged_pack(max_loop, monkeypatch):
+    """Byte-tier CTAs holding one 96 KB (r = 2^15) or 192 KB (r = 2^16) table each: the staged pack
+    (tables written item-major, then k_pack_transpose into the [word][item] arena: one extra launch
+    per class) and the direct pack (BATMAP_K1_STAGE=0) both give the oracle's supports and the
+    layout invariants, with and without forced failures; 100 + 80 items (one CTA per table on 148
+    SMs), so ragged 32-item transpose tiles occur."""
+    rng = np.random.default_rng(23)
+    m = 200000
+    pool = rng.choice(m, size=40000, replace=False)
+    rows = []
+    for size, cnt in ((12000, 100), (26000, 80)):
+        for _ in range(cnt):
+            k = int(size * rng.uniform(0.8, 1.0))
+            mine = np.concatenate([rng.choice(pool, size=k // 2, replace=False), rng.choice(m, size=k - k // 2)])
+            rows.append(np.unique(mine).astype(np.int32))
+    off = np.zeros(len(rows) + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    tids = np.concatenate(rows)
+    ref = oracle.pairs_horizontal(off, tids, m, threshold=4000)
+    launches = {}
+    for stage in ("0", "1"):
+        monkeypatch.setenv("BATMAP_K1_STAGE", stage)
+        c = _coll(off, tids, m, seed=4, max_loop=max_loop)
+        assert c.info()["n_classes"] == 2
+        launches[stage] = c.stats()["launches_build"]
+        _check_layout_invariants(c, off, tids, m, 4)
+        np.testing.assert_array_equal(_np(c.pair_supports(threshold=4000)), ref)
+        c.close()
+    if torch.cuda.get_device_properties(0).multi_processor_count <= 148:  # one CTA per table: both staged
+        assert launches["1"] == launches["0"] + 2, launches
+
+
 def _sharded(off, tids, m, n_parts, **kw):
     """Build every part of a sharded build in this process and exchange as build_distributed
     does (the all_gather is a concatenation here)."""
