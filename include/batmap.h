@@ -51,7 +51,7 @@ typedef struct batmap_collection* batmap_handle; /* library-owned; free with bat
  * speed differs):
  *   BATMAP_K1_BYTE=0|all      byte-table K1 tier never / for every class (default: measured policy)
  *   BATMAP_K1_SMALL, BATMAP_K1_SPREAD, BATMAP_K1_SIDE, BATMAP_K1_IPC   other K1 tier policies
- *   BATMAP_K1_STAGE=0|4       byte-tier staged pack off / also for 4 items per CTA (default: 1-2)
+ *   BATMAP_K1_STAGE=0|4       staged K1 pack off / byte tier also at 4 items per CTA (default: 1-2)
  *   BATMAP_K2_TN=64|128       K2 tile width (default: the planner's cost model)
  *   BATMAP_K2_PROMOTE=0, BATMAP_K2_VIRTUAL=0, BATMAP_K2_SPLIT=0        planner features off
  *   BATMAP_K2_SPLITF=f        split-K granularity (default 4); BATMAP_K2_ACCTAIL=0: no finer tail cut

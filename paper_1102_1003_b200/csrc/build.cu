@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(NT) k1_conc_cluster(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ tids, const int32_t* __restrict__ pos2orig,
     int64_t first, uint32_t r, int log2r, PiParams P, uint32_t r0, int log2r0, uint32_t max_loop_opt,
     uint32_t* __restrict__ arena_cls, int n_pad, uint64_t* __restrict__ fails, unsigned long long* __restrict__ fail_ctr,
-    int64_t fail_cap) {
+    int64_t fail_cap, uint32_t* __restrict__ stage) {
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) uint32_t T[];  // this CTA's slice: 3r / CS entries
     __shared__ uint32_t fl[kConcFailCap];
@@ -463,8 +463,14 @@ __global__ void __launch_bounds__(NT) k1_conc_cluster(
     if (CS > 1) cl.sync();
     else __syncthreads();
     const uint32_t q0 = rank * slice;
-    for (uint32_t wl = threadIdx.x; wl < slice / 4; wl += NT)
-        arena_cls[(int64_t)(q0 / 4 + wl) * n_pad + c] = pack_tagged(reinterpret_cast<const uint4*>(T)[wl]);
+    if (CS == 1 && stage) {  // the item's words as one contiguous row of the staging block (coalesced;
+                             // k_pack_transpose writes the arena), as the byte tier does
+        for (uint32_t wl = threadIdx.x; wl < slice / 4; wl += NT)
+            stage[(int64_t)c * (slice / 4) + wl] = pack_tagged(reinterpret_cast<const uint4*>(T)[wl]);
+    } else {
+        for (uint32_t wl = threadIdx.x; wl < slice / 4; wl += NT)
+            arena_cls[(int64_t)(q0 / 4 + wl) * n_pad + c] = pack_tagged(reinterpret_cast<const uint4*>(T)[wl]);
+    }
     if (CS > 1) cl.sync();  // no CTA may exit while another still reads its slice
 }
 
@@ -1225,12 +1231,29 @@ static batmap_status launch_cluster(const ClassInfo& c, batmap_collection* h, co
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    BM_CUDA(cudaLaunchKernelEx(&cfg, k1_conc_cluster<CS, NT>, offsets, tids, (const int32_t*)h->pos2orig_d,
-                               (int64_t)c.first, (uint32_t)c.r, ilog2_u64((uint64_t)c.r), h->pi, (uint32_t)h->r0,
-                               h->log2r0, h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, fails, fail_ctr,
-                               fail_cap));
-    h->launches += 1;
-    return BATMAP_OK;
+    // one item per CTA: staged pack as in the byte tier (BATMAP_K1_STAGE=0: direct)
+    uint32_t* stage = nullptr;
+    const char* se = getenv("BATMAP_K1_STAGE");
+    if (CS == 1 && !(se && se[0] == '0') && c.n >= 64 && dalloc_t(&stage, (int64_t)c.n * c.W, st) != BATMAP_OK) {
+        stage = nullptr;  // no room for the staging block: pack directly
+        cudaGetLastError();
+    }
+    const batmap_status rc = [&]() -> batmap_status {
+        BM_CUDA(cudaLaunchKernelEx(&cfg, k1_conc_cluster<CS, NT>, offsets, tids, (const int32_t*)h->pos2orig_d,
+                                   (int64_t)c.first, (uint32_t)c.r, ilog2_u64((uint64_t)c.r), h->pi, (uint32_t)h->r0,
+                                   h->log2r0, h->max_loop_opt, h->arena_d + c.word_off, c.n_pad, fails, fail_ctr,
+                                   fail_cap, stage));
+        h->launches += 1;
+        if (stage) {
+            const dim3 grid((unsigned)((c.n + 31) / 32), (unsigned)((c.W + 31) / 32));  // x: items, y: words
+            k_pack_transpose<<<grid, 256, 0, st>>>(stage, (int)c.n, (uint32_t)c.W, h->arena_d + c.word_off, c.n_pad);
+            BM_CUDA(cudaGetLastError());
+            h->launches += 1;
+        }
+        return BATMAP_OK;
+    }();
+    if (stage) dfree(stage, st);
+    return rc;
 }
 
 // cluster size: enough CTAs that each holds at most 192 KB of the item's 12r-byte table
