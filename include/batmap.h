@@ -58,7 +58,7 @@ typedef struct batmap_collection* batmap_handle; /* library-owned; free with bat
  *   BATMAP_K2_GROUP=g         tile rows per band of large rectangles (default: ~32 MB bands)
  *   BATMAP_K2_BALANCE=0       K2's balanced mode for ragged / diagonal tiles off
  *   BATMAP_K3_GROUPED=0       the one-warp-per-candidate triple kernel instead of the grouped one
- *   BATMAP_AB_CAP=n           force the A_b re-run path;  BATMAP_TRACE=1: host phase timestamps (stderr)
+ *   BATMAP_AB_CAP=n           force the A_b re-run path;  BATMAP_TRACE=1|2: host phase / plan-upload timestamps (stderr)
  */
 
 /* Build flags */

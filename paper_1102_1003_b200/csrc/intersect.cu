@@ -20,6 +20,9 @@
 // rectangles add their partial counts to global counters, thresholded by k2_acc_threshold.
 #include <cudaTypedefs.h>
 
+#include <chrono>
+#include <cstdio>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -1024,7 +1027,26 @@ void plan_k2_host(const std::vector<ClassInfo>& classes, int num_sms, int part, 
 }
 
 // Device half: scratch copies, tensor maps, and the plan's upload.
+namespace {
+struct MTrace {  // BATMAP_TRACE=2: timestamps inside the plan upload (diagnostics)
+    bool on;
+    std::chrono::steady_clock::time_point last;
+    MTrace() {
+        const char* e = getenv("BATMAP_TRACE");
+        on = e && e[0] == '2';
+        last = std::chrono::steady_clock::now();
+    }
+    void mark(const char* w) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[batmap upload] %-22s +%9.3f ms\n", w, std::chrono::duration<double, std::milli>(now - last).count());
+        last = now;
+    }
+};
+}  // namespace
+
 static batmap_status materialize_k2(batmap_collection* h, const Selection& sel, cudaStream_t st, K2Prepared* kp) {
+    MTrace mt;
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) {
         set_error("cuTensorMapEncodeTiled unavailable");
@@ -1034,6 +1056,7 @@ static batmap_status materialize_k2(batmap_collection* h, const Selection& sel, 
     const int C = (int)pl.eff.size();
     if (pl.work.empty()) return BATMAP_OK;
     if (pl.virt_words) BM_TRY(dalloc_t(&kp->virt_d, pl.virt_words, st));
+    mt.mark("virt alloc");
     if (pl.promo_words) {
         for (const PromoCopy& pc : pl.promo)
             if (pc.cls_hi - pc.cls_lo + 1 > kMaxPromoMembers) {
@@ -1048,6 +1071,7 @@ static batmap_status materialize_k2(batmap_collection* h, const Selection& sel, 
         BM_CUDA(cudaMemcpyAsync(kp->lw_d, lw.data(), lw.size(), cudaMemcpyHostToDevice, st));
         BM_CUDA(cudaStreamSynchronize(st));  // lw is a host temporary
     }
+    mt.mark("promo");
     kp->prm = new K2Maps();
     for (int a = 0; a < C; ++a) {  // row role (box 128 items) and column role (box tn items)
         const uint32_t* base = pl.eff_promo[a] >= 0 ? kp->promo_d : sel.arena;
@@ -1057,6 +1081,7 @@ static batmap_status materialize_k2(batmap_collection* h, const Selection& sel, 
     for (size_t k = 0; k < pl.virt.size(); ++k)
         BM_TRY(encode_map(enc, &kp->prm->b[C + k], kp->virt_d + pl.virt[k].dst_word_off, pl.virt[k].vpad,
                           pl.virt[k].W_a, kp->tn));
+    mt.mark("tensor maps");
     BM_TRY(dalloc_t(&kp->rects_d, (int64_t)pl.rects.size(), st));
     BM_TRY(dalloc_t(&kp->work_d, (int64_t)pl.work.size(), st));
     BM_TRY(dalloc_t(&kp->units_d, (int64_t)std::max<size_t>(pl.units.size(), 1), st));
@@ -1074,7 +1099,9 @@ static batmap_status materialize_k2(batmap_collection* h, const Selection& sel, 
                        {kp->tails_d, pl.tails.data(), pl.tails.size() * sizeof(TailTile)}};
     size_t total = 0;
     for (const Up& u : ups) total += (u.bytes + 15) / 16 * 16;
+    mt.mark("plan allocs");
     char* pin = static_cast<char*>(host_staging(total, 1));
+    mt.mark("staging");
     size_t at = 0;
     for (const Up& u : ups) {
         if (!u.bytes) continue;
@@ -1086,6 +1113,7 @@ static batmap_status materialize_k2(batmap_collection* h, const Selection& sel, 
         }
         BM_CUDA(cudaMemcpyAsync(u.dst, from, u.bytes, cudaMemcpyHostToDevice, st));
     }
+    mt.mark("copies queued");
     return BATMAP_OK;
 }
 
